@@ -1,0 +1,606 @@
+"""Python mirror of the reference's `dopf` C++ API for the ADMM hot path.
+
+Names, argument meaning and error behaviour follow the reference headers:
+  parse_feeder / parse_feeder_file / validate_feeder / serialize_feeder
+      proj/include/dopf/feeder.hpp:112-124
+  assemble_centralized                  proj/include/dopf/lp_builder.hpp:57
+  decompose / partition / reduce_subsystems
+      proj/include/dopf/decompose.hpp:84-91
+  Settings, precompute, solve, SolveResult, TraceRow, write_trace_csv,
+  write_solution                        proj/include/dopf/admm.hpp:14-133
+`solve` runs the iteration on the GPU (sm_100a kernels behind
+include/dopf_cuda.h); there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _native as N
+
+# ---------------------------------------------------------------- errors
+
+
+class ParseError(RuntimeError):
+    pass
+
+
+class SingularSubsystemError(RuntimeError):
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        # "numerically singular subsystem '<id>'"
+        self.subsystem_id = msg.split("'")[1] if "'" in msg else ""
+
+
+class InfeasibleSubsystemError(RuntimeError):
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        self.subsystem_id = msg.split("'")[1] if "'" in msg else ""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(code: int, msg: str):
+    if code == 0:
+        return
+    if code == 1:
+        raise ValueError(msg)          # std::invalid_argument
+    if code == 2:
+        raise SingularSubsystemError(msg)
+    if code in (3, 4):
+        raise CudaError(msg)
+    if code == 5:
+        raise MemoryError(msg)
+    if code == 6:
+        raise ParseError(msg)
+    if code == 7:
+        raise InfeasibleSubsystemError(msg)
+    if code == 8:
+        raise AssertionError(msg)      # std::logic_error
+    raise RuntimeError(msg)
+
+
+def _check(code: int):
+    if code != 0:
+        _raise(code, N.last_error())
+
+
+# ---------------------------------------------------------------- feeder
+
+
+@dataclass
+class Diagnostic:
+    severity: str
+    component: str
+    message: str
+
+
+class Feeder:
+    """Owning handle of a parsed, id-sorted feeder (reference Feeder)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.host().dopf_feeder_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def counts(self) -> dict:
+        out = (N.i32 * 5)()
+        _check(N.host().dopf_feeder_counts(self._h, out))
+        return {"buses": out[0], "generators": out[1], "lines": out[2], "loads": out[3],
+                "leaves": out[4]}
+
+    def serialize(self) -> str:
+        rc, text = N.text_call(N.host().dopf_feeder_serialize, self._h)
+        _check(rc)
+        return text
+
+
+def _new_feeder(fn, *args) -> Feeder:
+    h = C.c_void_p()
+    _check(fn(*args, C.byref(h)))
+    return Feeder(h.value)
+
+
+def parse_feeder(text: str) -> Feeder:
+    raw = text.encode()
+    return _new_feeder(N.host().dopf_feeder_parse, raw, len(raw))
+
+
+def parse_feeder_file(path: str) -> Feeder:
+    return _new_feeder(N.host().dopf_feeder_parse_file, str(path).encode())
+
+
+def synthetic_feeder(shape: str, seed: int) -> Feeder:
+    """Seeded feeder with the paper's structural counts ("ieee13"/"ieee123"/"ieee8500")."""
+    return _new_feeder(N.host().dopf_feeder_synthetic, shape.encode(), seed)
+
+
+def tiled_feeder(shape: str, copies: int, seed: int) -> Feeder:
+    return _new_feeder(N.host().dopf_feeder_synthetic_tiled, shape.encode(), copies, seed)
+
+
+def scale_loads(base: Feeder, seed: int) -> Feeder:
+    return _new_feeder(N.host().dopf_feeder_scale_loads, base.handle, seed)
+
+
+def serialize_feeder(f: Feeder) -> str:
+    return f.serialize()
+
+
+def validate_feeder(f: Feeder) -> List[Diagnostic]:
+    n_err = N.i32(0)
+    need = N.sz(0)
+    lib = N.host()
+    _check(lib.dopf_feeder_validate(f.handle, None, 0, C.byref(need), C.byref(n_err)))
+    buf = C.create_string_buffer(need.value)
+    _check(lib.dopf_feeder_validate(f.handle, buf, need.value, C.byref(need), C.byref(n_err)))
+    diags = []
+    for line in buf.value.decode().splitlines():
+        sev, comp, msg = line.split("\t", 2)
+        diags.append(Diagnostic(sev, comp, msg))
+    return diags
+
+
+def has_errors(diags: List[Diagnostic]) -> bool:
+    return any(d.severity == "error" for d in diags)
+
+
+# ---------------------------------------------------------------- LP
+
+
+VAR_KINDS = ["p_gen", "q_gen", "w", "p_bus_load", "q_bus_load", "p_load", "q_load", "p_flow",
+             "q_flow"]
+
+
+class LinearSystem:
+    """Centralized LP min c'x, Ax=b, lo<=x<=hi (reference LinearSystem)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        v = N.LpView_t()
+        _check(N.host().dopf_lp_view_get(self._h, C.byref(v)))
+        self._v = v
+        self.rows, self.cols, self.nnz = v.rows, v.cols, v.nnz
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.host().dopf_lp_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def view(self) -> N.LpView_t:
+        return self._v
+
+    def _arr(self, ptr, n):
+        return np.ctypeslib.as_array(ptr, shape=(n,)).copy() if n else np.zeros(0)
+
+    @property
+    def row_ptr(self):
+        return self._arr(self._v.row_ptr, self.rows + 1)
+
+    @property
+    def col_idx(self):
+        return self._arr(self._v.col_idx, self.nnz)
+
+    @property
+    def values(self):
+        return self._arr(self._v.values, self.nnz)
+
+    @property
+    def b(self):
+        return self._arr(self._v.b, self.rows)
+
+    @property
+    def c(self):
+        return self._arr(self._v.c, self.cols)
+
+    @property
+    def x_lo(self):
+        return self._arr(self._v.x_lo, self.cols)
+
+    @property
+    def x_hi(self):
+        return self._arr(self._v.x_hi, self.cols)
+
+    @property
+    def var_kind(self):
+        return self._arr(self._v.var_kind, self.cols)
+
+    def dense(self) -> np.ndarray:
+        a = np.zeros((self.rows, self.cols))
+        rp, ci, vals = self.row_ptr, self.col_idx, self.values
+        for i in range(self.rows):
+            a[i, ci[rp[i]:rp[i + 1]]] = vals[rp[i]:rp[i + 1]]
+        return a
+
+    def var_key(self, col: int) -> str:
+        buf = C.create_string_buffer(512)
+        _check(N.host().dopf_lp_var_key(self._h, col, buf, 512))
+        return buf.value.decode()
+
+    def row_tag(self, row: int) -> str:
+        buf = C.create_string_buffer(512)
+        _check(N.host().dopf_lp_row_tag(self._h, row, buf, 512))
+        return buf.value.decode()
+
+    def var_table(self) -> List[str]:
+        return [self.var_key(j) for j in range(self.cols)]
+
+    def column(self, key: str) -> int:
+        for j in range(self.cols):
+            if self.var_key(j) == key:
+                return j
+        raise KeyError(key)
+
+    def dump(self) -> str:
+        rc, text = N.text_call(N.host().dopf_lp_dump, self._h)
+        _check(rc)
+        return text
+
+
+def assemble_centralized(f: Feeder) -> LinearSystem:
+    h = C.c_void_p()
+    _check(N.host().dopf_lp_assemble(f.handle, C.byref(h)))
+    return LinearSystem(h.value)
+
+
+# ---------------------------------------------------------------- decomposed model
+
+
+@dataclass
+class Settings:
+    rho: float = 100.0
+    eps_rel: float = 1e-3
+    max_iter: int = 50000
+    workers: int = 1
+    record_iterates: bool = False
+
+    def to_c(self) -> N.Settings_t:
+        return N.Settings_t(float(self.rho), float(self.eps_rel), int(self.max_iter),
+                            int(self.workers), int(bool(self.record_iterates)), 0)
+
+
+class DecomposedModel:
+    """Decomposed model + (after precompute) the per-subsystem operators."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        self._view: Optional[N.ModelView_t] = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.host().dopf_model_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def view(self) -> N.ModelView_t:
+        if self._view is None:
+            v = N.ModelView_t()
+            _check(N.host().dopf_model_view_get(self._h, C.byref(v)))
+            self._view = v
+        return self._view
+
+    def precompute(self, workers: int = 1) -> "DecomposedModel":
+        """One-time operators P_s, v_s (reference admm.cpp:31-88)."""
+        _check(N.host().dopf_model_precompute(self._h, workers))
+        self._view = None
+        return self
+
+    def reduce(self, tol: float = 1e-9, workers: int = 1) -> None:
+        _check(N.host().dopf_model_reduce(self._h, tol, workers))
+        self._view = None
+
+    @property
+    def has_precompute(self) -> bool:
+        return bool(self.view().has_pre)
+
+    @property
+    def S(self) -> int:
+        return self.view().S
+
+    @property
+    def global_cols(self) -> int:
+        return self.view().n
+
+    @property
+    def total_local_vars(self) -> int:
+        return self.view().N_z
+
+    def arr(self, name: str) -> np.ndarray:
+        v = self.view()
+        S, n, Nz = v.S, v.n, v.N_z
+        sizes = {"z_offsets": S + 1, "l2g": Nz, "m_s": S, "a_offsets": S + 1,
+                 "b_offsets": S + 1, "p_offsets": S + 1, "v": Nz, "inv_copy": n,
+                 "csr_ptr": n + 1, "csr_copy": Nz, "c": n, "x_lo": n, "x_hi": n, "x0": n,
+                 "z0": Nz}
+        if name == "A":
+            size = int(self.arr("a_offsets")[-1])
+        elif name == "b":
+            size = int(self.arr("b_offsets")[-1])
+        elif name == "P":
+            size = int(self.arr("p_offsets")[-1])
+        else:
+            size = sizes[name]
+        ptr = getattr(v, name)
+        if not ptr or size == 0:
+            return np.zeros(size)
+        return np.ctypeslib.as_array(ptr, shape=(size,)).copy()
+
+    @property
+    def z_offsets(self):
+        return self.arr("z_offsets")
+
+    @property
+    def copy_counts(self):
+        return np.diff(self.arr("csr_ptr")) if self.has_precompute else \
+            np.bincount(self.arr("l2g"), minlength=self.global_cols)
+
+    def subsystem(self, s: int) -> dict:
+        zo = self.arr("z_offsets")
+        ao = self.arr("a_offsets")
+        bo = self.arr("b_offsets")
+        ns = int(zo[s + 1] - zo[s])
+        ms = int(self.arr("m_s")[s])
+        out = {"component_id": self.component_id(s),
+               "A": self.arr("A")[ao[s]:ao[s + 1]].reshape(ms, ns),
+               "b": self.arr("b")[bo[s]:bo[s + 1]],
+               "local_to_global": self.arr("l2g")[zo[s]:zo[s + 1]]}
+        if self.has_precompute:
+            po = self.arr("p_offsets")
+            out["P"] = self.arr("P")[po[s]:po[s + 1]].reshape(ns, ns)
+            out["v"] = self.arr("v")[zo[s]:zo[s + 1]]
+        return out
+
+    def component_id(self, s: int) -> str:
+        buf = C.create_string_buffer(1024)
+        _check(N.host().dopf_model_component_id(self._h, s, buf, 1024))
+        return buf.value.decode()
+
+    def rows_before_reduction(self) -> np.ndarray:
+        out = (N.i32 * max(1, self.S))()
+        _check(N.host().dopf_model_rows_before_reduction(self._h, out))
+        return np.array(out[:self.S], dtype=np.int32)
+
+    def dump_subsystems(self) -> str:
+        rc, text = N.text_call(N.host().dopf_model_dump_subsystems, self._h)
+        _check(rc)
+        return text
+
+    def stats(self) -> dict:
+        zo = self.arr("z_offsets")
+        ns = np.diff(zo)
+        ms = self.arr("m_s")
+        return {"S": int(self.S), "n": int(self.global_cols), "N_z": int(zo[-1]),
+                "sum_m": int(ms.sum()), "sum_n2": int((ns.astype(np.int64) ** 2).sum()),
+                "sum_mn": int((ms.astype(np.int64) * ns).sum()),
+                "m_mean": float(ms.mean()) if len(ms) else 0.0,
+                "m_max": int(ms.max()) if len(ms) else 0,
+                "n_mean": float(ns.mean()) if len(ns) else 0.0,
+                "n_max": int(ns.max()) if len(ns) else 0,
+                "n_min": int(ns.min()) if len(ns) else 0,
+                "n_std": float(ns.std()) if len(ns) else 0.0,
+                "m_std": float(ms.std()) if len(ms) else 0.0}
+
+
+def decompose(ls: LinearSystem, f: Feeder, tol: float = 1e-9, workers: int = 1) -> DecomposedModel:
+    h = C.c_void_p()
+    _check(N.host().dopf_model_decompose(ls.handle, f.handle, tol, workers, C.byref(h)))
+    return DecomposedModel(h.value)
+
+
+def partition(ls: LinearSystem, f: Feeder) -> DecomposedModel:
+    h = C.c_void_p()
+    _check(N.host().dopf_model_partition(ls.handle, f.handle, C.byref(h)))
+    return DecomposedModel(h.value)
+
+
+def model_from_arrays(subsystems, c, x_lo, x_hi, is_w=None) -> DecomposedModel:
+    """Build a model from dense subsystem data.
+
+    subsystems: list of (A (m x n_s), b (m), local_to_global (n_s)).
+    Mirrors test_util.hpp:52-74 (single_sub_model) and the hand-built
+    multi-copy models of test_admm.cpp:113-173.
+    """
+    n = len(c)
+    z_off = [0]
+    l2g, ms, A, b = [], [], [], []
+    for (a, bb, cols) in subsystems:
+        a = np.asarray(a, dtype=np.float64).reshape(len(bb), len(cols))
+        z_off.append(z_off[-1] + len(cols))
+        l2g += list(cols)
+        ms.append(a.shape[0])
+        A += list(a.reshape(-1))
+        b += list(np.asarray(bb, dtype=np.float64))
+
+    def arr(t, xs):
+        xs = list(xs)
+        return (t * max(1, len(xs)))(*xs)
+
+    isw = arr(N.i32, [int(v) for v in (is_w if is_w is not None else [0] * n)])
+    h = C.c_void_p()
+    _check(N.host().dopf_model_from_arrays(
+        len(subsystems), n, arr(N.i32, z_off), arr(N.i32, l2g), arr(N.i32, ms), arr(N.f64, A),
+        arr(N.f64, b), arr(N.f64, c), arr(N.f64, x_lo), arr(N.f64, x_hi), isw, C.byref(h)))
+    return DecomposedModel(h.value)
+
+
+def single_sub_model(a, b, c, lo, hi) -> DecomposedModel:
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[1]
+    return model_from_arrays([(a, b, list(range(n)))], c, lo, hi)
+
+
+# ---------------------------------------------------------------- results + solve
+
+
+CONVERGED, ITERATION_LIMIT = 0, 1
+
+
+@dataclass
+class TraceRow:
+    t: int
+    pres: float
+    dres: float
+    eps_prim: float
+    eps_dual: float
+    objective: float
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    z: np.ndarray
+    lam: np.ndarray
+    status: int
+    iterations: int
+    objective: float
+    max_local_infeasibility: float
+    trace: np.ndarray            # (iterations, 6): t, pres, dres, eps_prim, eps_dual, objective
+    timings: dict = field(default_factory=dict)
+
+    @property
+    def converged(self) -> bool:
+        return self.status == CONVERGED
+
+    def trace_rows(self) -> List[TraceRow]:
+        return [TraceRow(int(r[0]), *map(float, r[1:])) for r in self.trace]
+
+
+def _check_settings(settings: Settings):
+    # reference admm.cpp:173-175
+    if not settings.rho > 0:
+        raise ValueError("rho must be positive")
+    if not settings.eps_rel > 0:
+        raise ValueError("eps_rel must be positive")
+    if settings.max_iter < 1:
+        raise ValueError("max_iter must be positive")
+
+
+class CudaSolver:
+    """One device context: uploads a model once, solves many times."""
+
+    def __init__(self, device: int = 0):
+        lib = N.cuda()
+        h = C.c_void_p()
+        rc = lib.dopf_cuda_create(device, C.byref(h))
+        if rc != 0:
+            _raise(rc, "dopf_cuda_create failed: " + (N.last_error() or "no CUDA device"))
+        self._h = h
+        self._lib = lib
+        self.model: Optional[DecomposedModel] = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.dopf_cuda_destroy(h)
+            self._h = None
+
+    def _err(self, rc):
+        if rc != 0:
+            msg = self._lib.dopf_cuda_last_error(self._h)
+            _raise(rc, msg.decode() if msg else "CUDA solver error")
+
+    def upload(self, model: DecomposedModel) -> None:
+        if not model.has_precompute:
+            model.precompute()
+        self._err(self._lib.dopf_cuda_upload(self._h, C.byref(model.view())))
+        self.model = model
+
+    def info(self) -> dict:
+        i = N.BatchInfo_t()
+        self._err(self._lib.dopf_cuda_info(self._h, C.byref(i)))
+        return {"instances": i.instances, "blocks": i.blocks, "threads": i.threads,
+                "smem_bytes": i.smem_bytes, "resident": bool(i.resident)}
+
+    def kernel_launches(self) -> int:
+        return int(self._lib.dopf_cuda_kernel_launches(self._h))
+
+    def bytes_per_iteration(self) -> float:
+        return float(self._lib.dopf_cuda_bytes_per_iteration(self._h))
+
+    def solve(self, settings: Settings, outputs: bool = True) -> SolveResult:
+        _check_settings(settings)
+        v = self.model.view()
+        n, Nz = v.n, v.N_z
+        x = np.zeros(n)
+        z = np.zeros(Nz)
+        lam = np.zeros(Nz)
+        trace = np.zeros((settings.max_iter, 6))
+        r = N.ResultView_t()
+        if outputs:
+            r.x = x.ctypes.data_as(C.POINTER(C.c_double))
+            r.z = z.ctypes.data_as(C.POINTER(C.c_double))
+            r.lambda_ = lam.ctypes.data_as(C.POINTER(C.c_double))
+        r.trace = trace.ctypes.data_as(C.POINTER(C.c_double))
+        st = settings.to_c()
+        self._err(self._lib.dopf_cuda_solve(self._h, C.byref(st), C.byref(r)))
+        it = r.iterations
+        return SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
+                           trace[:it].copy(),
+                           {"solve": r.time_solve, "upload": r.time_upload,
+                            "download": r.time_download, "global": r.time_global,
+                            "local": r.time_local, "dual": r.time_dual})
+
+
+def solve(model: DecomposedModel, settings: Settings = Settings(), device: int = 0) -> SolveResult:
+    """Drop-in for dopf::solve (admm.hpp:126): precompute (host) + GPU iteration."""
+    _check_settings(settings)
+    import time
+    t0 = time.perf_counter()
+    if not model.has_precompute:
+        model.precompute(max(1, settings.workers))
+    t_pre = time.perf_counter() - t0
+    solver = CudaSolver(device)
+    solver.upload(model)
+    res = solver.solve(settings)
+    res.timings["precompute"] = t_pre
+    return res
+
+
+def write_trace_csv(trace: np.ndarray) -> str:
+    t = np.ascontiguousarray(trace, dtype=np.float64).reshape(-1, 6)
+    rc, text = N.text_call(N.host().dopf_write_trace_csv,
+                           t.ctypes.data_as(C.POINTER(C.c_double)), t.shape[0])
+    _check(rc)
+    return text
+
+
+def write_solution(ls: LinearSystem, x: np.ndarray) -> str:
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    rc, text = N.text_call(N.host().dopf_write_solution, ls.handle,
+                           xs.ctypes.data_as(C.POINTER(C.c_double)))
+    _check(rc)
+    return text
+
+
+def load_model(path_or_feeder, workers: int = 1, tol: float = 1e-9):
+    """parse -> validate -> assemble -> decompose (the CLI's solve pipeline)."""
+    f = path_or_feeder if isinstance(path_or_feeder, Feeder) else parse_feeder_file(path_or_feeder)
+    diags = validate_feeder(f)
+    if has_errors(diags):
+        raise ValueError("feeder fails validation: " + "; ".join(d.message for d in diags))
+    ls = assemble_centralized(f)
+    model = decompose(ls, f, tol, workers)
+    return f, ls, model
