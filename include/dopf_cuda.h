@@ -1,0 +1,76 @@
+/* Drop-in C ABI of the B200 ADMM solver: the replacement for the reference's
+ * solver entry point
+ *
+ *     SolveResult dopf::solve(const DecomposedModel&, const Settings&)
+ *         proj/include/dopf/admm.hpp:126, proj/src/admm.cpp:172-244
+ *
+ * split into create / upload / solve / destroy so a model is uploaded once
+ * and solved many times (scenario batches, warm benchmarks):
+ *
+ *   dopf_cuda_create   -- context on one device (streams, buffers)
+ *   dopf_cuda_upload   -- model + precomputed operators (admm.cpp:31-88 output)
+ *                         -> device layout in HBM (row-blocked, column-major
+ *                         per-subsystem P and A, CSR-by-column copy lists)
+ *   dopf_cuda_solve    -- settings validation (admm.cpp:173-175, code 1 =
+ *                         std::invalid_argument), the whole iteration loop on
+ *                         the device, results copied into caller buffers in
+ *                         the reference's layout (x by global column, z and
+ *                         lambda stacked by z_offsets)
+ *   dopf_cuda_last_error / dopf_cuda_destroy
+ *
+ * Status codes are dopf_status (dopf_types.h). iteration_limit is a result
+ * status (dopf_result_view.status), not an error, as in the reference.
+ * A context is not thread-safe; use one per thread/device.
+ */
+#ifndef DOPF_CUDA_H
+#define DOPF_CUDA_H
+
+#include "dopf_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dopf_cuda_ctx dopf_cuda_ctx;
+
+typedef struct dopf_cuda_info_t {
+  int32_t instances;   /* uploaded models                         */
+  int32_t blocks;      /* CTAs per instance                       */
+  int32_t threads;     /* threads per CTA                         */
+  int32_t smem_bytes;  /* dynamic shared memory per CTA           */
+  int32_t resident;    /* 1: all operators staged in shared memory */
+  int32_t sync_mode;   /* 0 block, 1 cluster, 2 grid barrier      */
+} dopf_cuda_info_t;
+
+int dopf_cuda_create(int device, dopf_cuda_ctx** out);
+int dopf_cuda_upload(dopf_cuda_ctx* ctx, const dopf_model_view* model);
+int dopf_cuda_solve(dopf_cuda_ctx* ctx, const dopf_settings* settings, dopf_result_view* result);
+/* Same loop, outputs left on the device (only scalars and, if result->trace
+ * is non-NULL, the trace are copied back). Used to time the kernel alone. */
+int dopf_cuda_solve_device(dopf_cuda_ctx* ctx, const dopf_settings* settings,
+                           dopf_result_view* result);
+const char* dopf_cuda_last_error(const dopf_cuda_ctx* ctx);
+void dopf_cuda_destroy(dopf_cuda_ctx* ctx);
+
+/* Independent scenarios of identical structure (BASELINE config 5): one
+ * cluster of CTAs per scenario, per-scenario convergence (a converged
+ * scenario stops, the others continue). results[i] receives scenario i. */
+int dopf_cuda_upload_batch(dopf_cuda_ctx* ctx, const dopf_model_view* models, int32_t count);
+int dopf_cuda_solve_batch(dopf_cuda_ctx* ctx, const dopf_settings* settings,
+                          dopf_result_view* results, int32_t count);
+
+int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
+/* Number of kernels this context launched so far (evidence for benchmarks). */
+int64_t dopf_cuda_kernel_launches(const dopf_cuda_ctx* ctx);
+/* Algorithmic HBM bytes of one iteration, summed over uploaded instances
+ * (BASELINE.md section 3 formula). */
+double dopf_cuda_bytes_per_iteration(const dopf_cuda_ctx* ctx);
+/* Device time (seconds) of the last solve's kernel, CUDA events on the
+ * launching stream. */
+double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DOPF_CUDA_H */

@@ -1,0 +1,67 @@
+"""Independent load scenarios solved together (BASELINE config 5).
+
+Each scenario is an independent reference `solve` (own iteration count and
+trace, admm.cpp:172-244); on the device each runs on its own cluster of CTAs
+and stops at its own convergence iteration.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List
+
+import numpy as np
+
+from . import _native as N
+from . import dopf
+
+
+class BatchSolver:
+    def __init__(self, device: int = 0):
+        self._s = dopf.CudaSolver(device)
+        self.models: List[dopf.DecomposedModel] = []
+
+    def upload(self, models: List[dopf.DecomposedModel]) -> None:
+        for m in models:
+            if not m.has_precompute:
+                m.precompute()
+        views = (N.ModelView_t * len(models))(*[m.view() for m in models])
+        self._s._err(self._s._lib.dopf_cuda_upload_batch(self._s._h, views, len(models)))
+        self.models = list(models)
+        self._views = views
+
+    def info(self) -> dict:
+        return self._s.info()
+
+    def kernel_launches(self) -> int:
+        return self._s.kernel_launches()
+
+    def bytes_per_iteration(self) -> float:
+        return self._s.bytes_per_iteration()
+
+    def solve(self, settings: dopf.Settings, outputs: bool = True, trace: bool = True):
+        dopf._check_settings(settings)
+        k = len(self.models)
+        rs = (N.ResultView_t * k)()
+        bufs = []
+        for i, m in enumerate(self.models):
+            v = m.view()
+            x, z, lam = np.zeros(v.n), np.zeros(v.N_z), np.zeros(v.N_z)
+            tr = np.zeros((settings.max_iter, 6)) if trace else None
+            if outputs:
+                rs[i].x = x.ctypes.data_as(C.POINTER(C.c_double))
+                rs[i].z = z.ctypes.data_as(C.POINTER(C.c_double))
+                rs[i].lambda_ = lam.ctypes.data_as(C.POINTER(C.c_double))
+            if trace:
+                rs[i].trace = tr.ctypes.data_as(C.POINTER(C.c_double))
+            bufs.append((x, z, lam, tr))
+        st = settings.to_c()
+        self._s._err(self._s._lib.dopf_cuda_solve_batch(self._s._h, C.byref(st), rs, k))
+        out = []
+        for i in range(k):
+            x, z, lam, tr = bufs[i]
+            it = rs[i].iterations
+            out.append(dopf.SolveResult(x, z, lam, rs[i].status, it, rs[i].objective,
+                                        rs[i].max_local_infeasibility,
+                                        tr[:it].copy() if tr is not None else np.zeros((0, 6)),
+                                        {"solve": rs[i].time_solve}))
+        return out

@@ -1,0 +1,59 @@
+// Launch interface of the persistent ADMM iteration kernel (admm_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "layout.hpp"
+
+namespace dopf::cuda {
+
+enum class SyncMode : int32_t { block = 0, cluster = 1, grid = 2 };
+
+struct KernelParams {
+  const BlockDesc* blocks;
+  const InstDesc* inst;
+  const double* P;
+  const double* A;
+  const int32_t* copies;
+  const RowMeta* rmeta;
+  const double* v;
+  const double* z0;
+  const ColMeta* cmeta;
+  const double* cc;
+  const double* cinv;
+  const double* clo;
+  const double* chi;
+  const AMeta* ameta;
+  const double* ab;
+  double* u;            // [2][rows_total] exchange values u = z - lambda/rho
+  double* z_out;        // [rows_total]
+  double* lam_out;      // [rows_total]
+  double* x_out;        // [x_total]
+  double* part;         // [instances][2][blocks_per_instance][kPartials]
+  unsigned int* bar;    // [instances] grid-barrier counters (grid mode)
+  double* trace;        // [instances][trace_stride][6] (may be null)
+  int32_t* iters;       // [instances]
+  int32_t* status;      // [instances] 0 converged, 1 iteration limit
+  double* maxinf;       // [instances]
+  double* objective;    // [instances]
+  double rho;
+  double eps_rel;
+  int64_t rows_total;
+  int64_t trace_stride; // rows per instance in `trace`
+  int32_t max_iter;
+  int32_t blocks_per_instance;
+  int32_t sync_mode;    // SyncMode
+  int32_t pad;
+};
+
+/// Launches the persistent kernel: one CTA per block descriptor, all
+/// iterations on device until every instance converged or hit max_iter.
+cudaError_t launch_admm(const KernelParams& p, int num_blocks, int K, std::size_t smem_bytes,
+                        SyncMode mode, int cluster_size, cudaStream_t stream);
+
+/// Largest dynamic shared memory the kernel may use on this device.
+int max_dynamic_smem(int device);
+
+}  // namespace dopf::cuda

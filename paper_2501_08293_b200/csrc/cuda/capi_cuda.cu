@@ -1,0 +1,421 @@
+// Drop-in C ABI (include/dopf_cuda.h) over the persistent ADMM kernel.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/dopf_cuda.h"
+#include "admm_kernels.cuh"
+#include "layout_builder.hpp"
+
+using namespace dopf::cuda;
+
+namespace {
+
+struct CudaFailure : std::runtime_error {
+  cudaError_t code;
+  CudaFailure(cudaError_t c, const std::string& what)
+      : std::runtime_error(what + ": " + cudaGetErrorString(c)), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure(e, what);
+}
+
+}  // namespace
+
+struct dopf_cuda_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+
+  HostLayout L;
+  bool uploaded = false;
+  SyncMode mode = SyncMode::block;
+  int cluster = 1;
+  int num_blocks = 0;
+  std::vector<int32_t> inst_nz, inst_n;
+
+  std::vector<void*> allocs;  // model-lifetime device buffers
+  BlockDesc* d_blocks = nullptr;
+  InstDesc* d_inst = nullptr;
+  double *d_P = nullptr, *d_A = nullptr, *d_v = nullptr, *d_z0 = nullptr;
+  int32_t* d_copies = nullptr;
+  RowMeta* d_rmeta = nullptr;
+  ColMeta* d_cmeta = nullptr;
+  double *d_cc = nullptr, *d_cinv = nullptr, *d_clo = nullptr, *d_chi = nullptr;
+  AMeta* d_ameta = nullptr;
+  double* d_ab = nullptr;
+  double *d_u = nullptr, *d_z = nullptr, *d_lam = nullptr, *d_x = nullptr, *d_part = nullptr;
+  unsigned int* d_bar = nullptr;
+  int32_t *d_iters = nullptr, *d_status = nullptr;
+  double *d_maxinf = nullptr, *d_obj = nullptr;
+  double* d_trace = nullptr;
+  std::size_t trace_cap = 0;  // doubles
+
+  int64_t launches = 0;
+  double last_kernel_s = 0;
+
+  void free_model() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    if (d_trace) cudaFree(d_trace);
+    d_trace = nullptr;
+    trace_cap = 0;
+    uploaded = false;
+  }
+
+  template <typename T>
+  T* put(const std::vector<T>& h) {
+    void* p = nullptr;
+    const std::size_t bytes = std::max<std::size_t>(sizeof(T), h.size() * sizeof(T));
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    allocs.push_back(p);
+    if (!h.empty()) ck(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, stream), "upload");
+    return static_cast<T*>(p);
+  }
+
+  template <typename T>
+  T* scratch(std::size_t count) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<std::size_t>(1, count) * sizeof(T)), "cudaMalloc");
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+namespace {
+
+int fail(dopf_cuda_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(dopf_cuda_ctx* ctx, F&& body) {
+  try {
+    body();
+    return DOPF_OK;
+  } catch (const CudaFailure& e) {
+    return fail(ctx, e.code == cudaErrorMemoryAllocation ? DOPF_ERR_OUT_OF_MEMORY : DOPF_ERR_CUDA,
+                e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(ctx, DOPF_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, DOPF_ERR_OUT_OF_MEMORY, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(ctx, DOPF_ERR_RUNTIME, e.what());
+  }
+}
+
+void check_settings(const dopf_settings* s) {
+  if (!s) throw std::invalid_argument("null settings");
+  if (!(s->rho > 0)) throw std::invalid_argument("rho must be positive");
+  if (!(s->eps_rel > 0)) throw std::invalid_argument("eps_rel must be positive");
+  if (s->max_iter < 1) throw std::invalid_argument("max_iter must be positive");
+}
+
+void upload_layout(dopf_cuda_ctx* c) {
+  HostLayout& L = c->L;
+  c->d_blocks = c->put(L.blocks);
+  c->d_inst = c->put(L.inst);
+  c->d_P = c->put(L.P);
+  c->d_A = c->put(L.A);
+  c->d_copies = c->put(L.copies);
+  c->d_rmeta = c->put(L.rmeta);
+  c->d_v = c->put(L.v);
+  c->d_z0 = c->put(L.z0);
+  c->d_cmeta = c->put(L.cmeta);
+  c->d_cc = c->put(L.cc);
+  c->d_cinv = c->put(L.cinv);
+  c->d_clo = c->put(L.clo);
+  c->d_chi = c->put(L.chi);
+  c->d_ameta = c->put(L.ameta);
+  c->d_ab = c->put(L.ab);
+  const std::size_t I = L.inst.size();
+  c->d_u = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));
+  c->d_z = c->scratch<double>(L.rows_total);
+  c->d_lam = c->scratch<double>(L.rows_total);
+  c->d_x = c->scratch<double>(L.x_total);
+  c->d_part = c->scratch<double>(I * 2 * L.blocks_per_instance * kPartials);
+  c->d_bar = c->scratch<unsigned int>(I);
+  c->d_iters = c->scratch<int32_t>(I);
+  c->d_status = c->scratch<int32_t>(I);
+  c->d_maxinf = c->scratch<double>(I);
+  c->d_obj = c->scratch<double>(I);
+  ck(cudaStreamSynchronize(c->stream), "upload sync");
+}
+
+void choose_sync(dopf_cuda_ctx* c) {
+  const int G = c->L.blocks_per_instance;
+  c->num_blocks = static_cast<int>(c->L.blocks.size());
+  if (G == 1) {
+    c->mode = SyncMode::block;
+    c->cluster = 1;
+  } else if (G <= 8) {
+    c->mode = SyncMode::cluster;
+    c->cluster = G;
+  } else {
+    if (c->L.inst.size() != 1)
+      throw std::invalid_argument("batched instances must fit a cluster of <= 8 CTAs");
+    if (G > c->sm_count) throw std::invalid_argument("instance needs more CTAs than SMs");
+    c->mode = SyncMode::grid;
+    c->cluster = 1;
+  }
+}
+
+LayoutOptions options_for(const dopf_cuda_ctx* c) {
+  LayoutOptions o;
+  o.smem_limit = static_cast<std::size_t>(c->smem_optin);
+  o.max_blocks = c->sm_count;
+  return o;
+}
+
+void finish_upload(dopf_cuda_ctx* c) {
+  if (c->L.K > kMaxK)
+    throw std::invalid_argument("model too large for the resident kernel (" +
+                                std::to_string(c->L.rows_total) + " rows)");
+  choose_sync(c);
+  upload_layout(c);
+  c->uploaded = true;
+}
+
+// Runs the kernel; copies scalars (and optionally vectors/trace) back.
+void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, int count,
+         bool copy_vectors) {
+  check_settings(s);
+  if (!c->uploaded) throw std::invalid_argument("no model uploaded");
+  HostLayout& L = c->L;
+  const std::size_t I = L.inst.size();
+  if (static_cast<std::size_t>(count) != I) throw std::invalid_argument("result count mismatch");
+  bool want_trace = false;
+  for (int i = 0; i < count; ++i) want_trace = want_trace || results[i].trace;
+  const std::size_t need = want_trace ? I * static_cast<std::size_t>(s->max_iter) * 6 : 0;
+  if (need > c->trace_cap) {
+    if (c->d_trace) cudaFree(c->d_trace);
+    c->d_trace = nullptr;
+    ck(cudaMalloc(&c->d_trace, need * sizeof(double)), "trace alloc");
+    c->trace_cap = need;
+  }
+  const auto t_up0 = std::chrono::steady_clock::now();
+  ck(cudaMemsetAsync(c->d_bar, 0, I * sizeof(unsigned int), c->stream), "memset");
+  ck(cudaMemcpyAsync(c->d_u, c->d_z0, L.rows_total * sizeof(double), cudaMemcpyDeviceToDevice,
+                     c->stream),
+     "u0");
+
+  KernelParams p{};
+  p.blocks = c->d_blocks;
+  p.inst = c->d_inst;
+  p.P = c->d_P;
+  p.A = c->d_A;
+  p.copies = c->d_copies;
+  p.rmeta = c->d_rmeta;
+  p.v = c->d_v;
+  p.z0 = c->d_z0;
+  p.cmeta = c->d_cmeta;
+  p.cc = c->d_cc;
+  p.cinv = c->d_cinv;
+  p.clo = c->d_clo;
+  p.chi = c->d_chi;
+  p.ameta = c->d_ameta;
+  p.ab = c->d_ab;
+  p.u = c->d_u;
+  p.z_out = c->d_z;
+  p.lam_out = c->d_lam;
+  p.x_out = c->d_x;
+  p.part = c->d_part;
+  p.bar = c->d_bar;
+  p.trace = want_trace ? c->d_trace : nullptr;
+  p.iters = c->d_iters;
+  p.status = c->d_status;
+  p.maxinf = c->d_maxinf;
+  p.objective = c->d_obj;
+  p.rho = s->rho;
+  p.eps_rel = s->eps_rel;
+  p.rows_total = L.rows_total;
+  p.trace_stride = s->max_iter;
+  p.max_iter = s->max_iter;
+  p.blocks_per_instance = L.blocks_per_instance;
+  p.sync_mode = static_cast<int32_t>(c->mode);
+
+  ck(cudaEventRecord(c->ev0, c->stream), "event");
+  ck(launch_admm(p, c->num_blocks, L.K, L.smem_bytes, c->mode, c->cluster, c->stream), "launch");
+  ck(cudaEventRecord(c->ev1, c->stream), "event");
+  ++c->launches;
+  ck(cudaEventSynchronize(c->ev1), "kernel");
+  ck(cudaGetLastError(), "kernel");
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "elapsed");
+  c->last_kernel_s = ms * 1e-3;
+  const auto t_dn0 = std::chrono::steady_clock::now();
+
+  std::vector<int32_t> iters(I), status(I);
+  std::vector<double> maxinf(I), obj(I);
+  ck(cudaMemcpy(iters.data(), c->d_iters, I * sizeof(int32_t), cudaMemcpyDeviceToHost), "d2h");
+  ck(cudaMemcpy(status.data(), c->d_status, I * sizeof(int32_t), cudaMemcpyDeviceToHost), "d2h");
+  ck(cudaMemcpy(maxinf.data(), c->d_maxinf, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+  ck(cudaMemcpy(obj.data(), c->d_obj, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+  std::vector<double> zdev, ldev, xall;
+  bool any_vec = false;
+  for (int i = 0; i < count; ++i)
+    any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
+  if (copy_vectors && any_vec) {
+    zdev.resize(L.rows_total);
+    ldev.resize(L.rows_total);
+    xall.resize(L.x_total);
+    ck(cudaMemcpy(zdev.data(), c->d_z, zdev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    ck(cudaMemcpy(ldev.data(), c->d_lam, ldev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    ck(cudaMemcpy(xall.data(), c->d_x, xall.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+  }
+  for (int i = 0; i < count; ++i) {
+    dopf_result_view& r = results[i];
+    const InstDesc& id = L.inst[i];
+    r.status = status[i];
+    r.iterations = iters[i];
+    r.objective = obj[i];
+    r.max_local_infeasibility = maxinf[i];
+    r.time_solve = c->last_kernel_s;
+    r.time_global = r.time_local = r.time_dual = 0.0;
+    if (copy_vectors && any_vec) {
+      if (r.x) std::memcpy(r.x, xall.data() + id.x_off, sizeof(double) * id.n);
+      for (int32_t d = id.row0; d < id.row0 + id.rows; ++d) {
+        const int32_t ref = L.ref_of_dev[d];
+        if (r.z) r.z[ref] = zdev[d];
+        if (r.lambda) r.lambda[ref] = ldev[d];
+      }
+    }
+    if (r.trace && iters[i] > 0)
+      ck(cudaMemcpy(r.trace, c->d_trace + static_cast<std::size_t>(i) * s->max_iter * 6,
+                    static_cast<std::size_t>(iters[i]) * 6 * sizeof(double), cudaMemcpyDeviceToHost),
+         "trace d2h");
+    r.time_download =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_dn0).count();
+    r.time_upload = std::chrono::duration<double>(t_dn0 - t_up0).count() - c->last_kernel_s;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dopf_cuda_create(int device, dopf_cuda_ctx** out) {
+  if (!out) return DOPF_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* c = new (std::nothrow) dopf_cuda_ctx();
+  if (!c) return DOPF_ERR_OUT_OF_MEMORY;
+  const int rc = guarded(c, [&] {
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) throw std::invalid_argument("no such CUDA device");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    c->device = device;
+    ck(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
+    c->smem_optin = max_dynamic_smem(device);
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreate(&c->ev0), "event");
+    ck(cudaEventCreate(&c->ev1), "event");
+  });
+  if (rc != DOPF_OK) {
+    // keep the message reachable for the caller through a leaked-free path
+    static thread_local std::string last;
+    last = c->err;
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return DOPF_OK;
+}
+
+int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
+  if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->free_model();
+    c->L = HostLayout();
+    const LayoutOptions opt = options_for(c);
+    const int G = choose_blocks(*m, opt);
+    add_instance(c->L, *m, G, opt);
+    c->inst_nz = {m->N_z};
+    c->inst_n = {m->n};
+    finish_upload(c);
+  });
+}
+
+int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t count) {
+  if (!c || !ms || count < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->free_model();
+    c->L = HostLayout();
+    LayoutOptions opt = options_for(c);
+    opt.max_blocks = 8;  // one cluster per scenario
+    const int G = choose_blocks(ms[0], opt);
+    c->inst_nz.clear();
+    c->inst_n.clear();
+    for (int i = 0; i < count; ++i) {
+      add_instance(c->L, ms[i], G, opt);
+      c->inst_nz.push_back(ms[i].N_z);
+      c->inst_n.push_back(ms[i].n);
+    }
+    for (const auto& id : c->L.inst)
+      if (id.blocks != c->L.blocks_per_instance)
+        throw std::invalid_argument("batched scenarios must share the subsystem structure");
+    finish_upload(c);
+  });
+}
+
+int dopf_cuda_solve(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r) {
+  if (!c || !r) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] { run(c, s, r, 1, true); });
+}
+
+int dopf_cuda_solve_device(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r) {
+  if (!c || !r) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] { run(c, s, r, 1, false); });
+}
+
+int dopf_cuda_solve_batch(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r,
+                          int32_t count) {
+  if (!c || !r) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] { run(c, s, r, count, true); });
+}
+
+const char* dopf_cuda_last_error(const dopf_cuda_ctx* c) { return c ? c->err.c_str() : ""; }
+
+void dopf_cuda_destroy(dopf_cuda_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  c->free_model();
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int dopf_cuda_info(const dopf_cuda_ctx* c, dopf_cuda_info_t* out) {
+  if (!c || !out) return DOPF_ERR_INVALID_ARGUMENT;
+  out->instances = static_cast<int32_t>(c->L.inst.size());
+  out->blocks = c->L.blocks_per_instance;
+  out->threads = kThreads;
+  out->smem_bytes = static_cast<int32_t>(c->L.smem_bytes);
+  out->resident = c->L.all_ops_in_smem ? 1 : 0;
+  out->sync_mode = static_cast<int32_t>(c->mode);
+  return DOPF_OK;
+}
+
+int64_t dopf_cuda_kernel_launches(const dopf_cuda_ctx* c) { return c ? c->launches : 0; }
+
+double dopf_cuda_bytes_per_iteration(const dopf_cuda_ctx* c) {
+  return c ? c->L.bytes_per_iteration : 0.0;
+}
+
+double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* c) { return c ? c->last_kernel_s : 0.0; }
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// Device layout of one or more ADMM instances (POD structs shared by the
+// host-side builder, layout.cpp, and the sm_100a kernels, admm_kernels.cu).
+//
+// HBM / shared-memory layout:
+//  * Subsystems are split into contiguous s-ranges, one per CTA ("block"),
+//    balanced by operator bytes; inside a block they are reordered by n_s
+//    (descending) so warps see uniform GEMV lengths.
+//  * A "device row" is one local variable (s, i). z, lambda and the exchange
+//    value u = z - lambda/rho are stored in device-row order.
+//  * P_s and A_s are packed per block, column-major per subsystem, so the
+//    threads owning rows i = 0..n_s-1 of a subsystem read consecutive
+//    addresses at every step j (coalesced in HBM, conflict-free in smem).
+//  * Each block computes the global update x_i for every column its rows
+//    reference, from the copies' u values (CSR by column, ascending s, the
+//    reference's summation order) -- so one grid/cluster barrier per
+//    iteration suffices and the result is bitwise deterministic.
+#pragma once
+
+#include <cstdint>
+
+namespace dopf::cuda {
+
+constexpr int kThreads = 512;   // CTA size of the iteration kernels
+constexpr int kMaxK = 4;        // max rows (and cols, A-rows) per thread
+constexpr int kPartials = 8;    // gap, step, bx2, z2, lam2, objective, maxinf, pad
+
+struct BlockDesc {
+  int32_t row0;        // first device row of this block (global across instances)
+  int32_t rows;        // local variables owned
+  int32_t cols;        // global columns referenced (x computed here)
+  int32_t arows;       // equality rows (A-tasks)
+  int64_t p_off;       // block's packed P in the global P array
+  int64_t a_off;       // block's packed A in the global A array
+  int32_t p_len;       // doubles
+  int32_t a_len;       // doubles
+  int32_t copy_off;    // block's copy list in the global copies array
+  int32_t copy_len;
+  int32_t col_off;     // block's column metadata
+  int32_t amet_off;    // block's A-task metadata
+  int32_t ops_in_smem; // 1: P and A staged in shared memory once, 0: read from HBM/L2
+  int32_t instance;
+  int32_t inst_block;  // index of this block within its instance
+  int32_t pad;
+};
+
+struct InstDesc {
+  int64_t x_off;       // instance's x in the global x array
+  int32_t n;           // global columns
+  int32_t blocks;      // CTAs cooperating on this instance
+  int32_t block0;      // first block
+  int32_t rows;        // N_z of the instance
+  int64_t trace_off;   // rows of 6 doubles
+  int32_t row0;        // first device row
+  int32_t pad;
+};
+
+// Row task: z_i = sum_j P(i,j) t_j + v_i for one (s, i).
+struct RowMeta {
+  int32_t pofs;   // offset of P(i, 0) within the block's P (column-major: stride n)
+  int32_t n;      // n_s
+  int32_t base;   // block-local row index of (s, 0)
+  int32_t xloc;   // block-local column index of local_to_global(s, i)
+};
+
+// Column task: x_c from its copies.
+struct ColMeta {
+  int32_t gcol;        // global column (within the instance)
+  int32_t copy_start;  // in the block's copy list
+  int32_t copy_count;
+  int32_t owner;       // 1: this block writes x and adds c*x to the objective
+};
+
+// Equality-check task: |A_r z_s - b_r| for one reduced row of a subsystem.
+struct AMeta {
+  int32_t aofs;   // offset of A(r, 0) within the block's A (column-major: stride m)
+  int32_t m;      // m_s
+  int32_t n;      // n_s
+  int32_t base;   // block-local row index of (s, 0)
+};
+
+}  // namespace dopf::cuda

@@ -1,0 +1,217 @@
+#include "layout_builder.hpp"
+
+#include <algorithm>
+#include <numeric>
+#include <stdexcept>
+
+namespace dopf::cuda {
+
+namespace {
+
+int ns_of(const dopf_model_view& m, int s) { return m.z_offsets[s + 1] - m.z_offsets[s]; }
+
+// Contiguous s-ranges with nearly equal operator cost.
+std::vector<int> split_points(const dopf_model_view& m, int G) {
+  std::vector<double> cost(m.S);
+  double total = 0;
+  for (int s = 0; s < m.S; ++s) {
+    const double n = ns_of(m, s), mm = m.m_s[s];
+    cost[s] = n * n + mm * n + 6.0 * n + 4.0;
+    total += cost[s];
+  }
+  std::vector<int> cuts{0};
+  double acc = 0;
+  int g = 1;
+  for (int s = 0; s < m.S && g < G; ++s) {
+    acc += cost[s];
+    if (acc >= total * g / G) {
+      if (s + 1 > cuts.back()) cuts.push_back(s + 1);
+      ++g;
+    }
+  }
+  if (cuts.back() != m.S) cuts.push_back(m.S);
+  return cuts;  // size <= G+1
+}
+
+}  // namespace
+
+std::size_t block_smem_bytes(const BlockDesc& b, bool ops_in_smem) {
+  std::size_t bytes = 0;
+  if (ops_in_smem) bytes += 8ull * (static_cast<std::size_t>(b.p_len) + b.a_len);
+  bytes += 16ull * b.rows;        // target, z
+  bytes += 8ull * b.cols;         // x
+  bytes += 40ull * b.cols;        // c/rho, inv, lo, hi, c
+  bytes += 4ull * b.copy_len;     // copy list
+  bytes = (bytes + 15) & ~std::size_t(15);
+  bytes += 8ull * kPartials * (kThreads / 32 + 2) + 256;  // reduction scratch
+  return bytes;
+}
+
+double algorithmic_bytes(const dopf_model_view& m) {
+  double n2 = 0, mn = 0, msum = 0;
+  for (int s = 0; s < m.S; ++s) {
+    const double n = ns_of(m, s);
+    n2 += n * n;
+    mn += m.m_s[s] * n;
+    msum += m.m_s[s];
+  }
+  return 8.0 * (n2 + mn + msum) + 56.0 * m.N_z + 48.0 * m.n + 4.0 * (2.0 * m.N_z + m.n + 1) +
+         16.0 * m.S;
+}
+
+double algorithmic_flops(const dopf_model_view& m) {
+  double n2 = 0, mn = 0;
+  for (int s = 0; s < m.S; ++s) {
+    const double n = ns_of(m, s);
+    n2 += n * n;
+    mn += m.m_s[s] * n;
+  }
+  return 2.0 * n2 + 2.0 * mn + 20.0 * m.N_z;
+}
+
+int choose_blocks(const dopf_model_view& m, const LayoutOptions& opt) {
+  if (opt.blocks_per_instance > 0) return opt.blocks_per_instance;
+  // Estimate per-block smem for a given G from totals; refine by trial.
+  const int rows_cap = opt.threads * kMaxK;
+  for (int G = 1; G <= opt.max_blocks; G = (G < 8 ? G + 1 : G + (G < 64 ? 8 : 16))) {
+    if (G > m.S) break;
+    HostLayout trial;
+    LayoutOptions o = opt;
+    add_instance(trial, m, G, o);
+    bool ok = trial.all_ops_in_smem;
+    for (const auto& b : trial.blocks) ok = ok && b.rows <= rows_cap;
+    if (ok && trial.K <= 2) return G;
+    if (ok && G >= 8 && trial.K <= kMaxK) {
+      // large instance: use the whole GPU for parallelism
+      return std::min(opt.max_blocks, m.S);
+    }
+  }
+  return std::min(opt.max_blocks, std::max(1, m.S));
+}
+
+void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOptions& opt) {
+  if (!m.has_pre) throw std::invalid_argument("model view lacks precomputed operators");
+  const int instance = static_cast<int>(L.inst.size());
+  const std::vector<int> cuts = split_points(m, std::max(1, std::min(G, std::max(1, m.S))));
+  const int nb = static_cast<int>(cuts.size()) - 1;
+  const int32_t inst_row0 = static_cast<int32_t>(L.rows_total);
+  const int32_t block0 = static_cast<int32_t>(L.blocks.size());
+
+  InstDesc id{};
+  id.x_off = L.x_total;
+  id.n = m.n;
+  id.blocks = std::max(nb, 1);
+  id.block0 = block0;
+  id.rows = m.N_z;
+  id.row0 = inst_row0;
+  L.inst.push_back(id);
+  L.x_total += m.n;
+
+  // Pass 1: device rows (subsystems by n_s descending inside each block).
+  std::vector<int32_t> dev_of_ref(m.N_z, -1);
+  std::vector<std::vector<int>> order(nb);
+  int32_t next_row = inst_row0;
+  std::vector<int32_t> block_row0(nb);
+  for (int g = 0; g < nb; ++g) {
+    auto& ord = order[g];
+    for (int s = cuts[g]; s < cuts[g + 1]; ++s) ord.push_back(s);
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int a, int b) { return ns_of(m, a) > ns_of(m, b); });
+    block_row0[g] = next_row;
+    for (int s : ord)
+      for (int i = 0; i < ns_of(m, s); ++i) dev_of_ref[m.z_offsets[s] + i] = next_row++;
+  }
+  L.rows_total = next_row;
+  L.rmeta.resize(next_row);
+  L.v.resize(next_row);
+  L.z0.resize(next_row);
+  L.ref_of_dev.resize(next_row);
+
+  // owner block of each column = block holding its first (lowest-s) copy
+  std::vector<int> block_of_s(m.S, 0);
+  for (int g = 0; g < nb; ++g)
+    for (int s = cuts[g]; s < cuts[g + 1]; ++s) block_of_s[s] = g;
+  std::vector<int> s_of_ref(m.N_z);
+  for (int s = 0; s < m.S; ++s)
+    for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) s_of_ref[k] = s;
+
+  std::vector<int> xloc_of(m.n, -1);
+  for (int g = 0; g < nb; ++g) {
+    BlockDesc bd{};
+    bd.row0 = block_row0[g];
+    bd.instance = instance;
+    bd.inst_block = g;
+    bd.p_off = static_cast<int64_t>(L.P.size());
+    bd.a_off = static_cast<int64_t>(L.A.size());
+    bd.copy_off = static_cast<int32_t>(L.copies.size());
+    bd.col_off = static_cast<int32_t>(L.cmeta.size());
+    bd.amet_off = static_cast<int32_t>(L.ameta.size());
+
+    // columns referenced by this block, ascending
+    std::vector<int> cols;
+    for (int s : order[g])
+      for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) cols.push_back(m.l2g[k]);
+    std::sort(cols.begin(), cols.end());
+    cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+    for (std::size_t q = 0; q < cols.size(); ++q) xloc_of[cols[q]] = static_cast<int>(q);
+
+    int32_t local = 0, pofs = 0, aofs = 0;
+    for (int s : order[g]) {
+      const int n = ns_of(m, s), ms = m.m_s[s];
+      const int base = local;
+      const double* Ps = m.P + m.p_offsets[s];  // row-major n x n
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) L.P.push_back(Ps[i * n + j]);
+      const double* As = m.A + m.a_offsets[s];  // row-major ms x n
+      for (int j = 0; j < n; ++j)
+        for (int r = 0; r < ms; ++r) L.A.push_back(As[r * n + j]);
+      for (int i = 0; i < n; ++i) {
+        const int ref = m.z_offsets[s] + i;
+        const int32_t dev = bd.row0 + local;
+        L.rmeta[dev] = RowMeta{pofs + i, n, base, xloc_of[m.l2g[ref]]};
+        L.v[dev] = m.v[ref];
+        L.z0[dev] = m.z0[ref];
+        L.ref_of_dev[dev] = ref;
+        ++local;
+      }
+      for (int r = 0; r < ms; ++r) {
+        L.ameta.push_back(AMeta{aofs + r, ms, n, base});
+        L.ab.push_back(m.b[m.b_offsets[s] + r]);
+      }
+      pofs += n * n;
+      aofs += ms * n;
+    }
+    bd.rows = local;
+    bd.arows = static_cast<int32_t>(L.ameta.size()) - bd.amet_off;
+    bd.p_len = pofs;
+    bd.a_len = aofs;
+    bd.cols = static_cast<int32_t>(cols.size());
+    for (int c : cols) {
+      ColMeta cm{};
+      cm.gcol = c;
+      cm.copy_start = static_cast<int32_t>(L.copies.size()) - bd.copy_off;
+      cm.copy_count = m.csr_ptr[c + 1] - m.csr_ptr[c];
+      for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q) L.copies.push_back(dev_of_ref[m.csr_copy[q]]);
+      cm.owner = block_of_s[s_of_ref[m.csr_copy[m.csr_ptr[c]]]] == g ? 1 : 0;
+      L.cmeta.push_back(cm);
+      L.cc.push_back(m.c[c]);
+      L.cinv.push_back(m.inv_copy[c]);
+      L.clo.push_back(m.x_lo[c]);
+      L.chi.push_back(m.x_hi[c]);
+    }
+    bd.copy_len = static_cast<int32_t>(L.copies.size()) - bd.copy_off;
+    for (int c : cols) xloc_of[c] = -1;
+
+    bd.ops_in_smem = block_smem_bytes(bd, true) <= opt.smem_limit ? 1 : 0;
+    if (!bd.ops_in_smem) L.all_ops_in_smem = false;
+    L.smem_bytes = std::max(L.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
+    const int k_rows = (bd.rows + opt.threads - 1) / opt.threads;
+    L.K = std::max(L.K, std::max(1, k_rows));
+    L.blocks.push_back(bd);
+  }
+  L.blocks_per_instance = std::max(L.blocks_per_instance, nb);
+  L.bytes_per_iteration += algorithmic_bytes(m);
+  L.flops_per_iteration += algorithmic_flops(m);
+}
+
+}  // namespace dopf::cuda

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 namespace dopf {
@@ -57,7 +58,9 @@ Attempt build(const ShapeSpec& spec, Rng& rng, double p3) {
 
   // Internal tree: chains that occasionally branch from a random earlier node.
   std::vector<int> parent(B, -1);
-  const int target_internal_leaves = std::max(1, K / 2);
+  // Every leaf of the internal tree takes one real leaf, so the internal tree
+  // has ~K leaves: many short laterals, shallow depth (fast consensus mixing).
+  const int target_internal_leaves = std::max(1, K - 1);
   const double p_branch = I > 2 ? static_cast<double>(target_internal_leaves - 1) / (I - 1) : 0.0;
   for (int i = 1; i < I; ++i)
     parent[i] = (i >= 2 && rng.unit() < p_branch) ? rng.below(i - 1) : i - 1;
@@ -136,7 +139,7 @@ Attempt build(const ShapeSpec& spec, Rng& rng, double p3) {
   }
 
   // Voltage-drop budget: sum over a root path of ~2(r+x)P stays below ~0.1.
-  const double z_scale = std::min(1.0, 1.0 / (spec.total_load * std::max(1, depth_max)));
+  const double z_scale = std::min(1.0, 5.0 / (spec.total_load * std::max(1, depth_max)));
   const double line_shunt_scale = std::min(1.0, 10.0 / spec.lines);
   const double flow_cap = std::max(2.0, 3.0 * spec.total_load);
   auto make_line = [&](const std::string& id, int from, int to, const std::vector<int>& ph,

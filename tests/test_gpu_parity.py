@@ -1,0 +1,148 @@
+"""GPU parity: the sm_100a path through the C ABI (include/dopf_cuda.h) vs the
+CPU oracle restating reference proj/src/admm.cpp:172-244.
+
+Bar (BASELINE.json north_star): identical iteration count and status;
+per-iterate x, z, lambda within 1e-9 relative (by construction the iterates
+are bitwise identical -- asserted separately on the fixtures); final objective
+within 1e-6 relative.
+"""
+import numpy as np
+import pytest
+
+from conftest import FIXTURES, fixture_path
+from oracle import oracle_py as O
+from paper_2501_08293_b200 import dopf
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9
+OBJ_REL = 1e-6
+
+
+def rel_err(a, b):
+    scale = max(1.0, float(np.max(np.abs(b)))) if b.size else 1.0
+    return float(np.max(np.abs(a - b))) / scale if b.size else 0.0
+
+
+def assert_same(gpu, ref, bitwise=False):
+    assert gpu.status == ref.status
+    assert gpu.iterations == ref.iterations
+    for name, a, b in (("x", gpu.x, ref.x), ("z", gpu.z, ref.z), ("lambda", gpu.lam, ref.lam)):
+        if bitwise:
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (name, rel_err(a, b))
+        assert rel_err(a, b) <= REL, name
+    assert abs(gpu.objective - ref.objective) <= OBJ_REL * max(1.0, abs(ref.objective))
+    # residual trace: tree vs sequential summation, ulp-level only
+    np.testing.assert_allclose(gpu.trace[:, 1:], ref.trace[:, 1:], rtol=1e-9, atol=1e-13)
+    assert gpu.max_local_infeasibility <= max(1e-8, 10 * ref.max_local_infeasibility)
+
+
+def model_of_fixture(name):
+    _, ls, model = dopf.load_model(fixture_path(name))
+    model.precompute()
+    return ls, model
+
+
+@pytest.fixture(scope="module")
+def solver():
+    return dopf.CudaSolver(0)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("eps", [1e-3, 1e-4])
+def test_fixture_solve_matches_oracle_bitwise(solver, name, eps):
+    _, model = model_of_fixture(name)
+    settings = dopf.Settings(rho=100.0, eps_rel=eps)
+    solver.upload(model)
+    gpu = solver.solve(settings)
+    ref = O.solve(model, settings)
+    assert gpu.status == dopf.CONVERGED
+    assert_same(gpu, ref, bitwise=True)
+
+
+@pytest.mark.parametrize("name", ["two_bus", "four_bus_delta"])
+def test_per_iterate_parity(solver, name):
+    """Every sampled iterate t: run the device loop with max_iter = t."""
+    _, model = model_of_fixture(name)
+    samples = [1, 2, 3, 5, 10, 50, 100, 300]
+    ref = O.solve(model, dopf.Settings(eps_rel=1e-12, max_iter=max(samples)), snap_iters=samples)
+    solver.upload(model)
+    # two_bus reaches exact consensus (pres = dres = 0) at t = 203 even at 1e-12
+    samples = [t for t in samples if t < ref.iterations] + [ref.iterations]
+    for t in samples:
+        gpu = solver.solve(dopf.Settings(eps_rel=1e-12, max_iter=t))
+        assert gpu.iterations == t
+        assert gpu.status == (ref.status if t == ref.iterations else dopf.ITERATION_LIMIT)
+        if t == ref.iterations:
+            snap = {"x": ref.x, "z": ref.z, "lambda": ref.lam}
+            assert np.array_equal(gpu.x, snap["x"]) and np.array_equal(gpu.z, snap["z"])
+            continue
+        snap = ref.snapshots[t]
+        assert np.array_equal(gpu.x, snap["x"]), t
+        assert np.array_equal(gpu.z, snap["z"]), t
+        assert np.array_equal(gpu.lam, snap["lambda"]), t
+
+
+def test_iteration_limit_is_a_status(solver):
+    _, model = model_of_fixture("two_bus")
+    solver.upload(model)
+    res = solver.solve(dopf.Settings(eps_rel=1e-12, max_iter=10))
+    assert res.status == dopf.ITERATION_LIMIT
+    assert res.iterations == 10 and res.trace.shape == (10, 6)
+    lo, hi = model.arr("x_lo"), model.arr("x_hi")
+    assert np.all(res.x >= lo) and np.all(res.x <= hi)
+
+
+def test_invalid_settings_raise(solver):
+    _, model = model_of_fixture("single_bus")
+    solver.upload(model)
+    for bad in (dopf.Settings(rho=0.0), dopf.Settings(eps_rel=0.0), dopf.Settings(max_iter=0)):
+        with pytest.raises(ValueError):
+            solver.solve(bad)
+
+
+@pytest.mark.parametrize("shape,seed", [("ieee13", 13), ("ieee123", 123)])
+def test_synthetic_feeder_parity(solver, shape, seed):
+    f = dopf.synthetic_feeder(shape, seed)
+    _, _, model = dopf.load_model(f, workers=4)
+    model.precompute(4)
+    settings = dopf.Settings()
+    solver.upload(model)
+    gpu = solver.solve(settings)
+    ref = O.solve(model, settings)
+    assert_same(gpu, ref, bitwise=True)
+
+
+def test_ieee8500_first_iterations_bitwise(solver):
+    f = dopf.synthetic_feeder("ieee8500", 8500)
+    _, _, model = dopf.load_model(f, workers=8)
+    model.precompute(8)
+    settings = dopf.Settings(eps_rel=1e-12, max_iter=60)
+    solver.upload(model)
+    info = solver.info()
+    assert info["resident"]
+    gpu = solver.solve(settings)
+    ref = O.solve(model, settings)
+    assert_same(gpu, ref, bitwise=True)
+
+
+def test_batch_of_scenarios(solver):
+    base = dopf.synthetic_feeder("ieee13", 13)
+    models = []
+    for k in range(6):
+        f = dopf.scale_loads(base, 4096 + k)
+        _, _, m = dopf.load_model(f)
+        m.precompute()
+        models.append(m)
+    settings = dopf.Settings(eps_rel=1e-3)
+    results = solver_batch(models, settings)
+    for m, gpu in zip(models, results):
+        ref = O.solve(m, settings)
+        assert_same(gpu, ref, bitwise=True)
+
+
+def solver_batch(models, settings):
+    from paper_2501_08293_b200.batch import BatchSolver
+    bs = BatchSolver(0)
+    bs.upload(models)
+    return bs.solve(settings)
