@@ -68,6 +68,11 @@ double dopf_cuda_bytes_per_iteration(const dopf_cuda_ctx* ctx);
 /* Device time (seconds) of the last solve's kernel, CUDA events on the
  * launching stream. */
 double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* ctx);
+/* Phase clock: when enabled, CTA 0 records SM cycles spent in each of the 8
+ * loop phases (top wait, target, GEMV, equality+dual, reduce, exchange,
+ * global update, combine) during the next solves. */
+int dopf_cuda_set_profiling(dopf_cuda_ctx* ctx, int32_t on);
+int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out8);
 
 #ifdef __cplusplus
 }

@@ -49,7 +49,7 @@ class LpView_t(C.Structure):
 
 class BatchInfo_t(C.Structure):
     _fields_ = [("instances", i32), ("blocks", i32), ("threads", i32), ("smem_bytes", i32),
-                ("resident", i32), ("reserved", i32)]
+                ("resident", i32), ("sync_mode", i32)]
 
 
 _host = None
@@ -123,6 +123,9 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_info", C.c_int, vp, P(BatchInfo_t))
     _sig(lib, "dopf_cuda_kernel_launches", i64, vp)
     _sig(lib, "dopf_cuda_bytes_per_iteration", f64, vp)
+    _sig(lib, "dopf_cuda_last_kernel_seconds", f64, vp)
+    _sig(lib, "dopf_cuda_set_profiling", C.c_int, vp, i32)
+    _sig(lib, "dopf_cuda_phase_cycles", C.c_int, vp, P(i64))
     _cuda = lib
     return lib
 

@@ -1,55 +1,73 @@
 // Persistent fp64 ADMM iteration kernel for sm_100a.
 //
 // One launch runs the whole loop of reference proj/src/admm.cpp:190-235 on
-// the device. Per iteration and per CTA ("block", a contiguous range of
+// the device. Per iteration t and per CTA ("block": a contiguous range of
 // subsystems, layout.hpp):
 //
-//   (1) global update, admm.cpp:118-129 (K2): for every column the block's
-//       rows reference, acc = sum of u = z - lambda/rho over its copies in
-//       ascending s (read from L2), x = clamp((acc - c/rho) * inv, lo, hi).
-//       Blocks compute shared columns redundantly (bitwise identical), so no
-//       second barrier is needed to broadcast x.
-//   (2) local update, admm.cpp:131-138 (K1): t = x[l2g] + lambda/rho,
-//       z = P t + v as a sequential-j dot product per row; P comes from
-//       shared memory (staged once per launch) or, when it does not fit, HBM.
-//   (3) ||A z - b||_inf, admm.cpp:203-205.
-//   (4) dual update, admm.cpp:140-143, and u = z - lambda/rho for the next
-//       global step; residual partial sums, admm.cpp:150-163.
-//   (5) warp-shuffle + block reduction of the partials (fixed order), one
-//       grid / cluster barrier, every block combines all partials in the same
-//       fixed order and takes the same stop decision (admm.hpp:63) -- the
-//       on-device convergence check. Block 0 writes the trace row.
+//   (L) local update, admm.cpp:131-138 (K1): t = x[l2g] + lambda/rho,
+//       z = P t + v as a sequential-j dot product per row; P staged in shared
+//       memory once per launch (or read from HBM when it does not fit).
+//   (A) ||A_s z_s - b_s||_inf, admm.cpp:203-205.
+//   (D) dual update, admm.cpp:140-143, exchange value u = z - lambda/rho,
+//       per-thread residual partial sums, admm.cpp:150-163.
+//   (F) publish: thread 0 releases the block's "u(t) ready" flag right after
+//       the u stores -- this is the only inter-CTA synchronisation of the
+//       iteration (cluster mode: the hardware cluster barrier instead).
+//   (R) while other blocks catch up: warp-shuffle block reduction of the
+//       residual partials (fixed order) into the block's slot for t. The slot
+//       becomes visible to other blocks through the NEXT flag release, so
+//       residual reduction is entirely off the critical path.
+//   (W) warp 0 polls every block's flag (acquire).
+//   (G) warps 1..15: global update for t+1, admm.cpp:118-129 (K2): for every
+//       column the block's rows reference, acc = sum of u over its copies in
+//       ascending s (L2 reads), x = clamp((acc - c/rho) * inv, lo, hi). Shared
+//       columns are computed redundantly (bitwise identical) by each block
+//       that needs them, so x is never broadcast.
+//   (S) concurrently warp 0: combines every block's slot of t-1 in a fixed
+//       order -> residuals, trace row, stop test (admm.hpp:63). The decision
+//       for t-1 is taken one iteration late; the state of t-1 (x in a 3-deep
+//       ring, z and lambda in registers) is kept so the result is exactly the
+//       reference's iterate at its stopping iteration.
 //
 // Bitwise parity with the CPU oracle: compiled with --fmad=false; every
 // iterate operation keeps the reference's form (division by rho, multiply by
 // the inverse copy count, std::min/std::max select semantics, sequential sums
 // in the reference order). Only the residual/objective reductions use a
 // different (tree) order; they feed the stop test and the trace only.
-#include <cooperative_groups.h>
-
 #include "admm_kernels.cuh"
 
 namespace dopf::cuda {
 
 namespace {
 
-__device__ __forceinline__ double ld_l2(const double* p) { return __ldcg(p); }
+constexpr int kWarps = kThreads / 32;
+constexpr int kColThreads = kThreads - 32;  // warps 1.. own the global-update columns
+constexpr int kSlots = 3;                   // partial-slot ring depth (see header comment)
 
+__device__ __forceinline__ double ld_l2(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ double sel_max(double a, double b) { return (a < b) ? b : a; }  // std::max
 __device__ __forceinline__ double sel_min(double a, double b) { return (b < a) ? b : a; }  // std::min
 
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    unsigned int seen;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
-    } while (seen < target);
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Relaxed poll (no per-poll L1 invalidation); one acquire fence after the
+// flag was observed orders the subsequent loads (fence-acquire pattern).
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Warp 0 waits until every block of the instance published flag >= value.
+__device__ __forceinline__ void wait_flags(const unsigned long long* flags, int G, int lane,
+                                           unsigned long long value) {
+  for (int g = lane; g < G; g += 32)
+    while (ld_relaxed_u64(flags + g) < value) {
+    }
+  fence_acq_rel();
+  __syncwarp();
 }
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -59,56 +77,74 @@ __device__ __forceinline__ void cluster_barrier() {
           : "memory");
 }
 
-constexpr int kWarps = kThreads / 32;
+// 7 reduction lanes: 0..5 sums (gap, step, bx2, z2, lam2, objective), 6 max.
+__device__ __forceinline__ void warp_reduce7(double (&v)[7], int width) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    if (off >= width) continue;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) v[q] = v[q] + __shfl_xor_sync(0xffffffffu, v[q], off);
+    v[6] = sel_max(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
+  }
+}
 
-template <int K>
+template <int K, bool kSmemOps>
 __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(16) double smem[];
   const BlockDesc bd = p.blocks[blockIdx.x];
   const InstDesc id = p.inst[bd.instance];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
 
-  // ---- shared-memory carve-up (must match block_smem_bytes) ----
-  unsigned char* cur = smem;
-  const double* sP;
-  const double* sA;
-  if (bd.ops_in_smem) {
-    double* dP = reinterpret_cast<double*>(cur);
-    cur += sizeof(double) * bd.p_len;
-    double* dA = reinterpret_cast<double*>(cur);
-    cur += sizeof(double) * bd.a_len;
-    for (int i = tid; i < bd.p_len; i += kThreads) dP[i] = p.P[bd.p_off + i];
-    for (int i = tid; i < bd.a_len; i += kThreads) dA[i] = p.A[bd.a_off + i];
-    sP = dP;
-    sA = dA;
-  } else {
-    sP = p.P + bd.p_off;
-    sA = p.A + bd.a_off;
+  // ---- shared-memory carve-up, in doubles (must match block_smem_bytes) ----
+  std::size_t off = 0;
+  const double* gP = p.P + bd.p_off;
+  const double* gA = p.A + bd.a_off;
+  double* sP = smem;
+  double* sA = smem;
+  if (kSmemOps) {
+    sP = smem + off;
+    off += bd.p_len;
+    sA = smem + off;
+    off += bd.a_len;
+    for (int i = tid; i < bd.p_len; i += kThreads) sP[i] = gP[i];
+    for (int i = tid; i < bd.a_len; i += kThreads) sA[i] = gA[i];
   }
-  double* tgt = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.rows;
-  double* zs = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.rows;
-  double* xs = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.cols;
-  double* c_rho = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.cols;
-  double* c_inv = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.cols;
-  double* c_lo = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.cols;
-  double* c_hi = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.cols;
-  double* c_cost = reinterpret_cast<double*>(cur);
-  cur += sizeof(double) * bd.cols;
-  int32_t* cps = reinterpret_cast<int32_t*>(cur);
-  cur += sizeof(int32_t) * bd.copy_len;
-  cur = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(cur) + 15) & ~uintptr_t(15));
-  double* red = reinterpret_cast<double*>(cur);  // [kWarps + 2][kPartials]
+  const double* Pop = kSmemOps ? sP : gP;
+  const double* Aop = kSmemOps ? sA : gA;
+  double* tgt = smem + off;
+  off += bd.rows;
+  double* zs = smem + off;
+  off += bd.rows;
+  double* vs = smem + off;
+  off += bd.rows;
+  double* xring = smem + off;  // [3][cols]
+  off += 3 * static_cast<std::size_t>(bd.cols);
+  double* c_rho = smem + off;
+  off += bd.cols;
+  double* c_inv = smem + off;
+  off += bd.cols;
+  double* c_lo = smem + off;
+  off += bd.cols;
+  double* c_hi = smem + off;
+  off += bd.cols;
+  double* c_cost = smem + off;
+  off += bd.cols;
+  double* red = smem + off;  // [kWarps][kPartials] + decision words
+  off += (kWarps + 2) * kPartials;
+  double* a_rhs = smem + off;  // equality-row rhs b_r
+  off += bd.arows;
+  AMeta* a_meta = reinterpret_cast<AMeta*>(smem + off);  // 16 B each
+  off += 2 * static_cast<std::size_t>(bd.arows);
+  int32_t* cps = reinterpret_cast<int32_t*>(smem + off);
 
   const double rho = p.rho;
   for (int i = tid; i < bd.copy_len; i += kThreads) cps[i] = p.copies[bd.copy_off + i];
+  for (int r = tid; r < bd.rows; r += kThreads) vs[r] = p.v[bd.row0 + r];
+  for (int a = tid; a < bd.arows; a += kThreads) {
+    a_meta[a] = p.ameta[bd.amet_off + a];
+    a_rhs[a] = p.ab[bd.amet_off + a];
+  }
   for (int c = tid; c < bd.cols; c += kThreads) {
     const double cost = p.cc[bd.col_off + c];
     c_rho[c] = cost / rho;  // admm.cpp:126 evaluates c_i / rho; same value every iteration
@@ -118,99 +154,156 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
     c_hi[c] = p.chi[bd.col_off + c];
   }
 
-  // ---- per-thread state (rows, columns, equality rows) in registers ----
+  // ---- per-thread state in registers ----
+  // rows r = tid + k*kThreads; A-rows likewise; columns c = (tid-32) + k*kColThreads
   RowMeta rm[K];
   ColMeta cm[K];
-  AMeta am[K];
-  double lam[K], zp[K], vv[K], bb[K], zn[K];
+  double lam[K], lr[K], zp[K];
+  const int ctid = tid - 32;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int r = tid + k * kThreads;
     if (r < bd.rows) {
       rm[k] = p.rmeta[bd.row0 + r];
-      vv[k] = p.v[bd.row0 + r];
       zp[k] = p.z0[bd.row0 + r];
     } else {
       rm[k] = RowMeta{0, 0, 0, 0};
-      vv[k] = 0.0;
       zp[k] = 0.0;
     }
     lam[k] = 0.0;
-    zn[k] = 0.0;
-    const int c = tid + k * kThreads;
-    cm[k] = c < bd.cols ? p.cmeta[bd.col_off + c] : ColMeta{0, 0, 0, 0};
-    const int a = tid + k * kThreads;
-    if (a < bd.arows) {
-      am[k] = p.ameta[bd.amet_off + a];
-      bb[k] = p.ab[bd.amet_off + a];
-    } else {
-      am[k] = AMeta{0, 0, 0, 0};
-      bb[k] = 0.0;
-    }
+    lr[k] = 0.0 / rho;  // lambda^0 / rho
+    const int c = ctid + k * kColThreads;
+    cm[k] = (ctid >= 0 && c < bd.cols) ? p.cmeta[bd.col_off + c] : ColMeta{0, 0, 0, 0};
   }
   __syncthreads();
 
   const double eps = p.eps_rel;
   const int G = id.blocks;
-  double* part = p.part + static_cast<int64_t>(bd.instance) * 2 * p.blocks_per_instance * kPartials;
-  double* u_even = p.u;
-  double* u_odd = p.u + p.rows_total;
+  const int64_t slot_stride = static_cast<int64_t>(p.blocks_per_instance) * kPartials;
+  double* slots = p.part + static_cast<int64_t>(bd.instance) * kSlots * slot_stride;
+  unsigned long long* flags = p.flags + static_cast<int64_t>(bd.instance) * p.blocks_per_instance;
+  double* u_buf[2] = {p.u, p.u + p.rows_total};
   double* trace = p.trace ? p.trace + static_cast<int64_t>(bd.instance) * p.trace_stride * 6 : nullptr;
   const bool leader = bd.inst_block == 0 && tid == 0;
+  const SyncMode mode = static_cast<SyncMode>(p.sync_mode);
 
-  double run_max = 0.0, last_obj = 0.0;
-  int status = 1;
-  int it = 1;
-  for (; it <= p.max_iter; ++it) {
-    const int parity = (it - 1) & 1;
-    const double* u_in = parity ? u_odd : u_even;
-    double* u_out = parity ? u_even : u_odd;
-
-    // (1) global update of the block's columns
+  // (G) global update from u_in into xdst (warps 1..); returns c'x share of owned columns
+  auto global_update = [&](const double* u_in, double* xdst) -> double {
     double obj = 0.0;
+    if (ctid < 0) return obj;
+    double a[K][4];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {  // issue the first (up to) 4 copy loads of every column
+      const int c = ctid + k * kColThreads;
+      const int cnt = c < bd.cols ? cm[k].copy_count : 0;
+      const int32_t* q = cps + cm[k].copy_start;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) a[k][e] = e < cnt ? ld_l2(u_in + q[e]) : 0.0;
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int c = tid + k * kThreads;
+      const int c = ctid + k * kColThreads;
       if (c < bd.cols) {
-        const int32_t* q = cps + cm[k].copy_start;
         const int cnt = cm[k].copy_count;
+        const int32_t* q = cps + cm[k].copy_start;
         double acc = 0.0;
-        int e = 0;
-        for (; e + 4 <= cnt; e += 4) {
-          const double a0 = ld_l2(u_in + q[e]), a1 = ld_l2(u_in + q[e + 1]);
-          const double a2 = ld_l2(u_in + q[e + 2]), a3 = ld_l2(u_in + q[e + 3]);
-          acc = acc + a0;
-          acc = acc + a1;
-          acc = acc + a2;
-          acc = acc + a3;
-        }
-        for (; e < cnt; ++e) acc = acc + ld_l2(u_in + q[e]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e < cnt) acc = acc + a[k][e];
+        for (int e = 4; e < cnt; ++e) acc = acc + ld_l2(u_in + q[e]);
         const double unclamped = (acc - c_rho[c]) * c_inv[c];
         const double xv = sel_min(sel_max(unclamped, c_lo[c]), c_hi[c]);
-        xs[c] = xv;
-        if (cm[k].owner) {
-          p.x_out[id.x_off + cm[k].gcol] = xv;
-          obj = obj + c_cost[c] * xv;
-        }
+        xdst[c] = xv;
+        if (cm[k].owner) obj = obj + c_cost[c] * xv;
       }
     }
-    __syncthreads();
+    return obj;
+  };
 
-    // (2a) consensus target t = x[l2g] + lambda / rho
+  // (S) warp 0: combine every block's slot for iteration s (fixed order), write
+  // the trace row, return the stop decision (all blocks decide identically).
+  auto combine = [&](int s, double& obj_s, double& mx_s) -> bool {
+    const double* base = slots + static_cast<int64_t>(s % kSlots) * slot_stride;
+    double t7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int g0 = lane; g0 < G; g0 += 64) {  // two slots per lane in flight
+      const int g1 = g0 + 32;
+      const double* r0 = base + g0 * kPartials;
+      const double* r1 = base + g1 * kPartials;
+      double a0[7], a1[7];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        a0[q] = ld_l2(r0 + q);
+        a1[q] = g1 < G ? ld_l2(r1 + q) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a0[q];
+      t7[6] = sel_max(t7[6], a0[6]);
+      if (g1 < G) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a1[q];
+        t7[6] = sel_max(t7[6], a1[6]);
+      }
+    }
+    warp_reduce7(t7, 32);
+    const double pres = sqrt(t7[0]);
+    const double dres = rho * sqrt(t7[1]);
+    const double eps_prim = eps * sel_max(sqrt(t7[2]), sqrt(t7[3]));
+    const double eps_dual = eps * sqrt(t7[4]);
+    if (leader && trace) {
+      double* row = trace + static_cast<int64_t>(s - 1) * 6;
+      row[0] = s;
+      row[1] = pres;
+      row[2] = dres;
+      row[3] = eps_prim;
+      row[4] = eps_dual;
+      row[5] = t7[5];
+    }
+    obj_s = t7[5];
+    mx_s = t7[6];
+    return pres <= eps_prim && dres <= eps_dual;
+  };
+
+  // optional phase clock (thread 0 of CTA 0): cycles spent between markers
+  const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
+  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tlast = clock64();
+#define PHASE(i)                      \
+  if (prof_on) {                      \
+    const long long tnow = clock64(); \
+    pacc[i] += tnow - tlast;          \
+    tlast = tnow;                     \
+  }
+
+  double obj = global_update(u_buf[0], xring);  // x^1 from u^0 = z^0
+  double run_max = 0.0, last_obj = 0.0;
+  int status = 1;
+  int stop_at = 0;  // converged iteration, 0 while running
+  int it = 1;
+  for (; it <= p.max_iter; ++it) {
+    const double* xt = xring + static_cast<std::size_t>((it - 1) % 3) * bd.cols;  // x^t
+    double* xnext = xring + static_cast<std::size_t>(it % 3) * bd.cols;            // x^{t+1}
+    double* u_out = u_buf[it & 1];
+    double* z_res = p.z_out + (it & 1) * p.rows_total;
+    double* l_res = p.lam_out + (it & 1) * p.rows_total;
+    __syncthreads();  // x^t complete
+    PHASE(0);
+
+    // (L1) consensus target t = x[l2g] + lambda / rho
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int r = tid + k * kThreads;
-      if (r < bd.rows) tgt[r] = xs[rm[k].xloc] + lam[k] / rho;
+      if (r < bd.rows) tgt[r] = xt[rm[k].xloc] + lr[k];  // lr = lambda / rho, same rounding
     }
     __syncthreads();
+    PHASE(1);
 
-    // (2b) z = P t + v, one row per thread, P column-major per subsystem
+    // (L2) z = P t + v, one row per thread, P column-major per subsystem
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int r = tid + k * kThreads;
       if (r < bd.rows) {
         const int n = rm[k].n;
-        const double* pr = sP + rm[k].pofs;
+        const double* pr = Pop + rm[k].pofs;
         const double* tb = tgt + rm[k].base;
         double acc = 0.0;
         int j = 0;
@@ -223,151 +316,176 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           acc = acc + p3 * tb[j + 3];
         }
         for (; j < n; ++j) acc = acc + pr[j * n] * tb[j];
-        zn[k] = acc + vv[k];
-        zs[r] = zn[k];
+        zs[r] = acc + vs[r];
       }
     }
     __syncthreads();
+    PHASE(2);
 
-    // (3) local equality residual ||A_s z_s - b_s||_inf
-    double mx = 0.0;
+    // (A) local equality residual ||A_s z_s - b_s||_inf
+    double v7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, obj, 0.0};
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int a = tid + k * kThreads;
       if (a < bd.arows) {
-        const int m = am[k].m, n = am[k].n;
-        const double* ar = sA + am[k].aofs;
-        const double* zb = zs + am[k].base;
+        const AMeta am = a_meta[a];
+        const int m = am.m, n = am.n;
+        const double* ar = Aop + am.aofs;
+        const double* zb = zs + am.base;
         double acc = 0.0;
         for (int j = 0; j < n; ++j) acc = acc + ar[j * m] * zb[j];
-        mx = sel_max(mx, fabs(acc - bb[k]));
+        v7[6] = sel_max(v7[6], fabs(acc - a_rhs[a]));
       }
     }
 
-    // (4) dual update, exchange value, residual partials
-    double gap = 0.0, step = 0.0, bx2 = 0.0, z2 = 0.0, l2 = 0.0;
+    // (D) dual update, exchange value, residual partials
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int r = tid + k * kThreads;
       if (r < bd.rows) {
-        const double z = zn[k];
-        const double bx = xs[rm[k].xloc];
+        const double z = zs[r];
+        const double bx = xt[rm[k].xloc];
         const double d = bx - z;
         const double ln = lam[k] + rho * d;
-        gap = gap + d * d;
+        v7[0] = v7[0] + d * d;
         const double dz = z - zp[k];
-        step = step + dz * dz;
-        bx2 = bx2 + bx * bx;
-        z2 = z2 + z * z;
-        l2 = l2 + ln * ln;
-        u_out[bd.row0 + r] = z - ln / rho;
+        v7[1] = v7[1] + dz * dz;
+        v7[2] = v7[2] + bx * bx;
+        v7[3] = v7[3] + z * z;
+        v7[4] = v7[4] + ln * ln;
+        lr[k] = ln / rho;  // reused as lambda/rho by the next target (admm.cpp:136)
+        u_out[bd.row0 + r] = z - lr[k];
+        // (z, lambda)^t to the parity-t result buffer: the stop decision for t
+        // arrives one iteration later, the buffer of t survives iteration t+1
+        z_res[bd.row0 + r] = z;
+        l_res[bd.row0 + r] = ln;
         lam[k] = ln;
         zp[k] = z;
       }
     }
+    __syncthreads();  // every u(t) store of this block issued
+    PHASE(3);
 
-    // (5) block reduction (fixed butterfly + fixed warp order)
-    double vals[7] = {gap, step, bx2, z2, l2, obj, mx};
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-      for (int q = 0; q < 6; ++q) vals[q] = vals[q] + __shfl_xor_sync(0xffffffffu, vals[q], off);
-      vals[6] = sel_max(vals[6], __shfl_xor_sync(0xffffffffu, vals[6], off));
-    }
+    // (F) publish u(t) (and, by program order, the slot of t-1)
+    if (mode == SyncMode::grid && tid == 0)
+      st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(it));
+
+    // (R) block reduction of the partials for t, off the critical path
+    warp_reduce7(v7, 32);
     if (lane == 0) {
 #pragma unroll
-      for (int q = 0; q < 7; ++q) red[warp * kPartials + q] = vals[q];
+      for (int q = 0; q < 7; ++q) red[warp * kPartials + q] = v7[q];
     }
     __syncthreads();
-    if (tid == 0) {
-      double s[7];
-#pragma unroll
-      for (int q = 0; q < 7; ++q) s[q] = red[q];
-      for (int w = 1; w < kWarps; ++w) {
-#pragma unroll
-        for (int q = 0; q < 6; ++q) s[q] = s[q] + red[w * kPartials + q];
-        s[6] = sel_max(s[6], red[w * kPartials + 6]);
-      }
-      double* dst = part + (static_cast<int64_t>(parity) * p.blocks_per_instance + bd.inst_block) * kPartials;
-#pragma unroll
-      for (int q = 0; q < 7; ++q) dst[q] = s[q];
-    }
-
-    // (6) one barrier per iteration
-    if (p.sync_mode == static_cast<int32_t>(SyncMode::grid))
-      grid_barrier(p.bar + bd.instance, static_cast<unsigned int>(G) * static_cast<unsigned int>(it));
-    else if (p.sync_mode == static_cast<int32_t>(SyncMode::cluster))
-      cluster_barrier();
-    else
-      __syncthreads();
-
-    // (7) combine the instance's partials (same order in every block)
     if (warp == 0) {
-      const double* src = part + static_cast<int64_t>(parity) * p.blocks_per_instance * kPartials;
-      double t[7] = {0, 0, 0, 0, 0, 0, 0};
-      for (int g = lane; g < G; g += 32) {
-        const double* row = src + g * kPartials;
+      double w7[7];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) t[q] = t[q] + ld_l2(row + q);
-        t[6] = sel_max(t[6], ld_l2(row + 6));
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-        for (int q = 0; q < 6; ++q) t[q] = t[q] + __shfl_xor_sync(0xffffffffu, t[q], off);
-        t[6] = sel_max(t[6], __shfl_xor_sync(0xffffffffu, t[6], off));
-      }
+      for (int q = 0; q < 7; ++q) w7[q] = lane < kWarps ? red[lane * kPartials + q] : 0.0;
+      warp_reduce7(w7, kWarps);
       if (lane == 0) {
+        double* my_slot = slots + static_cast<int64_t>(it % kSlots) * slot_stride +
+                          static_cast<int64_t>(bd.inst_block) * kPartials;
 #pragma unroll
-        for (int q = 0; q < 7; ++q) red[kWarps * kPartials + q] = t[q];
+        for (int q = 0; q < 7; ++q) my_slot[q] = w7[q];
+      }
+    }
+    PHASE(4);
+
+    // (W) wait until every block published u(t)
+    if (mode == SyncMode::grid) {
+      if (warp == 0) wait_flags(flags, G, lane, static_cast<unsigned long long>(it));
+      __syncthreads();
+    } else if (mode == SyncMode::cluster) {
+      cluster_barrier();
+    } else {
+      __syncthreads();
+    }
+    PHASE(5);
+
+    // (G) warps 1..: global update for t+1 || (S) warp 0: stop test for t-1
+    double obj_next = 0.0;
+    if (warp != 0) {
+      if (it < p.max_iter) obj_next = global_update(u_out, xnext);
+    } else if (it >= 2) {
+      double o, m;
+      const bool done = combine(it - 1, o, m);
+      if (lane == 0) {
+        red[kWarps * kPartials + 0] = done ? 1.0 : 0.0;
+        red[kWarps * kPartials + 1] = o;
+        red[kWarps * kPartials + 2] = m;
+      }
+    }
+    PHASE(6);
+    __syncthreads();
+    if (it >= 2) {
+      const double* dec = red + kWarps * kPartials;
+      last_obj = dec[1];
+      run_max = sel_max(run_max, dec[2]);
+      if (dec[0] != 0.0) {
+        stop_at = it - 1;
+        status = 0;
+        break;
+      }
+    }
+    // obj of x^{t+1}, reduced with the partials of t+1 (warp 0 holds none)
+    obj = obj_next;
+    PHASE(7);
+  }
+
+  if (stop_at == 0) {
+    // ran to max_iter: the residuals of the last iteration still need the
+    // slots of max_iter -> one more flag round, then combine.
+    it = p.max_iter;
+    if (mode == SyncMode::grid) {
+      if (tid == 0) st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(it + 1));
+      if (warp == 0) wait_flags(flags, G, lane, static_cast<unsigned long long>(it + 1));
+      __syncthreads();
+    } else if (mode == SyncMode::cluster) {
+      cluster_barrier();
+    } else {
+      __syncthreads();
+    }
+    if (warp == 0) {
+      double o, m;
+      const bool done = combine(it, o, m);
+      if (lane == 0) {
+        red[kWarps * kPartials + 0] = done ? 1.0 : 0.0;
+        red[kWarps * kPartials + 1] = o;
+        red[kWarps * kPartials + 2] = m;
       }
     }
     __syncthreads();
-    const double* tot = red + kWarps * kPartials;
-    const double pres = sqrt(tot[0]);
-    const double dres = rho * sqrt(tot[1]);
-    const double eps_prim = eps * sel_max(sqrt(tot[2]), sqrt(tot[3]));
-    const double eps_dual = eps * sqrt(tot[4]);
-    last_obj = tot[5];
-    run_max = sel_max(run_max, tot[6]);
-    if (leader && trace) {
-      double* row = trace + static_cast<int64_t>(it - 1) * 6;
-      row[0] = it;
-      row[1] = pres;
-      row[2] = dres;
-      row[3] = eps_prim;
-      row[4] = eps_dual;
-      row[5] = last_obj;
-    }
-    const bool done = pres <= eps_prim && dres <= eps_dual;
-    __syncthreads();  // everyone has read `tot` before the next iteration overwrites red[]
-    if (done) {
-      status = 0;
-      break;
-    }
+    const double* dec = red + kWarps * kPartials;
+    last_obj = dec[1];
+    run_max = sel_max(run_max, dec[2]);
+    status = dec[0] != 0.0 ? 0 : 1;
+    stop_at = it;
   }
-  const int iterations = it > p.max_iter ? p.max_iter : it;
+  if (prof_on)
+    for (int q = 0; q < 8; ++q) p.prof[q] = pacc[q];
 
+  // ---- results of iteration stop_at ----
+  // (z, lambda)^stop_at are in the result buffers of parity stop_at & 1 (the
+  // host reads them there); x^stop_at is still in the x ring.
+  const double* xfinal = xring + static_cast<std::size_t>((stop_at - 1) % 3) * bd.cols;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const int r = tid + k * kThreads;
-    if (r < bd.rows) {
-      p.z_out[bd.row0 + r] = zp[k];
-      p.lam_out[bd.row0 + r] = lam[k];
-    }
+    const int c = ctid + k * kColThreads;
+    if (ctid >= 0 && c < bd.cols && cm[k].owner) p.x_out[id.x_off + cm[k].gcol] = xfinal[c];
   }
   if (leader) {
-    p.iters[bd.instance] = iterations;
+    p.iters[bd.instance] = stop_at;
     p.status[bd.instance] = status;
     p.maxinf[bd.instance] = run_max;
     p.objective[bd.instance] = last_obj;
   }
 }
+#undef PHASE
 
-template <int K>
+template <int K, bool kSmemOps>
 cudaError_t launch_k(const KernelParams& p, int num_blocks, std::size_t smem, SyncMode mode,
                      int cluster_size, cudaStream_t stream) {
-  auto kern = admm_persistent<K>;
+  auto kern = admm_persistent<K, kSmemOps>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
@@ -400,15 +518,22 @@ cudaError_t launch_k(const KernelParams& p, int num_blocks, std::size_t smem, Sy
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
+template <int K>
+cudaError_t launch_ops(const KernelParams& p, int num_blocks, std::size_t smem, SyncMode mode,
+                       int cluster_size, bool smem_ops, cudaStream_t stream) {
+  return smem_ops ? launch_k<K, true>(p, num_blocks, smem, mode, cluster_size, stream)
+                  : launch_k<K, false>(p, num_blocks, smem, mode, cluster_size, stream);
+}
+
 }  // namespace
 
 cudaError_t launch_admm(const KernelParams& p, int num_blocks, int K, std::size_t smem,
-                        SyncMode mode, int cluster_size, cudaStream_t stream) {
+                        SyncMode mode, int cluster_size, bool smem_ops, cudaStream_t stream) {
   switch (K) {
-    case 1: return launch_k<1>(p, num_blocks, smem, mode, cluster_size, stream);
-    case 2: return launch_k<2>(p, num_blocks, smem, mode, cluster_size, stream);
-    case 3: return launch_k<3>(p, num_blocks, smem, mode, cluster_size, stream);
-    case 4: return launch_k<4>(p, num_blocks, smem, mode, cluster_size, stream);
+    case 1: return launch_ops<1>(p, num_blocks, smem, mode, cluster_size, smem_ops, stream);
+    case 2: return launch_ops<2>(p, num_blocks, smem, mode, cluster_size, smem_ops, stream);
+    case 3: return launch_ops<3>(p, num_blocks, smem, mode, cluster_size, smem_ops, stream);
+    case 4: return launch_ops<4>(p, num_blocks, smem, mode, cluster_size, smem_ops, stream);
     default: return cudaErrorInvalidValue;
   }
 }

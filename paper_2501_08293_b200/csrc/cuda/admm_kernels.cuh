@@ -31,9 +31,10 @@ struct KernelParams {
   double* z_out;        // [rows_total]
   double* lam_out;      // [rows_total]
   double* x_out;        // [x_total]
-  double* part;         // [instances][2][blocks_per_instance][kPartials]
-  unsigned int* bar;    // [instances] grid-barrier counters (grid mode)
+  double* part;         // [instances][3][blocks_per_instance][kPartials] residual slots
+  unsigned long long* flags;  // [instances][blocks_per_instance] "u(t) ready" (grid mode)
   double* trace;        // [instances][trace_stride][6] (may be null)
+  long long* prof;      // [8] phase cycle counters of CTA 0 (null: off)
   int32_t* iters;       // [instances]
   int32_t* status;      // [instances] 0 converged, 1 iteration limit
   double* maxinf;       // [instances]
@@ -51,7 +52,7 @@ struct KernelParams {
 /// Launches the persistent kernel: one CTA per block descriptor, all
 /// iterations on device until every instance converged or hit max_iter.
 cudaError_t launch_admm(const KernelParams& p, int num_blocks, int K, std::size_t smem_bytes,
-                        SyncMode mode, int cluster_size, cudaStream_t stream);
+                        SyncMode mode, int cluster_size, bool smem_ops, cudaStream_t stream);
 
 /// Largest dynamic shared memory the kernel may use on this device.
 int max_dynamic_smem(int device);

@@ -54,7 +54,7 @@ struct dopf_cuda_ctx {
   AMeta* d_ameta = nullptr;
   double* d_ab = nullptr;
   double *d_u = nullptr, *d_z = nullptr, *d_lam = nullptr, *d_x = nullptr, *d_part = nullptr;
-  unsigned int* d_bar = nullptr;
+  unsigned long long* d_flags = nullptr;
   int32_t *d_iters = nullptr, *d_status = nullptr;
   double *d_maxinf = nullptr, *d_obj = nullptr;
   double* d_trace = nullptr;
@@ -62,6 +62,8 @@ struct dopf_cuda_ctx {
 
   int64_t launches = 0;
   double last_kernel_s = 0;
+  bool profiling = false;
+  long long* d_prof = nullptr;
 
   void free_model() {
     for (void* p : allocs) cudaFree(p);
@@ -141,11 +143,11 @@ void upload_layout(dopf_cuda_ctx* c) {
   c->d_ab = c->put(L.ab);
   const std::size_t I = L.inst.size();
   c->d_u = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));
-  c->d_z = c->scratch<double>(L.rows_total);
-  c->d_lam = c->scratch<double>(L.rows_total);
+  c->d_z = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));    // [parity][row]
+  c->d_lam = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));
   c->d_x = c->scratch<double>(L.x_total);
-  c->d_part = c->scratch<double>(I * 2 * L.blocks_per_instance * kPartials);
-  c->d_bar = c->scratch<unsigned int>(I);
+  c->d_part = c->scratch<double>(I * 3 * L.blocks_per_instance * kPartials);
+  c->d_flags = c->scratch<unsigned long long>(I * L.blocks_per_instance);
   c->d_iters = c->scratch<int32_t>(I);
   c->d_status = c->scratch<int32_t>(I);
   c->d_maxinf = c->scratch<double>(I);
@@ -205,7 +207,10 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     c->trace_cap = need;
   }
   const auto t_up0 = std::chrono::steady_clock::now();
-  ck(cudaMemsetAsync(c->d_bar, 0, I * sizeof(unsigned int), c->stream), "memset");
+  ck(cudaMemsetAsync(c->d_flags, 0, I * L.blocks_per_instance * sizeof(unsigned long long), c->stream),
+     "memset");
+  ck(cudaMemsetAsync(c->d_part, 0, I * 3 * L.blocks_per_instance * kPartials * sizeof(double), c->stream),
+     "memset");
   ck(cudaMemcpyAsync(c->d_u, c->d_z0, L.rows_total * sizeof(double), cudaMemcpyDeviceToDevice,
                      c->stream),
      "u0");
@@ -231,8 +236,9 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.lam_out = c->d_lam;
   p.x_out = c->d_x;
   p.part = c->d_part;
-  p.bar = c->d_bar;
+  p.flags = c->d_flags;
   p.trace = want_trace ? c->d_trace : nullptr;
+  p.prof = c->profiling ? c->d_prof : nullptr;
   p.iters = c->d_iters;
   p.status = c->d_status;
   p.maxinf = c->d_maxinf;
@@ -246,7 +252,8 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.sync_mode = static_cast<int32_t>(c->mode);
 
   ck(cudaEventRecord(c->ev0, c->stream), "event");
-  ck(launch_admm(p, c->num_blocks, L.K, L.smem_bytes, c->mode, c->cluster, c->stream), "launch");
+  ck(launch_admm(p, c->num_blocks, L.K, L.smem_bytes, c->mode, c->cluster, L.all_ops_in_smem, c->stream),
+     "launch");
   ck(cudaEventRecord(c->ev1, c->stream), "event");
   ++c->launches;
   ck(cudaEventSynchronize(c->ev1), "kernel");
@@ -267,8 +274,9 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   for (int i = 0; i < count; ++i)
     any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
   if (copy_vectors && any_vec) {
-    zdev.resize(L.rows_total);
-    ldev.resize(L.rows_total);
+    // both parity buffers: instance i's final iterate sits in parity iters[i] & 1
+    zdev.resize(2 * static_cast<std::size_t>(L.rows_total));
+    ldev.resize(2 * static_cast<std::size_t>(L.rows_total));
     xall.resize(L.x_total);
     ck(cudaMemcpy(zdev.data(), c->d_z, zdev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
     ck(cudaMemcpy(ldev.data(), c->d_lam, ldev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
@@ -285,10 +293,11 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     r.time_global = r.time_local = r.time_dual = 0.0;
     if (copy_vectors && any_vec) {
       if (r.x) std::memcpy(r.x, xall.data() + id.x_off, sizeof(double) * id.n);
+      const std::size_t base = (iters[i] & 1) * static_cast<std::size_t>(L.rows_total);
       for (int32_t d = id.row0; d < id.row0 + id.rows; ++d) {
         const int32_t ref = L.ref_of_dev[d];
-        if (r.z) r.z[ref] = zdev[d];
-        if (r.lambda) r.lambda[ref] = ldev[d];
+        if (r.z) r.z[ref] = zdev[base + d];
+        if (r.lambda) r.lambda[ref] = ldev[base + d];
       }
     }
     if (r.trace && iters[i] > 0)
@@ -417,5 +426,27 @@ double dopf_cuda_bytes_per_iteration(const dopf_cuda_ctx* c) {
 }
 
 double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* c) { return c ? c->last_kernel_s : 0.0; }
+
+int dopf_cuda_set_profiling(dopf_cuda_ctx* c, int32_t on) {
+  if (!c) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (on && !c->d_prof) {
+      ck(cudaMalloc(&c->d_prof, 8 * sizeof(long long)), "cudaMalloc");
+      ck(cudaMemset(c->d_prof, 0, 8 * sizeof(long long)), "memset");
+    }
+    c->profiling = on != 0;
+  });
+}
+
+int dopf_cuda_phase_cycles(const dopf_cuda_ctx* c, int64_t* out8) {
+  if (!c || !out8) return DOPF_ERR_INVALID_ARGUMENT;
+  if (!c->d_prof) {
+    for (int q = 0; q < 8; ++q) out8[q] = 0;
+    return DOPF_OK;
+  }
+  return guarded(const_cast<dopf_cuda_ctx*>(c), [&] {
+    ck(cudaMemcpy(out8, c->d_prof, 8 * sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
+  });
+}
 
 }  // extern "C"

@@ -36,15 +36,14 @@ std::vector<int> split_points(const dopf_model_view& m, int G) {
 }  // namespace
 
 std::size_t block_smem_bytes(const BlockDesc& b, bool ops_in_smem) {
-  std::size_t bytes = 0;
-  if (ops_in_smem) bytes += 8ull * (static_cast<std::size_t>(b.p_len) + b.a_len);
-  bytes += 16ull * b.rows;        // target, z
-  bytes += 8ull * b.cols;         // x
-  bytes += 40ull * b.cols;        // c/rho, inv, lo, hi, c
-  bytes += 4ull * b.copy_len;     // copy list
-  bytes = (bytes + 15) & ~std::size_t(15);
-  bytes += 8ull * kPartials * (kThreads / 32 + 2) + 256;  // reduction scratch
-  return bytes;
+  // must match the carve-up at the top of admm_persistent
+  std::size_t doubles = 0;
+  if (ops_in_smem) doubles += static_cast<std::size_t>(b.p_len) + b.a_len;
+  doubles += 3ull * b.rows;                     // target, z, v
+  doubles += 8ull * b.cols;                     // x (three buffers), c/rho, inv, lo, hi, c
+  doubles += (kThreads / 32 + 2ull) * kPartials;  // reduction scratch
+  doubles += 3ull * b.arows;                    // equality rows: rhs + AMeta (16 B)
+  return 8 * doubles + 4ull * b.copy_len + 64;
 }
 
 double algorithmic_bytes(const dopf_model_view& m) {
@@ -71,20 +70,23 @@ double algorithmic_flops(const dopf_model_view& m) {
 
 int choose_blocks(const dopf_model_view& m, const LayoutOptions& opt) {
   if (opt.blocks_per_instance > 0) return opt.blocks_per_instance;
-  // Estimate per-block smem for a given G from totals; refine by trial.
-  const int rows_cap = opt.threads * kMaxK;
-  for (int G = 1; G <= opt.max_blocks; G = (G < 8 ? G + 1 : G + (G < 64 ? 8 : 16))) {
-    if (G > m.S) break;
+  // Lower bound on the CTA count from the instance's total shared-memory
+  // footprint and row count, then the smallest G <= 8 (one cluster) whose
+  // blocks all fit; larger instances take one CTA per SM.
+  double bytes = 0;
+  for (int s = 0; s < m.S; ++s) {
+    const double n = ns_of(m, s);
+    bytes += 8.0 * (n * n + m.m_s[s] * n) + 16.0 * n + 4.0 * n;
+  }
+  bytes += 56.0 * m.n;
+  const int rows_cap = opt.threads * 2;
+  int g0 = static_cast<int>(bytes / (0.92 * static_cast<double>(opt.smem_limit))) + 1;
+  g0 = std::max(g0, (m.N_z + rows_cap - 1) / rows_cap);
+  g0 = std::max(1, std::min(g0, std::max(1, m.S)));
+  for (int G = g0; G <= 8 && G <= m.S; ++G) {
     HostLayout trial;
-    LayoutOptions o = opt;
-    add_instance(trial, m, G, o);
-    bool ok = trial.all_ops_in_smem;
-    for (const auto& b : trial.blocks) ok = ok && b.rows <= rows_cap;
-    if (ok && trial.K <= 2) return G;
-    if (ok && G >= 8 && trial.K <= kMaxK) {
-      // large instance: use the whole GPU for parallelism
-      return std::min(opt.max_blocks, m.S);
-    }
+    add_instance(trial, m, G, opt);
+    if (trial.all_ops_in_smem && trial.K <= 2) return G;
   }
   return std::min(opt.max_blocks, std::max(1, m.S));
 }
@@ -206,7 +208,8 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     if (!bd.ops_in_smem) L.all_ops_in_smem = false;
     L.smem_bytes = std::max(L.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
     const int k_rows = (bd.rows + opt.threads - 1) / opt.threads;
-    L.K = std::max(L.K, std::max(1, k_rows));
+    const int k_cols = (bd.cols + opt.threads - 33) / (opt.threads - 32);  // warps 1.. own columns
+    L.K = std::max(L.K, std::max(1, std::max(k_rows, k_cols)));
     L.blocks.push_back(bd);
   }
   L.blocks_per_instance = std::max(L.blocks_per_instance, nb);

@@ -532,7 +532,8 @@ class CudaSolver:
         i = N.BatchInfo_t()
         self._err(self._lib.dopf_cuda_info(self._h, C.byref(i)))
         return {"instances": i.instances, "blocks": i.blocks, "threads": i.threads,
-                "smem_bytes": i.smem_bytes, "resident": bool(i.resident)}
+                "smem_bytes": i.smem_bytes, "resident": bool(i.resident),
+                "sync": {0: "block", 1: "cluster", 2: "grid"}.get(i.sync_mode, "?")}
 
     def kernel_launches(self) -> int:
         return int(self._lib.dopf_cuda_kernel_launches(self._h))
