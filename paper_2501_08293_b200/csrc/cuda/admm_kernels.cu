@@ -1,33 +1,35 @@
 // Persistent fp64 ADMM iteration kernel for sm_100a.
 //
 // One launch runs the whole loop of reference proj/src/admm.cpp:190-235 on
-// the device. Per iteration t and per CTA ("block": a contiguous range of
-// subsystems, layout.hpp):
+// the device. Each CTA ("block", a contiguous range of subsystems,
+// layout.hpp) is warp-specialised:
 //
-//   (L) local update, admm.cpp:131-138 (K1): t = x[l2g] + lambda/rho,
-//       z = P t + v as a sequential-j dot product per row; P staged in shared
-//       memory once per launch (or read from HBM when it does not fit).
+//  compute warps 1..15, per iteration t
+//   (L) local update, admm.cpp:131-138 (K1): target = x[l2g] + lambda/rho,
+//       z = P target + v, a sequential-j dot product per row; P staged in
+//       shared memory once per launch (or read from HBM when it does not fit).
 //   (A) ||A_s z_s - b_s||_inf, admm.cpp:203-205.
-//   (D) dual update, admm.cpp:140-143, exchange value u = z - lambda/rho,
-//       per-thread residual partial sums, admm.cpp:150-163.
-//   (F) publish: thread 0 releases the block's "u(t) ready" flag right after
-//       the u stores -- this is the only inter-CTA synchronisation of the
-//       iteration (cluster mode: the hardware cluster barrier instead).
-//   (R) while other blocks catch up: warp-shuffle block reduction of the
-//       residual partials (fixed order) into the block's slot for t. The slot
-//       becomes visible to other blocks through the NEXT flag release, so
-//       residual reduction is entirely off the critical path.
-//   (W) warp 0 polls every block's flag (acquire).
-//   (G) warps 1..15: global update for t+1, admm.cpp:118-129 (K2): for every
-//       column the block's rows reference, acc = sum of u over its copies in
+//   (D) dual update, admm.cpp:140-143; exchange value u = z - lambda/rho;
+//       per-warp residual partials, admm.cpp:150-163.
+//   --- arrive(publish) / sync(exchanged) with the service warp ---
+//   (G) global update for t+1, admm.cpp:118-129 (K2): for every column the
+//       block's rows reference, acc = sum of u over the column's copies in
 //       ascending s (L2 reads), x = clamp((acc - c/rho) * inv, lo, hi). Shared
-//       columns are computed redundantly (bitwise identical) by each block
+//       columns are computed redundantly (bitwise identical) by every block
 //       that needs them, so x is never broadcast.
-//   (S) concurrently warp 0: combines every block's slot of t-1 in a fixed
-//       order -> residuals, trace row, stop test (admm.hpp:63). The decision
-//       for t-1 is taken one iteration late; the state of t-1 (x in a 3-deep
-//       ring, z and lambda in registers) is kept so the result is exactly the
-//       reference's iterate at its stopping iteration.
+//
+//  service warp 0, per iteration t
+//   (F) after the compute warps' u(t) stores: release the block's flag(t) --
+//       the only inter-CTA synchronisation of the iteration;
+//   (R) reduce the 15 warp partials in a fixed order into the block's slot(t);
+//   (W) poll every block's flag(t) (relaxed loads + one acquire fence), then
+//       let the compute warps start (G);
+//   (S) combine all blocks' slots of t-1 (published before their flag(t)) in a
+//       fixed order: residuals, trace row, stop test (admm.hpp:63). The compute
+//       warps read the decision for t-2 after the exchange of t, so residual
+//       work never sits on the critical path. State of the last two
+//       iterations is kept (x in a 3-deep ring, z/lambda in 3 result buffers),
+//       so the output is exactly the iterate of the stopping iteration.
 //
 // Bitwise parity with the CPU oracle: compiled with --fmad=false; every
 // iterate operation keeps the reference's form (division by rho, multiply by
@@ -41,18 +43,24 @@ namespace dopf::cuda {
 namespace {
 
 constexpr int kWarps = kThreads / 32;
-constexpr int kColThreads = kThreads - 32;  // warps 1.. own the global-update columns
-constexpr int kSlots = 3;                   // partial-slot ring depth (see header comment)
+constexpr int kCW = kThreads - 32;  // compute threads (warps 1..)
+constexpr int kSlots = 3;           // partial-slot ring (see header)
+constexpr int kDec = 4;             // decision ring
+enum : int { kBarCompute = 1, kBarPublish = 2, kBarExchanged = 3 };
 
 __device__ __forceinline__ double ld_l2(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ double sel_max(double a, double b) { return (a < b) ? b : a; }  // std::max
 __device__ __forceinline__ double sel_min(double a, double b) { return (b < a) ? b : a; }  // std::min
 
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// Relaxed poll (no per-poll L1 invalidation); one acquire fence after the
-// flag was observed orders the subsequent loads (fence-acquire pattern).
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -60,7 +68,8 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-// Warp 0 waits until every block of the instance published flag >= value.
+// Warp 0: wait until every block of the instance published flag >= value
+// (relaxed polls, then one acquire fence for the whole warp).
 __device__ __forceinline__ void wait_flags(const unsigned long long* flags, int G, int lane,
                                            unsigned long long value) {
   for (int g = lane; g < G; g += 32)
@@ -68,13 +77,6 @@ __device__ __forceinline__ void wait_flags(const unsigned long long* flags, int 
     }
   fence_acq_rel();
   __syncwarp();
-}
-
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile(
-      "barrier.cluster.arrive.release.aligned;\n\t"
-      "barrier.cluster.wait.acquire.aligned;\n" ::
-          : "memory");
 }
 
 // 7 reduction lanes: 0..5 sums (gap, step, bx2, z2, lam2, objective), 6 max.
@@ -130,8 +132,10 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   off += bd.cols;
   double* c_cost = smem + off;
   off += bd.cols;
-  double* red = smem + off;  // [kWarps][kPartials] + decision words
-  off += (kWarps + 2) * kPartials;
+  double* red = smem + off;  // [kWarps][kPartials] warp partials
+  off += kWarps * kPartials;
+  double* dec = smem + off;  // [kDec][4]: done, objective, running max, spare
+  off += kDec * 4;
   double* a_rhs = smem + off;  // equality-row rhs b_r
   off += bd.arows;
   AMeta* a_meta = reinterpret_cast<AMeta*>(smem + off);  // 16 B each
@@ -139,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   int32_t* cps = reinterpret_cast<int32_t*>(smem + off);
 
   const double rho = p.rho;
+  const double eps = p.eps_rel;
   for (int i = tid; i < bd.copy_len; i += kThreads) cps[i] = p.copies[bd.copy_off + i];
   for (int r = tid; r < bd.rows; r += kThreads) vs[r] = p.v[bd.row0 + r];
   for (int a = tid; a < bd.arows; a += kThreads) {
@@ -153,334 +158,272 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
     c_lo[c] = p.clo[bd.col_off + c];
     c_hi[c] = p.chi[bd.col_off + c];
   }
+  if (tid < kDec * 4) dec[tid] = 0.0;
 
-  // ---- per-thread state in registers ----
-  // rows r = tid + k*kThreads; A-rows likewise; columns c = (tid-32) + k*kColThreads
-  RowMeta rm[K];
-  ColMeta cm[K];
-  double lam[K], lr[K], zp[K];
-  const int ctid = tid - 32;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int r = tid + k * kThreads;
-    if (r < bd.rows) {
-      rm[k] = p.rmeta[bd.row0 + r];
-      zp[k] = p.z0[bd.row0 + r];
-    } else {
-      rm[k] = RowMeta{0, 0, 0, 0};
-      zp[k] = 0.0;
-    }
-    lam[k] = 0.0;
-    lr[k] = 0.0 / rho;  // lambda^0 / rho
-    const int c = ctid + k * kColThreads;
-    cm[k] = (ctid >= 0 && c < bd.cols) ? p.cmeta[bd.col_off + c] : ColMeta{0, 0, 0, 0};
-  }
-  __syncthreads();
-
-  const double eps = p.eps_rel;
   const int G = id.blocks;
   const int64_t slot_stride = static_cast<int64_t>(p.blocks_per_instance) * kPartials;
   double* slots = p.part + static_cast<int64_t>(bd.instance) * kSlots * slot_stride;
   unsigned long long* flags = p.flags + static_cast<int64_t>(bd.instance) * p.blocks_per_instance;
   double* u_buf[2] = {p.u, p.u + p.rows_total};
   double* trace = p.trace ? p.trace + static_cast<int64_t>(bd.instance) * p.trace_stride * 6 : nullptr;
-  const bool leader = bd.inst_block == 0 && tid == 0;
   const SyncMode mode = static_cast<SyncMode>(p.sync_mode);
+  const bool exchange = mode != SyncMode::block;  // flags needed across CTAs
+  __syncthreads();
 
-  // (G) global update from u_in into xdst (warps 1..); returns c'x share of owned columns
-  auto global_update = [&](const double* u_in, double* xdst) -> double {
-    double obj = 0.0;
-    if (ctid < 0) return obj;
-    double a[K][4];
+  int stop_at = 0;  // set by the branch that detects the stop; broadcast below
+  if (warp == 0) {
+    // ======================= service warp =======================
+    const bool leader = bd.inst_block == 0 && lane == 0;
+    double run_max = 0.0;
+    // combine every block's slot of iteration s in a fixed order
+    auto combine = [&](int s) {
+      const double* base = slots + static_cast<int64_t>(s % kSlots) * slot_stride;
+      double t7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      for (int g0 = lane; g0 < G; g0 += 64) {  // two slots per lane in flight
+        const int g1 = g0 + 32;
+        const double* r0 = base + g0 * kPartials;
+        const double* r1 = base + g1 * kPartials;
+        double a0[7], a1[7];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {  // issue the first (up to) 4 copy loads of every column
-      const int c = ctid + k * kColThreads;
-      const int cnt = c < bd.cols ? cm[k].copy_count : 0;
-      const int32_t* q = cps + cm[k].copy_start;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) a[k][e] = e < cnt ? ld_l2(u_in + q[e]) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int c = ctid + k * kColThreads;
-      if (c < bd.cols) {
-        const int cnt = cm[k].copy_count;
-        const int32_t* q = cps + cm[k].copy_start;
-        double acc = 0.0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (e < cnt) acc = acc + a[k][e];
-        for (int e = 4; e < cnt; ++e) acc = acc + ld_l2(u_in + q[e]);
-        const double unclamped = (acc - c_rho[c]) * c_inv[c];
-        const double xv = sel_min(sel_max(unclamped, c_lo[c]), c_hi[c]);
-        xdst[c] = xv;
-        if (cm[k].owner) obj = obj + c_cost[c] * xv;
-      }
-    }
-    return obj;
-  };
-
-  // (S) warp 0: combine every block's slot for iteration s (fixed order), write
-  // the trace row, return the stop decision (all blocks decide identically).
-  auto combine = [&](int s, double& obj_s, double& mx_s) -> bool {
-    const double* base = slots + static_cast<int64_t>(s % kSlots) * slot_stride;
-    double t7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int g0 = lane; g0 < G; g0 += 64) {  // two slots per lane in flight
-      const int g1 = g0 + 32;
-      const double* r0 = base + g0 * kPartials;
-      const double* r1 = base + g1 * kPartials;
-      double a0[7], a1[7];
-#pragma unroll
-      for (int q = 0; q < 7; ++q) {
-        a0[q] = ld_l2(r0 + q);
-        a1[q] = g1 < G ? ld_l2(r1 + q) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a0[q];
-      t7[6] = sel_max(t7[6], a0[6]);
-      if (g1 < G) {
-#pragma unroll
-        for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a1[q];
-        t7[6] = sel_max(t7[6], a1[6]);
-      }
-    }
-    warp_reduce7(t7, 32);
-    const double pres = sqrt(t7[0]);
-    const double dres = rho * sqrt(t7[1]);
-    const double eps_prim = eps * sel_max(sqrt(t7[2]), sqrt(t7[3]));
-    const double eps_dual = eps * sqrt(t7[4]);
-    if (leader && trace) {
-      double* row = trace + static_cast<int64_t>(s - 1) * 6;
-      row[0] = s;
-      row[1] = pres;
-      row[2] = dres;
-      row[3] = eps_prim;
-      row[4] = eps_dual;
-      row[5] = t7[5];
-    }
-    obj_s = t7[5];
-    mx_s = t7[6];
-    return pres <= eps_prim && dres <= eps_dual;
-  };
-
-  // optional phase clock (thread 0 of CTA 0): cycles spent between markers
-  const bool prof_on = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
-  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tlast = clock64();
-#define PHASE(i)                      \
-  if (prof_on) {                      \
-    const long long tnow = clock64(); \
-    pacc[i] += tnow - tlast;          \
-    tlast = tnow;                     \
-  }
-
-  double obj = global_update(u_buf[0], xring);  // x^1 from u^0 = z^0
-  double run_max = 0.0, last_obj = 0.0;
-  int status = 1;
-  int stop_at = 0;  // converged iteration, 0 while running
-  int it = 1;
-  for (; it <= p.max_iter; ++it) {
-    const double* xt = xring + static_cast<std::size_t>((it - 1) % 3) * bd.cols;  // x^t
-    double* xnext = xring + static_cast<std::size_t>(it % 3) * bd.cols;            // x^{t+1}
-    double* u_out = u_buf[it & 1];
-    double* z_res = p.z_out + (it & 1) * p.rows_total;
-    double* l_res = p.lam_out + (it & 1) * p.rows_total;
-    __syncthreads();  // x^t complete
-    PHASE(0);
-
-    // (L1) consensus target t = x[l2g] + lambda / rho
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int r = tid + k * kThreads;
-      if (r < bd.rows) tgt[r] = xt[rm[k].xloc] + lr[k];  // lr = lambda / rho, same rounding
-    }
-    __syncthreads();
-    PHASE(1);
-
-    // (L2) z = P t + v, one row per thread, P column-major per subsystem
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int r = tid + k * kThreads;
-      if (r < bd.rows) {
-        const int n = rm[k].n;
-        const double* pr = Pop + rm[k].pofs;
-        const double* tb = tgt + rm[k].base;
-        double acc = 0.0;
-        int j = 0;
-        for (; j + 4 <= n; j += 4) {
-          const double p0 = pr[(j + 0) * n], p1 = pr[(j + 1) * n];
-          const double p2 = pr[(j + 2) * n], p3 = pr[(j + 3) * n];
-          acc = acc + p0 * tb[j];
-          acc = acc + p1 * tb[j + 1];
-          acc = acc + p2 * tb[j + 2];
-          acc = acc + p3 * tb[j + 3];
+        for (int q = 0; q < 7; ++q) {
+          a0[q] = ld_l2(r0 + q);
+          a1[q] = g1 < G ? ld_l2(r1 + q) : 0.0;
         }
-        for (; j < n; ++j) acc = acc + pr[j * n] * tb[j];
-        zs[r] = acc + vs[r];
-      }
-    }
-    __syncthreads();
-    PHASE(2);
-
-    // (A) local equality residual ||A_s z_s - b_s||_inf
-    double v7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, obj, 0.0};
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int a = tid + k * kThreads;
-      if (a < bd.arows) {
-        const AMeta am = a_meta[a];
-        const int m = am.m, n = am.n;
-        const double* ar = Aop + am.aofs;
-        const double* zb = zs + am.base;
-        double acc = 0.0;
-        for (int j = 0; j < n; ++j) acc = acc + ar[j * m] * zb[j];
-        v7[6] = sel_max(v7[6], fabs(acc - a_rhs[a]));
-      }
-    }
-
-    // (D) dual update, exchange value, residual partials
+        for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a0[q];
+        t7[6] = sel_max(t7[6], a0[6]);
+        if (g1 < G) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int r = tid + k * kThreads;
-      if (r < bd.rows) {
-        const double z = zs[r];
-        const double bx = xt[rm[k].xloc];
-        const double d = bx - z;
-        const double ln = lam[k] + rho * d;
-        v7[0] = v7[0] + d * d;
-        const double dz = z - zp[k];
-        v7[1] = v7[1] + dz * dz;
-        v7[2] = v7[2] + bx * bx;
-        v7[3] = v7[3] + z * z;
-        v7[4] = v7[4] + ln * ln;
-        lr[k] = ln / rho;  // reused as lambda/rho by the next target (admm.cpp:136)
-        u_out[bd.row0 + r] = z - lr[k];
-        // (z, lambda)^t to the parity-t result buffer: the stop decision for t
-        // arrives one iteration later, the buffer of t survives iteration t+1
-        z_res[bd.row0 + r] = z;
-        l_res[bd.row0 + r] = ln;
-        lam[k] = ln;
-        zp[k] = z;
+          for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a1[q];
+          t7[6] = sel_max(t7[6], a1[6]);
+        }
       }
-    }
-    __syncthreads();  // every u(t) store of this block issued
-    PHASE(3);
+      warp_reduce7(t7, 32);
+      const double pres = sqrt(t7[0]);
+      const double dres = rho * sqrt(t7[1]);
+      const double eps_prim = eps * sel_max(sqrt(t7[2]), sqrt(t7[3]));
+      const double eps_dual = eps * sqrt(t7[4]);
+      run_max = sel_max(run_max, t7[6]);
+      if (lane == 0) {
+        double* rec = dec + (s % kDec) * 4;
+        rec[0] = (pres <= eps_prim && dres <= eps_dual) ? 1.0 : 0.0;
+        rec[1] = t7[5];
+        rec[2] = run_max;
+        if (leader && trace) {
+          double* row = trace + static_cast<int64_t>(s - 1) * 6;
+          row[0] = s;
+          row[1] = pres;
+          row[2] = dres;
+          row[3] = eps_prim;
+          row[4] = eps_dual;
+          row[5] = t7[5];
+        }
+      }
+      __syncwarp();
+    };
+    auto publish_and_wait = [&](int value) {
+      if (!exchange) return;
+      if (lane == 0) st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(value));
+      wait_flags(flags, G, lane, static_cast<unsigned long long>(value));
+    };
 
-    // (F) publish u(t) (and, by program order, the slot of t-1)
-    if (mode == SyncMode::grid && tid == 0)
-      st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(it));
-
-    // (R) block reduction of the partials for t, off the critical path
-    warp_reduce7(v7, 32);
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 7; ++q) red[warp * kPartials + q] = v7[q];
-    }
-    __syncthreads();
-    if (warp == 0) {
+    int t = 1;
+    for (;; ++t) {
+      named_sync(kBarPublish, kThreads);  // compute warps: u(t) stored, warp partials in red[]
+      if (exchange && lane == 0)
+        st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(t));
+      // (R) fixed-order reduction of the 15 warp partials -> slot(t)
       double w7[7];
 #pragma unroll
-      for (int q = 0; q < 7; ++q) w7[q] = lane < kWarps ? red[lane * kPartials + q] : 0.0;
+      for (int q = 0; q < 7; ++q) w7[q] = (lane >= 1 && lane < kWarps) ? red[lane * kPartials + q] : 0.0;
       warp_reduce7(w7, kWarps);
       if (lane == 0) {
-        double* my_slot = slots + static_cast<int64_t>(it % kSlots) * slot_stride +
+        double* my_slot = slots + static_cast<int64_t>(t % kSlots) * slot_stride +
                           static_cast<int64_t>(bd.inst_block) * kPartials;
 #pragma unroll
         for (int q = 0; q < 7; ++q) my_slot[q] = w7[q];
       }
+      // (W) every block's u(t) is visible
+      if (exchange) wait_flags(flags, G, lane, static_cast<unsigned long long>(t));
+      const bool cw_stop = (t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter;
+      named_arrive(kBarExchanged, kThreads);
+      // (S) residuals / stop test of t-1 (slots published before flag(t))
+      if (t >= 2) combine(t - 1);
+      if (cw_stop) break;
     }
-    PHASE(4);
-
-    // (W) wait until every block published u(t)
-    if (mode == SyncMode::grid) {
-      if (warp == 0) wait_flags(flags, G, lane, static_cast<unsigned long long>(it));
-      __syncthreads();
-    } else if (mode == SyncMode::cluster) {
-      cluster_barrier();
+    if (t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) {
+      stop_at = t - 2;
     } else {
-      __syncthreads();
+      // reached max_iter: the slots of max_iter become visible with one more flag
+      publish_and_wait(t + 1);
+      combine(t);
+      stop_at = (t >= 2 && dec[((t - 1) % kDec) * 4] != 0.0) ? t - 1 : t;
     }
-    PHASE(5);
-
-    // (G) warps 1..: global update for t+1 || (S) warp 0: stop test for t-1
-    double obj_next = 0.0;
-    if (warp != 0) {
-      if (it < p.max_iter) obj_next = global_update(u_out, xnext);
-    } else if (it >= 2) {
-      double o, m;
-      const bool done = combine(it - 1, o, m);
-      if (lane == 0) {
-        red[kWarps * kPartials + 0] = done ? 1.0 : 0.0;
-        red[kWarps * kPartials + 1] = o;
-        red[kWarps * kPartials + 2] = m;
+    if (lane == 0) {
+      const double* rec = dec + (stop_at % kDec) * 4;
+      red[0] = stop_at;
+      if (bd.inst_block == 0) {
+        p.iters[bd.instance] = stop_at;
+        p.status[bd.instance] = rec[0] != 0.0 ? 0 : 1;
+        p.maxinf[bd.instance] = rec[2];
+        p.objective[bd.instance] = rec[1];
       }
     }
-    PHASE(6);
-    __syncthreads();
-    if (it >= 2) {
-      const double* dec = red + kWarps * kPartials;
-      last_obj = dec[1];
-      run_max = sel_max(run_max, dec[2]);
-      if (dec[0] != 0.0) {
-        stop_at = it - 1;
-        status = 0;
-        break;
-      }
-    }
-    // obj of x^{t+1}, reduced with the partials of t+1 (warp 0 holds none)
-    obj = obj_next;
-    PHASE(7);
-  }
-
-  if (stop_at == 0) {
-    // ran to max_iter: the residuals of the last iteration still need the
-    // slots of max_iter -> one more flag round, then combine.
-    it = p.max_iter;
-    if (mode == SyncMode::grid) {
-      if (tid == 0) st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(it + 1));
-      if (warp == 0) wait_flags(flags, G, lane, static_cast<unsigned long long>(it + 1));
-      __syncthreads();
-    } else if (mode == SyncMode::cluster) {
-      cluster_barrier();
-    } else {
-      __syncthreads();
-    }
-    if (warp == 0) {
-      double o, m;
-      const bool done = combine(it, o, m);
-      if (lane == 0) {
-        red[kWarps * kPartials + 0] = done ? 1.0 : 0.0;
-        red[kWarps * kPartials + 1] = o;
-        red[kWarps * kPartials + 2] = m;
-      }
-    }
-    __syncthreads();
-    const double* dec = red + kWarps * kPartials;
-    last_obj = dec[1];
-    run_max = sel_max(run_max, dec[2]);
-    status = dec[0] != 0.0 ? 0 : 1;
-    stop_at = it;
-  }
-  if (prof_on)
-    for (int q = 0; q < 8; ++q) p.prof[q] = pacc[q];
-
-  // ---- results of iteration stop_at ----
-  // (z, lambda)^stop_at are in the result buffers of parity stop_at & 1 (the
-  // host reads them there); x^stop_at is still in the x ring.
-  const double* xfinal = xring + static_cast<std::size_t>((stop_at - 1) % 3) * bd.cols;
+  } else {
+    // ======================= compute warps =======================
+    const int ctid = tid - 32;
+    RowMeta rm[K];
+    ColMeta cm[K];
+    double lam[K], lr[K], zp[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int c = ctid + k * kColThreads;
-    if (ctid >= 0 && c < bd.cols && cm[k].owner) p.x_out[id.x_off + cm[k].gcol] = xfinal[c];
+    for (int k = 0; k < K; ++k) {
+      const int r = ctid + k * kCW;
+      if (r < bd.rows) {
+        rm[k] = p.rmeta[bd.row0 + r];
+        zp[k] = p.z0[bd.row0 + r];
+      } else {
+        rm[k] = RowMeta{0, 0, 0, 0};
+        zp[k] = 0.0;
+      }
+      lam[k] = 0.0;
+      lr[k] = 0.0 / rho;  // lambda^0 / rho
+      cm[k] = r < bd.cols ? p.cmeta[bd.col_off + r] : ColMeta{0, 0, 0, 0};
+    }
+
+    // (G) global update from u_in into xdst; returns the c'x share of owned columns
+    auto global_update = [&](const double* u_in, double* xdst) -> double {
+      double obj = 0.0;
+      double a[K][4];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {  // issue the first (up to) 4 copy loads of every column
+        const int c = ctid + k * kCW;
+        const int cnt = c < bd.cols ? cm[k].copy_count : 0;
+        const int32_t* q = cps + cm[k].copy_start;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a[k][e] = e < cnt ? ld_l2(u_in + q[e]) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = ctid + k * kCW;
+        if (c < bd.cols) {
+          const int cnt = cm[k].copy_count;
+          const int32_t* q = cps + cm[k].copy_start;
+          double acc = 0.0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (e < cnt) acc = acc + a[k][e];
+          for (int e = 4; e < cnt; ++e) acc = acc + ld_l2(u_in + q[e]);
+          const double unclamped = (acc - c_rho[c]) * c_inv[c];
+          const double xv = sel_min(sel_max(unclamped, c_lo[c]), c_hi[c]);
+          xdst[c] = xv;
+          if (cm[k].owner) obj = obj + c_cost[c] * xv;
+        }
+      }
+      return obj;
+    };
+
+    double obj = global_update(u_buf[0], xring);  // x^1 from u^0 = z^0
+    named_sync(kBarCompute, kCW);
+    for (int t = 1;; ++t) {
+      const double* xt = xring + static_cast<std::size_t>((t - 1) % 3) * bd.cols;  // x^t
+      double* u_out = u_buf[t & 1];
+      double* z_res = p.z_out + static_cast<int64_t>(t % 3) * p.rows_total;
+      double* l_res = p.lam_out + static_cast<int64_t>(t % 3) * p.rows_total;
+
+      // (L1) consensus target
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int r = ctid + k * kCW;
+        if (r < bd.rows) tgt[r] = xt[rm[k].xloc] + lr[k];  // lr = lambda / rho, same rounding
+      }
+      named_sync(kBarCompute, kCW);
+
+      // (L2) z = P t + v, one row per thread, P column-major per subsystem
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int r = ctid + k * kCW;
+        if (r < bd.rows) {
+          const int n = rm[k].n;
+          const double* pr = Pop + rm[k].pofs;
+          const double* tb = tgt + rm[k].base;
+          double acc = 0.0;
+          int j = 0;
+          for (; j + 4 <= n; j += 4) {
+            const double p0 = pr[(j + 0) * n], p1 = pr[(j + 1) * n];
+            const double p2 = pr[(j + 2) * n], p3 = pr[(j + 3) * n];
+            acc = acc + p0 * tb[j];
+            acc = acc + p1 * tb[j + 1];
+            acc = acc + p2 * tb[j + 2];
+            acc = acc + p3 * tb[j + 3];
+          }
+          for (; j < n; ++j) acc = acc + pr[j * n] * tb[j];
+          zs[r] = acc + vs[r];
+        }
+      }
+      named_sync(kBarCompute, kCW);
+
+      // (A) local equality residual ||A_s z_s - b_s||_inf
+      double v7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, obj, 0.0};
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int a = ctid + k * kCW;
+        if (a < bd.arows) {
+          const AMeta am = a_meta[a];
+          const double* ar = Aop + am.aofs;
+          const double* zb = zs + am.base;
+          double acc = 0.0;
+          for (int j = 0; j < am.n; ++j) acc = acc + ar[j * am.m] * zb[j];
+          v7[6] = sel_max(v7[6], fabs(acc - a_rhs[a]));
+        }
+      }
+      // (D) dual update, exchange value, residual partials
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int r = ctid + k * kCW;
+        if (r < bd.rows) {
+          const double z = zs[r];
+          const double bx = xt[rm[k].xloc];
+          const double d = bx - z;
+          const double ln = lam[k] + rho * d;
+          v7[0] = v7[0] + d * d;
+          const double dz = z - zp[k];
+          v7[1] = v7[1] + dz * dz;
+          v7[2] = v7[2] + bx * bx;
+          v7[3] = v7[3] + z * z;
+          v7[4] = v7[4] + ln * ln;
+          lr[k] = ln / rho;  // reused as lambda/rho by the next target (admm.cpp:136)
+          u_out[bd.row0 + r] = z - lr[k];
+          z_res[bd.row0 + r] = z;   // (z, lambda)^t kept until the stop test of t is known
+          l_res[bd.row0 + r] = ln;
+          lam[k] = ln;
+          zp[k] = z;
+        }
+      }
+      warp_reduce7(v7, 32);
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 7; ++q) red[warp * kPartials + q] = v7[q];
+      }
+      named_arrive(kBarPublish, kThreads);
+      named_sync(kBarExchanged, kThreads);
+      if ((t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter) break;
+      obj = global_update(u_out, xring + static_cast<std::size_t>(t % 3) * bd.cols);  // x^{t+1}
+      named_sync(kBarCompute, kCW);
+    }
   }
-  if (leader) {
-    p.iters[bd.instance] = stop_at;
-    p.status[bd.instance] = status;
-    p.maxinf[bd.instance] = run_max;
-    p.objective[bd.instance] = last_obj;
+  __syncthreads();
+  stop_at = static_cast<int>(red[0]);
+  if (warp != 0) {
+    // owners write x^stop_at (still in the ring); (z, lambda)^stop_at are in
+    // result buffer stop_at % 3, which the host reads
+    const int ctid = tid - 32;
+    const double* xfinal = xring + static_cast<std::size_t>((stop_at - 1) % 3) * bd.cols;
+    for (int c = ctid; c < bd.cols; c += kCW) {
+      const ColMeta cmc = p.cmeta[bd.col_off + c];
+      if (cmc.owner) p.x_out[id.x_off + cmc.gcol] = xfinal[c];
+    }
   }
 }
-#undef PHASE
 
 template <int K, bool kSmemOps>
 cudaError_t launch_k(const KernelParams& p, int num_blocks, std::size_t smem, SyncMode mode,

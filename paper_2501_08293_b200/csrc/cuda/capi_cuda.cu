@@ -143,8 +143,8 @@ void upload_layout(dopf_cuda_ctx* c) {
   c->d_ab = c->put(L.ab);
   const std::size_t I = L.inst.size();
   c->d_u = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));
-  c->d_z = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));    // [parity][row]
-  c->d_lam = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));
+  c->d_z = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));    // [t % 3][row]
+  c->d_lam = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));
   c->d_x = c->scratch<double>(L.x_total);
   c->d_part = c->scratch<double>(I * 3 * L.blocks_per_instance * kPartials);
   c->d_flags = c->scratch<unsigned long long>(I * L.blocks_per_instance);
@@ -274,9 +274,9 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   for (int i = 0; i < count; ++i)
     any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
   if (copy_vectors && any_vec) {
-    // both parity buffers: instance i's final iterate sits in parity iters[i] & 1
-    zdev.resize(2 * static_cast<std::size_t>(L.rows_total));
-    ldev.resize(2 * static_cast<std::size_t>(L.rows_total));
+    // all three result buffers: instance i's final iterate sits in buffer iters[i] % 3
+    zdev.resize(3 * static_cast<std::size_t>(L.rows_total));
+    ldev.resize(3 * static_cast<std::size_t>(L.rows_total));
     xall.resize(L.x_total);
     ck(cudaMemcpy(zdev.data(), c->d_z, zdev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
     ck(cudaMemcpy(ldev.data(), c->d_lam, ldev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
@@ -293,7 +293,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     r.time_global = r.time_local = r.time_dual = 0.0;
     if (copy_vectors && any_vec) {
       if (r.x) std::memcpy(r.x, xall.data() + id.x_off, sizeof(double) * id.n);
-      const std::size_t base = (iters[i] & 1) * static_cast<std::size_t>(L.rows_total);
+      const std::size_t base = (iters[i] % 3) * static_cast<std::size_t>(L.rows_total);
       for (int32_t d = id.row0; d < id.row0 + id.rows; ++d) {
         const int32_t ref = L.ref_of_dev[d];
         if (r.z) r.z[ref] = zdev[base + d];

@@ -41,7 +41,7 @@ std::size_t block_smem_bytes(const BlockDesc& b, bool ops_in_smem) {
   if (ops_in_smem) doubles += static_cast<std::size_t>(b.p_len) + b.a_len;
   doubles += 3ull * b.rows;                     // target, z, v
   doubles += 8ull * b.cols;                     // x (three buffers), c/rho, inv, lo, hi, c
-  doubles += (kThreads / 32 + 2ull) * kPartials;  // reduction scratch
+  doubles += (kThreads / 32ull) * kPartials + 16;  // warp partials + decision ring
   doubles += 3ull * b.arows;                    // equality rows: rhs + AMeta (16 B)
   return 8 * doubles + 4ull * b.copy_len + 64;
 }
@@ -79,7 +79,7 @@ int choose_blocks(const dopf_model_view& m, const LayoutOptions& opt) {
     bytes += 8.0 * (n * n + m.m_s[s] * n) + 16.0 * n + 4.0 * n;
   }
   bytes += 56.0 * m.n;
-  const int rows_cap = opt.threads * 2;
+  const int rows_cap = (opt.threads - 32) * 2;
   int g0 = static_cast<int>(bytes / (0.92 * static_cast<double>(opt.smem_limit))) + 1;
   g0 = std::max(g0, (m.N_z + rows_cap - 1) / rows_cap);
   g0 = std::max(1, std::min(g0, std::max(1, m.S)));
@@ -207,9 +207,10 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     bd.ops_in_smem = block_smem_bytes(bd, true) <= opt.smem_limit ? 1 : 0;
     if (!bd.ops_in_smem) L.all_ops_in_smem = false;
     L.smem_bytes = std::max(L.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
-    const int k_rows = (bd.rows + opt.threads - 1) / opt.threads;
-    const int k_cols = (bd.cols + opt.threads - 33) / (opt.threads - 32);  // warps 1.. own columns
-    L.K = std::max(L.K, std::max(1, std::max(k_rows, k_cols)));
+    // warps 1.. (opt.threads - 32 threads) own rows, columns and equality rows
+    const int cw = opt.threads - 32;
+    const int k_need = (std::max(bd.rows, std::max(bd.cols, bd.arows)) + cw - 1) / cw;
+    L.K = std::max(L.K, std::max(1, k_need));
     L.blocks.push_back(bd);
   }
   L.blocks_per_instance = std::max(L.blocks_per_instance, nb);
