@@ -54,6 +54,19 @@ int oracle_check_feasibility(const dopf_lp_view* lp, const double* x, double* ma
 int oracle_reconstruct(const dopf_model_view* model, const double* x, const double* z,
                        double* out);
 
+/* Single iteration steps (admm_steps.cpp), for the reference's per-function
+ * known-answer tests (proj/tests/test_admm.cpp:113-303). */
+int oracle_global_update(const dopf_model_view* model, const double* z, const double* lambda,
+                         double rho, double* x);
+int oracle_local_update(const dopf_model_view* model, int32_t s, const double* x,
+                        const double* lambda_s, double rho, double* z_s);
+int oracle_dual_update(const dopf_model_view* model, int32_t s, const double* x,
+                       const double* z_s, double* lambda_s, double rho);
+/* out4 = {pres, dres, eps_prim, eps_dual} */
+int oracle_residuals(const dopf_model_view* model, const double* x, const double* z,
+                     const double* z_prev, const double* lambda, double rho, double eps_rel,
+                     double* out4);
+
 #ifdef __cplusplus
 }
 #endif

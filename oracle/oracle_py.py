@@ -37,6 +37,13 @@ def lib():
                                                P(N.i32), P(N.i32), P(N.f64)]
         L.oracle_reconstruct.restype = C.c_int
         L.oracle_reconstruct.argtypes = [P(N.ModelView_t), P(N.f64), P(N.f64), P(N.f64)]
+        L.oracle_global_update.argtypes = [P(N.ModelView_t), P(N.f64), P(N.f64), N.f64, P(N.f64)]
+        L.oracle_local_update.argtypes = [P(N.ModelView_t), N.i32, P(N.f64), P(N.f64), N.f64,
+                                          P(N.f64)]
+        L.oracle_dual_update.argtypes = [P(N.ModelView_t), N.i32, P(N.f64), P(N.f64), P(N.f64),
+                                         N.f64]
+        L.oracle_residuals.argtypes = [P(N.ModelView_t), P(N.f64), P(N.f64), P(N.f64), P(N.f64),
+                                       N.f64, N.f64, P(N.f64)]
         _lib = L
     return _lib
 
@@ -112,3 +119,41 @@ def reconstruct_centralized(model: "dopf.DecomposedModel", x, z):
     out = np.zeros(model.global_cols)
     lib().oracle_reconstruct(C.byref(model.view()), _p(x), _p(z), _p(out))
     return out
+
+
+def _f(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def global_update(model, z, lam, rho):
+    """x from the copies (admm.cpp:118-129)."""
+    x = np.zeros(model.global_cols)
+    z, lam = _f(z), _f(lam)
+    assert lib().oracle_global_update(C.byref(model.view()), _p(z), _p(lam), rho, _p(x)) == 0
+    return x
+
+
+def local_update(model, s, x, lam_s, rho):
+    """z_s = P_s (x[l2g] + lambda_s / rho) + v_s (admm.cpp:131-138)."""
+    zo = model.z_offsets
+    out = np.zeros(int(zo[s + 1] - zo[s]))
+    x, lam_s = _f(x), _f(lam_s)
+    assert lib().oracle_local_update(C.byref(model.view()), s, _p(x), _p(lam_s), rho, _p(out)) == 0
+    return out
+
+
+def dual_update(model, s, x, z_s, lam_s, rho):
+    """lambda_s + rho (x[l2g] - z_s) (admm.cpp:140-143); returns the new lambda_s."""
+    lam = _f(lam_s).copy()
+    x, z_s = _f(x), _f(z_s)
+    assert lib().oracle_dual_update(C.byref(model.view()), s, _p(x), _p(z_s), _p(lam), rho) == 0
+    return lam
+
+
+def residuals(model, x, z, z_prev, lam, rho, eps_rel):
+    """(pres, dres, eps_prim, eps_dual) (admm.cpp:145-170)."""
+    out = np.zeros(4)
+    x, z, z_prev, lam = _f(x), _f(z), _f(z_prev), _f(lam)
+    assert lib().oracle_residuals(C.byref(model.view()), _p(x), _p(z), _p(z_prev), _p(lam), rho,
+                                  eps_rel, _p(out)) == 0
+    return tuple(float(v) for v in out)
