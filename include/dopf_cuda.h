@@ -68,11 +68,30 @@ double dopf_cuda_bytes_per_iteration(const dopf_cuda_ctx* ctx);
 /* Device time (seconds) of the last solve's kernel, CUDA events on the
  * launching stream. */
 double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* ctx);
-/* Phase clock: when enabled, CTA 0 records SM cycles spent in each of the 8
- * loop phases (top wait, target, GEMV, equality+dual, reduce, exchange,
- * global update, combine) during the next solves. */
+/* Phase clock: when enabled (counters reset), every CTA records the SM cycles
+ * spent in each of the 8 loop phases during the next solves: compute warps --
+ * target, GEMV, dual + publish, equality check + partial reductions, exchange
+ * wait, global update; service warp -- neighbour-flag wait, all-flag wait +
+ * residual combine. out receives [min(max_blocks, CTAs)][8] counters. */
 int dopf_cuda_set_profiling(dopf_cuda_ctx* ctx, int32_t on);
-int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out8);
+int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out, int32_t max_blocks);
+
+/* Device layout of one model, computed on the host only (no GPU needed):
+ * what dopf_cuda_upload would build for a device with `max_blocks` SMs and
+ * `smem_limit` bytes of opt-in shared memory per CTA. */
+typedef struct dopf_layout_stats {
+  int32_t blocks;          /* CTAs for the instance                          */
+  int32_t rows_per_thread; /* K: rows (and columns) per compute thread       */
+  int32_t resident;        /* 1: every block's operators fit shared memory   */
+  int32_t max_neighbours;  /* most blocks any block shares columns with      */
+  int64_t smem_bytes;      /* largest block's shared-memory footprint        */
+  int64_t remote_copies;   /* copy reads that cross blocks, per iteration    */
+  int64_t local_copies;    /* copy reads served from the block's own rows    */
+  int64_t exported_rows;   /* rows whose u is stored to global memory        */
+  double bytes_per_iteration; /* algorithmic bytes     */
+} dopf_layout_stats;
+int dopf_layout_probe(const dopf_model_view* model, int32_t max_blocks, int64_t smem_limit,
+                      dopf_layout_stats* out);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,12 @@ class LpView_t(C.Structure):
                 ("c", P(f64)), ("x_lo", P(f64)), ("x_hi", P(f64)), ("var_kind", P(i32))]
 
 
+class LayoutStats_t(C.Structure):
+    _fields_ = [("blocks", i32), ("rows_per_thread", i32), ("resident", i32),
+                ("max_neighbours", i32), ("smem_bytes", i64), ("remote_copies", i64),
+                ("local_copies", i64), ("exported_rows", i64), ("bytes_per_iteration", f64)]
+
+
 class BatchInfo_t(C.Structure):
     _fields_ = [("instances", i32), ("blocks", i32), ("threads", i32), ("smem_bytes", i32),
                 ("resident", i32), ("sync_mode", i32)]
@@ -125,7 +131,8 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_bytes_per_iteration", f64, vp)
     _sig(lib, "dopf_cuda_last_kernel_seconds", f64, vp)
     _sig(lib, "dopf_cuda_set_profiling", C.c_int, vp, i32)
-    _sig(lib, "dopf_cuda_phase_cycles", C.c_int, vp, P(i64))
+    _sig(lib, "dopf_cuda_phase_cycles", C.c_int, vp, P(i64), i32)
+    _sig(lib, "dopf_layout_probe", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))
     _cuda = lib
     return lib
 

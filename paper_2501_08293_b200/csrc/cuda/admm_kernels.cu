@@ -1,35 +1,54 @@
 // Persistent fp64 ADMM iteration kernel for sm_100a.
 //
 // One launch runs the whole loop of reference proj/src/admm.cpp:190-235 on
-// the device. Each CTA ("block", a contiguous range of subsystems,
-// layout.hpp) is warp-specialised:
+// the device. Each CTA ("block": a piece of the depth-first walk of the
+// component graph, layout.hpp) is warp-specialised:
 //
 //  compute warps 1..15, per iteration t
 //   (L) local update, admm.cpp:131-138 (K1): target = x[l2g] + lambda/rho,
-//       z = P target + v, a sequential-j dot product per row; P staged in
-//       shared memory once per launch (or read from HBM when it does not fit).
-//   (A) ||A_s z_s - b_s||_inf, admm.cpp:203-205.
-//   (D) dual update, admm.cpp:140-143; exchange value u = z - lambda/rho;
-//       per-warp residual partials, admm.cpp:150-163.
-//   --- arrive(publish) / sync(exchanged) with the service warp ---
+//       z = P target + v, a sequential-j dot product per row (the K rows of a
+//       thread are interleaved for ILP); P staged in shared memory once per
+//       launch (or read from HBM/L2 when it does not fit).
+//   (D) dual update, admm.cpp:140-143, and the exchange value
+//       u = z - lambda/rho, kept in shared memory; rows another block reads
+//       ("exported") are also stored to global memory.
+//   --- arrive(publish): the service warp releases this block's flag(t) ---
+//   (A) ||A_s z_s - b_s||_inf (admm.cpp:203-205) and the residual partial
+//       sums (admm.cpp:150-163) -- off the critical path, overlapping the
+//       exchange.
+//   --- sync(exchanged): every neighbour block published u(t) ---
 //   (G) global update for t+1, admm.cpp:118-129 (K2): for every column the
 //       block's rows reference, acc = sum of u over the column's copies in
-//       ascending s (L2 reads), x = clamp((acc - c/rho) * inv, lo, hi). Shared
-//       columns are computed redundantly (bitwise identical) by every block
-//       that needs them, so x is never broadcast.
+//       ascending s (own copies from shared memory, a neighbour's from L2),
+//       x = clamp((acc - c/rho) * inv, lo, hi). Shared columns are computed
+//       redundantly (bitwise identical) by every block that needs them, so x
+//       is never broadcast.
 //
 //  service warp 0, per iteration t
-//   (F) after the compute warps' u(t) stores: release the block's flag(t) --
-//       the only inter-CTA synchronisation of the iteration;
-//   (R) reduce the 15 warp partials in a fixed order into the block's slot(t);
-//   (W) poll every block's flag(t) (relaxed loads + one acquire fence), then
-//       let the compute warps start (G);
-//   (S) combine all blocks' slots of t-1 (published before their flag(t)) in a
-//       fixed order: residuals, trace row, stop test (admm.hpp:63). The compute
-//       warps read the decision for t-2 after the exchange of t, so residual
-//       work never sits on the critical path. State of the last two
-//       iterations is kept (x in a 3-deep ring, z/lambda in 3 result buffers),
-//       so the output is exactly the iterate of the stopping iteration.
+//   (F) after the compute warps' u(t) stores: release the block's flag(t);
+//   (R) reduce the 15 warp partials in a fixed order into the block's slot(t)
+//       and count it in the instance's slot counter (red.release.gpu.add);
+//   (W) poll the NEIGHBOURS' flag(t) (one relaxed load per lane, then one
+//       acquire fence) and fetch the decision record of t-2, then let the
+//       compute warps start (G);
+//   (S) leader CTA only: once the counter shows every block's slot of t-1,
+//       combine them in a fixed order (residuals, trace row, stop test,
+//       admm.hpp:63) and publish the decision record of t-1. One poller per
+//       instance instead of an all-to-all flag scan keeps L2 quiet. The
+//       compute warps act on the decision for t-2 after the exchange of t, so
+//       the residual reduction never sits on the critical path. State of the
+//       last iterations is kept (x in a 3-deep ring, z/lambda in 3 result
+//       buffers), so the output is exactly the iterate of the stopping
+//       iteration.
+//
+// Memory ordering of the exchange: compute warps store u(t) (plain st.global),
+// bar.arrive(publish) synchronises with the service warp's bar.sync, whose
+// lane 0 then does st.release.gpu of flag(t) (cumulative release). A reader
+// observes flag >= t with relaxed loads, executes fence.acq_rel.gpu, then
+// bar.arrive(exchanged) -> the compute warps' bar.sync; their ld.global.cg of
+// u(t) follow. Remote u is double-buffered by iteration parity: a block
+// overwrites u(t) (at t+2) only after seeing every neighbour's flag(t+1),
+// i.e. after each neighbour finished reading u(t).
 //
 // Bitwise parity with the CPU oracle: compiled with --fmad=false; every
 // iterate operation keeps the reference's form (division by rho, multiply by
@@ -45,8 +64,12 @@ namespace {
 constexpr int kWarps = kThreads / 32;
 constexpr int kCW = kThreads - 32;  // compute threads (warps 1..)
 constexpr int kSlots = 3;           // partial-slot ring (see header)
-constexpr int kDec = 4;             // decision ring
-enum : int { kBarCompute = 1, kBarPublish = 2, kBarExchanged = 3 };
+constexpr int kDec = 4;             // decision ring (shared memory)
+constexpr int kDecG = 8;            // decision ring (global, written by the leader CTA)
+constexpr int kLine = 16;           // u64 words per 128-byte line: flags are one per line
+enum : int { kBarCompute = 1, kBarPublish = 2, kBarExchanged = 3, kBarPartials = 4 };
+// phase clock slots (per CTA): compute warp 1 lane 0, service lane 0
+enum : int { kPhTarget = 0, kPhGemv, kPhDual, kPhEqRed, kPhWait, kPhGlobal, kPhSvcNbr, kPhSvcAll };
 
 __device__ __forceinline__ double ld_l2(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ double sel_max(double a, double b) { return (a < b) ? b : a; }  // std::max
@@ -66,28 +89,63 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-// Warp 0: wait until every block of the instance published flag >= value
-// (relaxed polls, then one acquire fence for the whole warp).
-__device__ __forceinline__ void wait_flags(const unsigned long long* flags, int G, int lane,
-                                           unsigned long long value) {
-  for (int g = lane; g < G; g += 32)
-    while (ld_relaxed_u64(flags + g) < value) {
+// Warp 0: wait for the neighbour blocks (lane q watches neighbour q; the
+// layout guarantees at most 32 neighbours).
+__device__ __forceinline__ void wait_nbr_flags(const unsigned long long* flags, int my_nbr, int lane,
+                                               int cnt, unsigned long long value) {
+  if (lane < cnt)
+    while (ld_relaxed_u64(flags + my_nbr) < value) {
     }
   fence_acq_rel();
   __syncwarp();
 }
 
-// 7 reduction lanes: 0..5 sums (gap, step, bx2, z2, lam2, objective), 6 max.
-__device__ __forceinline__ void warp_reduce7(double (&v)[7], int width) {
+// Sums of 8 values over the 32 lanes of a warp by recursive halving (9
+// double shuffles instead of 40). On return lane L holds the total of value
+// index sum8_index(L); the four lanes sharing an index hold identical bits
+// (every step is a commutative a + b). Fixed pattern => deterministic.
+__device__ __forceinline__ int sum8_index(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+__device__ __forceinline__ int sum8_lane(int index) {
+  return ((index >> 2) & 1) * 16 + ((index >> 1) & 1) * 8 + (index & 1) * 4;
+}
+__device__ __forceinline__ double sum8(const double (&v)[8], int lane) {
+  double w[4];
+  const bool h1 = (lane >> 4) & 1;
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    if (off >= width) continue;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) v[q] = v[q] + __shfl_xor_sync(0xffffffffu, v[q], off);
-    v[6] = sel_max(v[6], __shfl_xor_sync(0xffffffffu, v[6], off));
+  for (int q = 0; q < 4; ++q) {
+    const double keep = h1 ? v[q + 4] : v[q];
+    const double send = h1 ? v[q] : v[q + 4];
+    w[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
+  const bool h2 = (lane >> 3) & 1;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const double keep = h2 ? w[q + 2] : w[q];
+    const double send = h2 ? w[q] : w[q + 2];
+    w[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const bool h3 = (lane >> 2) & 1;
+  double x = (h3 ? w[1] : w[0]) + __shfl_xor_sync(0xffffffffu, h3 ? w[0] : w[1], 4);
+  x = x + __shfl_xor_sync(0xffffffffu, x, 2);
+  x = x + __shfl_xor_sync(0xffffffffu, x, 1);
+  return x;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = sel_max(v, __shfl_xor_sync(0xffffffffu, v, off));
+  return v;
 }
 
 template <int K, bool kSmemOps>
@@ -114,14 +172,15 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   }
   const double* Pop = kSmemOps ? sP : gP;
   const double* Aop = kSmemOps ? sA : gA;
-  double* tgt = smem + off;
+  // tu: GEMV target during (L), then the exchange value u from (D) to (G)
+  double* tu = smem + off;
   off += bd.rows;
   double* zs = smem + off;
   off += bd.rows;
   double* vs = smem + off;
   off += bd.rows;
-  double* xring = smem + off;  // [3][cols]
-  off += 3 * static_cast<std::size_t>(bd.cols);
+  double* xring = smem + off;  // [4][cols]: x^s in slot s % 4
+  off += 4 * static_cast<std::size_t>(bd.cols);
   double* c_rho = smem + off;
   off += bd.cols;
   double* c_inv = smem + off;
@@ -132,10 +191,12 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   off += bd.cols;
   double* c_cost = smem + off;
   off += bd.cols;
-  double* red = smem + off;  // [kWarps][kPartials] warp partials
-  off += kWarps * kPartials;
+  double* red = smem + off;  // [2][kWarps][kPartials] warp partials, by iteration parity
+  off += 2 * kWarps * kPartials;
   double* dec = smem + off;  // [kDec][4]: done, objective, running max, spare
   off += kDec * 4;
+  long long* ph = reinterpret_cast<long long*>(smem + off);  // [8] phase clock
+  off += 8;
   double* a_rhs = smem + off;  // equality-row rhs b_r
   off += bd.arows;
   AMeta* a_meta = reinterpret_cast<AMeta*>(smem + off);  // 16 B each
@@ -145,7 +206,10 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   const double rho = p.rho;
   const double eps = p.eps_rel;
   for (int i = tid; i < bd.copy_len; i += kThreads) cps[i] = p.copies[bd.copy_off + i];
-  for (int r = tid; r < bd.rows; r += kThreads) vs[r] = p.v[bd.row0 + r];
+  for (int r = tid; r < bd.rows; r += kThreads) {
+    vs[r] = p.v[bd.row0 + r];
+    tu[r] = p.z0[bd.row0 + r];  // u^0 = z^0 - 0/rho
+  }
   for (int a = tid; a < bd.arows; a += kThreads) {
     a_meta[a] = p.ameta[bd.amet_off + a];
     a_rhs[a] = p.ab[bd.amet_off + a];
@@ -159,174 +223,269 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
     c_hi[c] = p.chi[bd.col_off + c];
   }
   if (tid < kDec * 4) dec[tid] = 0.0;
+  if (tid < 8) ph[tid] = 0;
 
   const int G = id.blocks;
   const int64_t slot_stride = static_cast<int64_t>(p.blocks_per_instance) * kPartials;
   double* slots = p.part + static_cast<int64_t>(bd.instance) * kSlots * slot_stride;
-  unsigned long long* flags = p.flags + static_cast<int64_t>(bd.instance) * p.blocks_per_instance;
-  double* u_buf[2] = {p.u, p.u + p.rows_total};
+  unsigned long long* flags =
+      p.flags + static_cast<int64_t>(bd.instance) * p.blocks_per_instance * kLine;
+  unsigned long long* ctl = p.ctl + static_cast<int64_t>(bd.instance) * kCtlWords;
   double* trace = p.trace ? p.trace + static_cast<int64_t>(bd.instance) * p.trace_stride * 6 : nullptr;
   const SyncMode mode = static_cast<SyncMode>(p.sync_mode);
   const bool exchange = mode != SyncMode::block;  // flags needed across CTAs
+  const bool clock_on = p.prof != nullptr;
   __syncthreads();
 
   int stop_at = 0;  // set by the branch that detects the stop; broadcast below
+  double m_fold[4] = {0.0, 0.0, 0.0, 0.0};  // compute threads: infeasibility ring at exit
+  int thread_last = 0;                      // compute threads: last iteration executed
   if (warp == 0) {
     // ======================= service warp =======================
-    const bool leader = bd.inst_block == 0 && lane == 0;
-    double run_max = 0.0;
-    // combine every block's slot of iteration s in a fixed order
+    const bool leader_cta = bd.inst_block == 0;  // the instance's residual combiner
+    const int my_nbr = lane < bd.nbr_cnt ? p.nbrs[bd.nbr_off + lane] : 0;
+    const bool tick = clock_on && lane == 0;
+    unsigned long long* counter = ctl;            // slots published, G per iteration
+    unsigned long long* decw = ctl + kLine;       // [kDecG] (s << 1) | stop
+    double* dec_obj = reinterpret_cast<double*>(ctl + 2 * kLine);  // [kDecG] objective
+    // (S, leader CTA) combine every block's slot of iteration s in a fixed
+    // order; publish the decision word and the objective of s
     auto combine = [&](int s) {
+      if (exchange) {
+        if (lane == 0)
+          while (ld_acquire_u64(counter) < static_cast<unsigned long long>(G) * s) {
+          }
+        __syncwarp();
+      }
       const double* base = slots + static_cast<int64_t>(s % kSlots) * slot_stride;
-      double t7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      double t8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       for (int g0 = lane; g0 < G; g0 += 64) {  // two slots per lane in flight
         const int g1 = g0 + 32;
         const double* r0 = base + g0 * kPartials;
         const double* r1 = base + g1 * kPartials;
-        double a0[7], a1[7];
+        double a0[6], a1[6];
 #pragma unroll
-        for (int q = 0; q < 7; ++q) {
+        for (int q = 0; q < 6; ++q) {
           a0[q] = ld_l2(r0 + q);
           a1[q] = g1 < G ? ld_l2(r1 + q) : 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a0[q];
-        t7[6] = sel_max(t7[6], a0[6]);
+        for (int q = 0; q < 6; ++q) t8[q] = t8[q] + a0[q];
         if (g1 < G) {
 #pragma unroll
-          for (int q = 0; q < 6; ++q) t7[q] = t7[q] + a1[q];
-          t7[6] = sel_max(t7[6], a1[6]);
+          for (int q = 0; q < 6; ++q) t8[q] = t8[q] + a1[q];
         }
       }
-      warp_reduce7(t7, 32);
-      const double pres = sqrt(t7[0]);
-      const double dres = rho * sqrt(t7[1]);
-      const double eps_prim = eps * sel_max(sqrt(t7[2]), sqrt(t7[3]));
-      const double eps_dual = eps * sqrt(t7[4]);
-      run_max = sel_max(run_max, t7[6]);
+      const double mine = sum8(t8, lane);
+      double tot[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) tot[q] = __shfl_sync(0xffffffffu, mine, sum8_lane(q));
       if (lane == 0) {
-        double* rec = dec + (s % kDec) * 4;
-        rec[0] = (pres <= eps_prim && dres <= eps_dual) ? 1.0 : 0.0;
-        rec[1] = t7[5];
-        rec[2] = run_max;
-        if (leader && trace) {
+        const double pres = sqrt(tot[0]);
+        const double dres = rho * sqrt(tot[1]);
+        const double eps_prim = eps * sel_max(sqrt(tot[2]), sqrt(tot[3]));
+        const double eps_dual = eps * sqrt(tot[4]);
+        const bool stop = pres <= eps_prim && dres <= eps_dual;
+        dec_obj[s % kDecG] = tot[5];
+        if (trace) {
           double* row = trace + static_cast<int64_t>(s - 1) * 6;
           row[0] = s;
           row[1] = pres;
           row[2] = dres;
           row[3] = eps_prim;
           row[4] = eps_dual;
-          row[5] = t7[5];
+          row[5] = tot[5];
         }
+        st_release_u64(decw + s % kDecG, (static_cast<unsigned long long>(s) << 1) | (stop ? 1ull : 0ull));
       }
       __syncwarp();
     };
-    auto publish_and_wait = [&](int value) {
-      if (!exchange) return;
-      if (lane == 0) st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(value));
-      wait_flags(flags, G, lane, static_cast<unsigned long long>(value));
+    // stop bit of iteration s -> the block's shared-memory ring (lane 0)
+    auto fetch = [&](int s) {
+      if (lane == 0) {
+        unsigned long long w;
+        do {
+          w = ld_acquire_u64(decw + s % kDecG);
+        } while ((w >> 1) != static_cast<unsigned long long>(s));
+        dec[(s % kDec) * 4] = (w & 1ull) ? 1.0 : 0.0;
+      }
+      __syncwarp();
     };
 
     int t = 1;
     for (;; ++t) {
-      named_sync(kBarPublish, kThreads);  // compute warps: u(t) stored, warp partials in red[]
-      if (exchange && lane == 0)
-        st_release_u64(flags + bd.inst_block, static_cast<unsigned long long>(t));
-      // (R) fixed-order reduction of the 15 warp partials -> slot(t)
-      double w7[7];
-#pragma unroll
-      for (int q = 0; q < 7; ++q) w7[q] = (lane >= 1 && lane < kWarps) ? red[lane * kPartials + q] : 0.0;
-      warp_reduce7(w7, kWarps);
-      if (lane == 0) {
-        double* my_slot = slots + static_cast<int64_t>(t % kSlots) * slot_stride +
-                          static_cast<int64_t>(bd.inst_block) * kPartials;
-#pragma unroll
-        for (int q = 0; q < 7; ++q) my_slot[q] = w7[q];
-      }
-      // (W) every block's u(t) is visible
-      if (exchange) wait_flags(flags, G, lane, static_cast<unsigned long long>(t));
+      named_sync(kBarPublish, kThreads);  // compute warps: u(t) stored
+      if (exchange && lane == 0) st_release_u64(flags + bd.inst_block * kLine, static_cast<unsigned long long>(t));
+      // (W) every neighbour's u(t) is visible; decision of t-2 -- overlaps the
+      // compute warps' interior update, equality check and reductions
+      const long long c0 = tick ? clock64() : 0;
+      if (exchange) wait_nbr_flags(flags, my_nbr * kLine, lane, bd.nbr_cnt, static_cast<unsigned long long>(t));
+      if (t >= 3) fetch(t - 2);
+      const long long c1 = tick ? clock64() : 0;
+      named_sync(kBarPartials, kThreads);  // warp partials of t in red[t & 1]
       const bool cw_stop = (t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter;
       named_arrive(kBarExchanged, kThreads);
-      // (S) residuals / stop test of t-1 (slots published before flag(t))
-      if (t >= 2) combine(t - 1);
+      // (R) fixed-order reduction of the 15 warp partials -> slot(t), counted
+      {
+        const double* rb = red + (t & 1) * kWarps * kPartials;
+        double w8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w8[q] = (lane >= 1 && lane < kWarps && q < 6) ? rb[lane * kPartials + q] : 0.0;
+        const double mine = sum8(w8, lane);
+        double* my_slot = slots + static_cast<int64_t>(t % kSlots) * slot_stride +
+                          static_cast<int64_t>(bd.inst_block) * kPartials;
+        if ((lane & 3) == 0 && sum8_index(lane) < 6) my_slot[sum8_index(lane)] = mine;
+        __syncwarp();
+        if (exchange && lane == 0) {
+          __threadfence();  // the other lanes' slot stores, then the counted release
+          red_release_add_u64(counter, 1ull);
+        }
+      }
+      if (leader_cta && t >= 2) combine(t - 1);  // residuals / stop test of t-1
+      if (tick) {
+        ph[kPhSvcNbr] += c1 - c0;
+        ph[kPhSvcAll] += clock64() - c1;
+      }
       if (cw_stop) break;
     }
     if (t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) {
       stop_at = t - 2;
     } else {
-      // reached max_iter: the slots of max_iter become visible with one more flag
-      publish_and_wait(t + 1);
-      combine(t);
+      // reached max_iter: decide between t-1 and t
+      if (leader_cta) combine(t);
+      if (t >= 2) fetch(t - 1);
+      fetch(t);
       stop_at = (t >= 2 && dec[((t - 1) % kDec) * 4] != 0.0) ? t - 1 : t;
     }
     if (lane == 0) {
-      const double* rec = dec + (stop_at % kDec) * 4;
       red[0] = stop_at;
-      if (bd.inst_block == 0) {
+      if (leader_cta) {
         p.iters[bd.instance] = stop_at;
-        p.status[bd.instance] = rec[0] != 0.0 ? 0 : 1;
-        p.maxinf[bd.instance] = rec[2];
-        p.objective[bd.instance] = rec[1];
+        p.status[bd.instance] = dec[(stop_at % kDec) * 4] != 0.0 ? 0 : 1;
+        p.objective[bd.instance] = dec_obj[stop_at % kDecG];  // written by this CTA
       }
     }
   } else {
     // ======================= compute warps =======================
     const int ctid = tid - 32;
-    RowMeta rm[K];
-    ColMeta cm[K];
+    const bool tick = clock_on && ctid == 0;
+    // per-thread metadata, packed to keep the K-way state in registers:
+    //  row: pofs, and n (bits 0-6) | exported (7) | base (8-19) | xloc (20-31)
+    //  col: copy_start (bits 0-22) | copy_count (23-30) | owner (31)
+    // Interior columns (every copy in this block) are [0, cols_int), thread
+    // slots c = ctid + k * kCW; boundary columns [cols_int, cols) get one slot
+    // per thread, c = cols_int + ctid (the layout guarantees <= kCW of them).
+    int32_t pofs[K];
+    uint32_t rpk[K], cpk[K];
     double lam[K], lr[K], zp[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int r = ctid + k * kCW;
+      pofs[k] = 0;
+      rpk[k] = 0;
+      zp[k] = 0.0;
       if (r < bd.rows) {
-        rm[k] = p.rmeta[bd.row0 + r];
+        const RowMeta rm = p.rmeta[bd.row0 + r];
+        pofs[k] = rm.pofs;
+        rpk[k] = static_cast<uint32_t>(rm.n) | (static_cast<uint32_t>(rm.exported) << 7) |
+                 (static_cast<uint32_t>(rm.base) << 8) | (static_cast<uint32_t>(rm.xloc) << 20);
         zp[k] = p.z0[bd.row0 + r];
-      } else {
-        rm[k] = RowMeta{0, 0, 0, 0};
-        zp[k] = 0.0;
       }
       lam[k] = 0.0;
       lr[k] = 0.0 / rho;  // lambda^0 / rho
-      cm[k] = r < bd.cols ? p.cmeta[bd.col_off + r] : ColMeta{0, 0, 0, 0};
     }
+    auto pack_col = [&](int c) -> uint32_t {
+      const ColMeta cm = p.cmeta[bd.col_off + c];
+      return static_cast<uint32_t>(cm.copy_start) | (static_cast<uint32_t>(cm.copy_count) << 23) |
+             (static_cast<uint32_t>(cm.owner) << 31);
+    };
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = ctid + k * kCW;
+      cpk[k] = c < bd.cols_int ? pack_col(c) : 0u;
+    }
+    const int cb = bd.cols_int + ctid;
+    const uint32_t cpkb = cb < bd.cols ? pack_col(cb) : 0u;
 
-    // (G) global update from u_in into xdst; returns the c'x share of owned columns
-    auto global_update = [&](const double* u_in, double* xdst) -> double {
+    auto row_n = [](uint32_t v) { return static_cast<int>(v & 0x7fu); };
+    auto row_exported = [](uint32_t v) { return (v >> 7) & 1u; };
+    auto row_base = [](uint32_t v) { return static_cast<int>((v >> 8) & 0xfffu); };
+    auto row_xloc = [](uint32_t v) { return static_cast<int>(v >> 20); };
+    auto col_start = [](uint32_t v) { return static_cast<int>(v & 0x7fffffu); };
+    auto col_count = [](uint32_t v) { return static_cast<int>((v >> 23) & 0xffu); };
+
+    // x_c = clamp((acc - c/rho) * inv, lo, hi) (admm.cpp:126-127); returns c_c x_c for owners
+    auto finish_col = [&](int c, uint32_t pk, double acc, double* xdst) -> double {
+      const double unclamped = (acc - c_rho[c]) * c_inv[c];
+      const double xv = sel_min(sel_max(unclamped, c_lo[c]), c_hi[c]);
+      xdst[c] = xv;
+      return (pk >> 31) ? c_cost[c] * xv : 0.0;
+    };
+    // (G, interior) every copy in shared memory: acc = sum in ascending s
+    auto global_interior = [&](double* xdst) -> double {
       double obj = 0.0;
       double a[K][4];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {  // issue the first (up to) 4 copy loads of every column
+      for (int k = 0; k < K; ++k) {
         const int c = ctid + k * kCW;
-        const int cnt = c < bd.cols ? cm[k].copy_count : 0;
-        const int32_t* q = cps + cm[k].copy_start;
+        const int cnt = c < bd.cols_int ? col_count(cpk[k]) : 0;
+        const int32_t* q = cps + col_start(cpk[k]);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) a[k][e] = e < cnt ? ld_l2(u_in + q[e]) : 0.0;
+        for (int e = 0; e < 4; ++e) a[k][e] = e < cnt ? tu[q[e]] : 0.0;
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int c = ctid + k * kCW;
-        if (c < bd.cols) {
-          const int cnt = cm[k].copy_count;
-          const int32_t* q = cps + cm[k].copy_start;
+        if (c < bd.cols_int) {
+          const int cnt = col_count(cpk[k]);
+          const int32_t* q = cps + col_start(cpk[k]);
           double acc = 0.0;
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (e < cnt) acc = acc + a[k][e];
-          for (int e = 4; e < cnt; ++e) acc = acc + ld_l2(u_in + q[e]);
-          const double unclamped = (acc - c_rho[c]) * c_inv[c];
-          const double xv = sel_min(sel_max(unclamped, c_lo[c]), c_hi[c]);
-          xdst[c] = xv;
-          if (cm[k].owner) obj = obj + c_cost[c] * xv;
+          for (int e = 4; e < cnt; ++e) acc = acc + tu[q[e]];
+          obj = obj + finish_col(c, cpk[k], acc, xdst);
         }
       }
       return obj;
     };
+    // (G, boundary) copies of other blocks read from L2 (u_in), own copies
+    // from shared memory; every load of the column is issued before the sum
+    auto global_boundary = [&](const double* u_in, double* xdst) -> double {
+      if (cb >= bd.cols) return 0.0;
+      const int cnt = col_count(cpkb);
+      const int32_t* q = cps + col_start(cpkb);
+      double a[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        a[e] = 0.0;
+        if (e < cnt) {
+          const int32_t ref = q[e];
+          a[e] = ref >= 0 ? tu[ref] : ld_l2(u_in + decode_remote(ref));
+        }
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e < cnt) acc = acc + a[e];
+      for (int e = 8; e < cnt; ++e) {
+        const int32_t ref = q[e];
+        acc = acc + (ref >= 0 ? tu[ref] : ld_l2(u_in + decode_remote(ref)));
+      }
+      return finish_col(cb, cpkb, acc, xdst);
+    };
 
-    double obj = global_update(u_buf[0], xring);  // x^1 from u^0 = z^0
+    // x^1 from u^0 = z^0 (tu holds z^0; remote copies from p.u, initialised to z^0)
+    double obj = global_interior(xring + bd.cols);
+    obj = obj + global_boundary(p.u, xring + bd.cols);
     named_sync(kBarCompute, kCW);
-    for (int t = 1;; ++t) {
-      const double* xt = xring + static_cast<std::size_t>((t - 1) % 3) * bd.cols;  // x^t
-      double* u_out = u_buf[t & 1];
+    long long c0 = tick ? clock64() : 0, c1 = 0;
+    double m_old = 0.0, m2 = 0.0, m1 = 0.0, m0 = 0.0;  // infeasibility: <= t-3, t-2, t-1, t
+    int t = 1;
+    for (;; ++t) {
+      const double* xt = xring + static_cast<std::size_t>(t % 4) * bd.cols;  // x^t
+      double* xnext = xring + static_cast<std::size_t>((t + 1) % 4) * bd.cols;
+      double* u_out = p.u + (t & 1) * p.rows_total;
       double* z_res = p.z_out + static_cast<int64_t>(t % 3) * p.rows_total;
       double* l_res = p.lam_out + static_cast<int64_t>(t % 3) * p.rows_total;
 
@@ -334,36 +493,93 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int r = ctid + k * kCW;
-        if (r < bd.rows) tgt[r] = xt[rm[k].xloc] + lr[k];  // lr = lambda / rho, same rounding
+        if (r < bd.rows) tu[r] = xt[row_xloc(rpk[k])] + lr[k];  // lr = lambda / rho, same rounding
       }
       named_sync(kBarCompute, kCW);
+      if (tick) {
+        c1 = clock64();
+        ph[kPhTarget] += c1 - c0;
+        c0 = c1;
+      }
 
-      // (L2) z = P t + v, one row per thread, P column-major per subsystem
+      // (L2) z = P t + v, one row per thread and slot k, P column-major per
+      // subsystem (consecutive threads read consecutive words). Each row's
+      // loads are issued 8 at a time ahead of its sequential-j sum.
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int r = ctid + k * kCW;
         if (r < bd.rows) {
-          const int n = rm[k].n;
-          const double* pr = Pop + rm[k].pofs;
-          const double* tb = tgt + rm[k].base;
+          const int n = row_n(rpk[k]);
+          const double* pr = Pop + pofs[k];
+          const double* tb = tu + row_base(rpk[k]);
           double acc = 0.0;
-          int j = 0;
-          for (; j + 4 <= n; j += 4) {
-            const double p0 = pr[(j + 0) * n], p1 = pr[(j + 1) * n];
-            const double p2 = pr[(j + 2) * n], p3 = pr[(j + 3) * n];
-            acc = acc + p0 * tb[j];
-            acc = acc + p1 * tb[j + 1];
-            acc = acc + p2 * tb[j + 2];
-            acc = acc + p3 * tb[j + 3];
+          for (int j0 = 0; j0 < n; j0 += 8) {
+            double pv[8], tv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              pv[e] = 0.0;
+              tv[e] = 0.0;
+              if (j0 + e < n) {
+                pv[e] = pr[(j0 + e) * n];
+                tv[e] = tb[j0 + e];
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (j0 + e < n) acc = acc + pv[e] * tv[e];
           }
-          for (; j < n; ++j) acc = acc + pr[j * n] * tb[j];
           zs[r] = acc + vs[r];
         }
       }
+      // every row's target read before (D) overwrites tu; z visible to (A)
       named_sync(kBarCompute, kCW);
+      if (tick) {
+        c1 = clock64();
+        ph[kPhGemv] += c1 - c0;
+        c0 = c1;
+      }
 
-      // (A) local equality residual ||A_s z_s - b_s||_inf
-      double v7[7] = {0.0, 0.0, 0.0, 0.0, 0.0, obj, 0.0};
+      // (D) dual update, exchange value (critical path: only what others need)
+      double v8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, obj, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int r = ctid + k * kCW;
+        if (r < bd.rows) {
+          const double z = zs[r];
+          const double bx = xt[row_xloc(rpk[k])];
+          const double d = bx - z;
+          const double ln = lam[k] + rho * d;
+          v8[0] = v8[0] + d * d;
+          const double dz = z - zp[k];
+          v8[1] = v8[1] + dz * dz;
+          v8[2] = v8[2] + bx * bx;
+          v8[3] = v8[3] + z * z;
+          v8[4] = v8[4] + ln * ln;
+          lr[k] = ln / rho;  // reused as lambda/rho by the next target (admm.cpp:136)
+          const double u = z - lr[k];
+          tu[r] = u;
+          if (row_exported(rpk[k])) u_out[bd.row0 + r] = u;
+          lam[k] = ln;
+          zp[k] = z;
+        }
+      }
+      named_arrive(kBarPublish, kThreads);
+      named_sync(kBarCompute, kCW);  // every u(t) in shared memory
+      if (tick) {
+        c1 = clock64();
+        ph[kPhDual] += c1 - c0;
+        c0 = c1;
+      }
+      // (G, interior) x^{t+1} of the columns no other block holds -- overlaps
+      // the exchange; x^{t+1} goes to slot (t+1) % 4, so x^{t-2} (a possible
+      // stopping iterate) survives
+      double obj_next = global_interior(xnext);
+      // (A) local equality residual ||A_s z_s - b_s||_inf, result copies,
+      // partial reductions -- overlapping the exchange. The infeasibility is
+      // a max over iterations (admm.cpp:219-220): each thread keeps its own
+      // running max (m_old: iterations <= t-3) plus the last three
+      // iterations, folded once the stopping iteration is known.
+      double e_t = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int a = ctid + k * kCW;
@@ -372,52 +588,88 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           const double* ar = Aop + am.aofs;
           const double* zb = zs + am.base;
           double acc = 0.0;
-          for (int j = 0; j < am.n; ++j) acc = acc + ar[j * am.m] * zb[j];
-          v7[6] = sel_max(v7[6], fabs(acc - a_rhs[a]));
+          for (int j0 = 0; j0 < am.n; j0 += 8) {
+            double av[8], zv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              av[e] = 0.0;
+              zv[e] = 0.0;
+              if (j0 + e < am.n) {
+                av[e] = ar[(j0 + e) * am.m];
+                zv[e] = zb[j0 + e];
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (j0 + e < am.n) acc = acc + av[e] * zv[e];
+          }
+          e_t = sel_max(e_t, fabs(acc - a_rhs[a]));
         }
       }
-      // (D) dual update, exchange value, residual partials
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int r = ctid + k * kCW;
         if (r < bd.rows) {
-          const double z = zs[r];
-          const double bx = xt[rm[k].xloc];
-          const double d = bx - z;
-          const double ln = lam[k] + rho * d;
-          v7[0] = v7[0] + d * d;
-          const double dz = z - zp[k];
-          v7[1] = v7[1] + dz * dz;
-          v7[2] = v7[2] + bx * bx;
-          v7[3] = v7[3] + z * z;
-          v7[4] = v7[4] + ln * ln;
-          lr[k] = ln / rho;  // reused as lambda/rho by the next target (admm.cpp:136)
-          u_out[bd.row0 + r] = z - lr[k];
-          z_res[bd.row0 + r] = z;   // (z, lambda)^t kept until the stop test of t is known
-          l_res[bd.row0 + r] = ln;
-          lam[k] = ln;
-          zp[k] = z;
+          z_res[bd.row0 + r] = zp[k];  // (z, lambda)^t kept until the stop test of t is known
+          l_res[bd.row0 + r] = lam[k];
         }
       }
-      warp_reduce7(v7, 32);
-      if (lane == 0) {
-#pragma unroll
-        for (int q = 0; q < 7; ++q) red[warp * kPartials + q] = v7[q];
+      m_old = sel_max(m_old, m2);
+      m2 = m1;
+      m1 = m0;
+      m0 = e_t;
+      {
+        const double mine = sum8(v8, lane);
+        if ((lane & 3) == 0) red[(t & 1) * kWarps * kPartials + warp * kPartials + sum8_index(lane)] = mine;
       }
-      named_arrive(kBarPublish, kThreads);
+      named_arrive(kBarPartials, kThreads);
+      if (tick) {
+        c1 = clock64();
+        ph[kPhEqRed] += c1 - c0;
+        c0 = c1;
+      }
       named_sync(kBarExchanged, kThreads);
+      if (tick) {
+        c1 = clock64();
+        ph[kPhWait] += c1 - c0;
+        c0 = c1;
+      }
       if ((t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter) break;
-      obj = global_update(u_out, xring + static_cast<std::size_t>(t % 3) * bd.cols);  // x^{t+1}
+      // (G, boundary) x^{t+1} of the columns shared with neighbours
+      obj = obj_next + global_boundary(u_out, xnext);
       named_sync(kBarCompute, kCW);
+      if (tick) {
+        c1 = clock64();
+        ph[kPhGlobal] += c1 - c0;
+        c0 = c1;
+      }
     }
+    m_fold[0] = m_old;
+    m_fold[1] = m2;
+    m_fold[2] = m1;
+    m_fold[3] = m0;
+    thread_last = t;
   }
   __syncthreads();
   stop_at = static_cast<int>(red[0]);
+  if (clock_on && tid < 8) p.prof[blockIdx.x * 8 + tid] += ph[tid];
+  if (warp != 0) {
+    // max_local_infeasibility over iterations 1..stop_at: the loop ended at
+    // t = last with stop_at in {last-2, last-1, last}
+    const int last = thread_last;
+    double mx = sel_max(m_fold[0], m_fold[1]);  // m_old, m2 (iteration last-2)
+    if (last - 1 <= stop_at) mx = sel_max(mx, m_fold[2]);
+    if (last <= stop_at) mx = sel_max(mx, m_fold[3]);
+    mx = warp_max(mx);
+    if (lane == 0)
+      atomicMax(reinterpret_cast<unsigned long long*>(p.maxinf + bd.instance),
+                static_cast<unsigned long long>(__double_as_longlong(mx)));  // mx >= 0: bit order = value order
+  }
   if (warp != 0) {
     // owners write x^stop_at (still in the ring); (z, lambda)^stop_at are in
     // result buffer stop_at % 3, which the host reads
     const int ctid = tid - 32;
-    const double* xfinal = xring + static_cast<std::size_t>((stop_at - 1) % 3) * bd.cols;
+    const double* xfinal = xring + static_cast<std::size_t>(stop_at % 4) * bd.cols;
     for (int c = ctid; c < bd.cols; c += kCW) {
       const ColMeta cmc = p.cmeta[bd.col_off + c];
       if (cmc.owner) p.x_out[id.x_off + cmc.gcol] = xfinal[c];

@@ -53,8 +53,10 @@ struct dopf_cuda_ctx {
   double *d_cc = nullptr, *d_cinv = nullptr, *d_clo = nullptr, *d_chi = nullptr;
   AMeta* d_ameta = nullptr;
   double* d_ab = nullptr;
+  int32_t* d_nbrs = nullptr;
   double *d_u = nullptr, *d_z = nullptr, *d_lam = nullptr, *d_x = nullptr, *d_part = nullptr;
   unsigned long long* d_flags = nullptr;
+  unsigned long long* d_ctl = nullptr;
   int32_t *d_iters = nullptr, *d_status = nullptr;
   double *d_maxinf = nullptr, *d_obj = nullptr;
   double* d_trace = nullptr;
@@ -63,7 +65,8 @@ struct dopf_cuda_ctx {
   int64_t launches = 0;
   double last_kernel_s = 0;
   bool profiling = false;
-  long long* d_prof = nullptr;
+  long long* d_prof = nullptr;  // [blocks][8] phase cycles
+  std::size_t prof_cap = 0;
 
   void free_model() {
     for (void* p : allocs) cudaFree(p);
@@ -141,13 +144,15 @@ void upload_layout(dopf_cuda_ctx* c) {
   c->d_chi = c->put(L.chi);
   c->d_ameta = c->put(L.ameta);
   c->d_ab = c->put(L.ab);
+  c->d_nbrs = c->put(L.nbrs);
   const std::size_t I = L.inst.size();
   c->d_u = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));
   c->d_z = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));    // [t % 3][row]
   c->d_lam = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));
   c->d_x = c->scratch<double>(L.x_total);
   c->d_part = c->scratch<double>(I * 3 * L.blocks_per_instance * kPartials);
-  c->d_flags = c->scratch<unsigned long long>(I * L.blocks_per_instance);
+  c->d_flags = c->scratch<unsigned long long>(I * L.blocks_per_instance * 16);
+  c->d_ctl = c->scratch<unsigned long long>(I * kCtlWords);
   c->d_iters = c->scratch<int32_t>(I);
   c->d_status = c->scratch<int32_t>(I);
   c->d_maxinf = c->scratch<double>(I);
@@ -184,6 +189,9 @@ void finish_upload(dopf_cuda_ctx* c) {
   if (c->L.K > kMaxK)
     throw std::invalid_argument("model too large for the resident kernel (" +
                                 std::to_string(c->L.rows_total) + " rows)");
+  if (c->L.max_neighbours > 32)
+    throw std::invalid_argument("a block shares columns with more than 32 other blocks (" +
+                                std::to_string(c->L.max_neighbours) + ")");
   choose_sync(c);
   upload_layout(c);
   c->uploaded = true;
@@ -207,8 +215,11 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     c->trace_cap = need;
   }
   const auto t_up0 = std::chrono::steady_clock::now();
-  ck(cudaMemsetAsync(c->d_flags, 0, I * L.blocks_per_instance * sizeof(unsigned long long), c->stream),
+  ck(cudaMemsetAsync(c->d_flags, 0, I * L.blocks_per_instance * 16 * sizeof(unsigned long long),
+                     c->stream),
      "memset");
+  ck(cudaMemsetAsync(c->d_ctl, 0, I * kCtlWords * sizeof(unsigned long long), c->stream), "memset");
+  ck(cudaMemsetAsync(c->d_maxinf, 0, I * sizeof(double), c->stream), "memset");
   ck(cudaMemsetAsync(c->d_part, 0, I * 3 * L.blocks_per_instance * kPartials * sizeof(double), c->stream),
      "memset");
   ck(cudaMemcpyAsync(c->d_u, c->d_z0, L.rows_total * sizeof(double), cudaMemcpyDeviceToDevice,
@@ -231,13 +242,22 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.chi = c->d_chi;
   p.ameta = c->d_ameta;
   p.ab = c->d_ab;
+  p.nbrs = c->d_nbrs;
   p.u = c->d_u;
   p.z_out = c->d_z;
   p.lam_out = c->d_lam;
   p.x_out = c->d_x;
   p.part = c->d_part;
   p.flags = c->d_flags;
+  p.ctl = c->d_ctl;
   p.trace = want_trace ? c->d_trace : nullptr;
+  if (c->profiling && c->prof_cap < static_cast<std::size_t>(c->num_blocks) * 8) {
+    if (c->d_prof) cudaFree(c->d_prof);
+    c->d_prof = nullptr;
+    c->prof_cap = static_cast<std::size_t>(c->num_blocks) * 8;
+    ck(cudaMalloc(&c->d_prof, c->prof_cap * sizeof(long long)), "cudaMalloc");
+    ck(cudaMemset(c->d_prof, 0, c->prof_cap * sizeof(long long)), "memset");
+  }
   p.prof = c->profiling ? c->d_prof : nullptr;
   p.iters = c->d_iters;
   p.status = c->d_status;
@@ -427,25 +447,52 @@ double dopf_cuda_bytes_per_iteration(const dopf_cuda_ctx* c) {
 
 double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* c) { return c ? c->last_kernel_s : 0.0; }
 
+int dopf_layout_probe(const dopf_model_view* m, int32_t max_blocks, int64_t smem_limit,
+                      dopf_layout_stats* out) {
+  if (!m || !out || max_blocks < 1 || smem_limit < 1024) return DOPF_ERR_INVALID_ARGUMENT;
+  try {
+    LayoutOptions opt;
+    opt.smem_limit = static_cast<std::size_t>(smem_limit);
+    opt.max_blocks = max_blocks;
+    HostLayout L;
+    add_instance(L, *m, choose_blocks(*m, opt), opt);
+    out->blocks = L.blocks_per_instance;
+    out->rows_per_thread = L.K;
+    out->resident = L.all_ops_in_smem ? 1 : 0;
+    out->max_neighbours = L.max_neighbours;
+    out->smem_bytes = static_cast<int64_t>(L.smem_bytes);
+    int64_t remote = 0, local = 0, exported = 0;
+    for (int32_t c : L.copies) (c < 0 ? remote : local) += 1;
+    for (const RowMeta& r : L.rmeta) exported += r.exported ? 1 : 0;
+    out->remote_copies = remote;
+    out->local_copies = local;
+    out->exported_rows = exported;
+    out->bytes_per_iteration = L.bytes_per_iteration;
+    return DOPF_OK;
+  } catch (const std::invalid_argument&) {
+    return DOPF_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return DOPF_ERR_RUNTIME;
+  }
+}
+
 int dopf_cuda_set_profiling(dopf_cuda_ctx* c, int32_t on) {
   if (!c) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    if (on && !c->d_prof) {
-      ck(cudaMalloc(&c->d_prof, 8 * sizeof(long long)), "cudaMalloc");
-      ck(cudaMemset(c->d_prof, 0, 8 * sizeof(long long)), "memset");
-    }
+    if (c->d_prof) ck(cudaMemset(c->d_prof, 0, c->prof_cap * sizeof(long long)), "memset");
     c->profiling = on != 0;
   });
 }
 
-int dopf_cuda_phase_cycles(const dopf_cuda_ctx* c, int64_t* out8) {
-  if (!c || !out8) return DOPF_ERR_INVALID_ARGUMENT;
-  if (!c->d_prof) {
-    for (int q = 0; q < 8; ++q) out8[q] = 0;
-    return DOPF_OK;
-  }
+int dopf_cuda_phase_cycles(const dopf_cuda_ctx* c, int64_t* out, int32_t max_blocks) {
+  if (!c || !out || max_blocks < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  const int nb = std::min<int>(max_blocks, c->num_blocks);
+  for (int q = 0; q < 8 * max_blocks; ++q) out[q] = 0;
+  if (!c->d_prof) return DOPF_OK;
   return guarded(const_cast<dopf_cuda_ctx*>(c), [&] {
-    ck(cudaMemcpy(out8, c->d_prof, 8 * sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
+    ck(cudaMemcpy(out, c->d_prof, static_cast<std::size_t>(nb) * 8 * sizeof(long long),
+                  cudaMemcpyDeviceToHost),
+       "d2h");
   });
 }
 

@@ -2,9 +2,13 @@
 // host-side builder, layout.cpp, and the sm_100a kernels, admm_kernels.cu).
 //
 // HBM / shared-memory layout:
-//  * Subsystems are split into contiguous s-ranges, one per CTA ("block"),
-//    balanced by operator bytes; inside a block they are reordered by n_s
-//    (descending) so warps see uniform GEMV lengths.
+//  * Subsystems are ordered by a depth-first walk of the component graph
+//    (two subsystems are adjacent when they hold copies of the same global
+//    column) and the walk is cut into contiguous pieces, one per CTA
+//    ("block"), balanced by operator bytes. Most consensus columns then have
+//    all their copies inside one block, and a block shares columns with only
+//    a handful of others (its "neighbours"). Inside a block subsystems are
+//    reordered by n_s (descending) so warps see uniform GEMV lengths.
 //  * A "device row" is one local variable (s, i). z, lambda and the exchange
 //    value u = z - lambda/rho are stored in device-row order.
 //  * P_s and A_s are packed per block, column-major per subsystem, so the
@@ -12,11 +16,21 @@
 //    addresses at every step j (coalesced in HBM, conflict-free in smem).
 //  * Each block computes the global update x_i for every column its rows
 //    reference, from the copies' u values (CSR by column, ascending s, the
-//    reference's summation order) -- so one grid/cluster barrier per
-//    iteration suffices and the result is bitwise deterministic.
+//    reference's summation order): copies held by the block itself are read
+//    from shared memory, copies of other blocks from L2 after that block's
+//    "u(t) published" flag. Only rows some other block reads ("exported"
+//    rows) are written to global memory. Each block waits for its neighbours
+//    only -- no grid-wide barrier on the critical path -- and the result is
+//    bitwise deterministic.
 #pragma once
 
 #include <cstdint>
+
+#ifdef __CUDACC__
+#define DOPF_HD __host__ __device__
+#else
+#define DOPF_HD
+#endif
 
 namespace dopf::cuda {
 
@@ -40,6 +54,9 @@ struct BlockDesc {
   int32_t ops_in_smem; // 1: P and A staged in shared memory once, 0: read from HBM/L2
   int32_t instance;
   int32_t inst_block;  // index of this block within its instance
+  int32_t nbr_off;     // neighbour list (instance-local block indices) in the global nbrs array
+  int32_t nbr_cnt;
+  int32_t cols_int;    // columns [0, cols_int) have every copy in this block; the rest are boundary
   int32_t pad;
 };
 
@@ -56,11 +73,18 @@ struct InstDesc {
 
 // Row task: z_i = sum_j P(i,j) t_j + v_i for one (s, i).
 struct RowMeta {
-  int32_t pofs;   // offset of P(i, 0) within the block's P (column-major: stride n)
-  int32_t n;      // n_s
-  int32_t base;   // block-local row index of (s, 0)
-  int32_t xloc;   // block-local column index of local_to_global(s, i)
+  int32_t pofs;      // offset of P(i, 0) within the block's P (column-major: stride n)
+  int16_t n;         // n_s
+  int16_t exported;  // 1: another block reads this row's u (store it to global memory)
+  int32_t base;      // block-local row index of (s, 0)
+  int32_t xloc;      // block-local column index of local_to_global(s, i)
 };
+
+// Copy reference in a block's copy list: >= 0 is a block-local row (u read
+// from shared memory), < 0 encodes global device row -(ref + 1) (u read from
+// L2 after the owning block's flag).
+DOPF_HD inline int32_t encode_remote(int32_t dev_row) { return -(dev_row + 1); }
+DOPF_HD inline int32_t decode_remote(int32_t ref) { return -ref - 1; }
 
 // Column task: x_c from its copies.
 struct ColMeta {

@@ -10,27 +10,66 @@ namespace {
 
 int ns_of(const dopf_model_view& m, int s) { return m.z_offsets[s + 1] - m.z_offsets[s]; }
 
-// Contiguous s-ranges with nearly equal operator cost.
-std::vector<int> split_points(const dopf_model_view& m, int G) {
-  std::vector<double> cost(m.S);
-  double total = 0;
-  for (int s = 0; s < m.S; ++s) {
-    const double n = ns_of(m, s), mm = m.m_s[s];
-    cost[s] = n * n + mm * n + 6.0 * n + 4.0;
-    total += cost[s];
+double sub_cost(const dopf_model_view& m, int s) {
+  const double n = ns_of(m, s), mm = m.m_s[s];
+  return n * n + mm * n + 6.0 * n + 4.0;
+}
+
+// Depth-first order of the component graph: subsystems s and s' are adjacent
+// when they hold copies of one global column. Cutting this walk into
+// contiguous pieces keeps most copies of a column inside one block.
+std::vector<int> locality_order(const dopf_model_view& m) {
+  std::vector<int> s_of_ref(m.N_z);
+  for (int s = 0; s < m.S; ++s)
+    for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) s_of_ref[k] = s;
+  std::vector<std::vector<int>> adj(m.S);
+  for (int c = 0; c < m.n; ++c)
+    for (int a = m.csr_ptr[c]; a < m.csr_ptr[c + 1]; ++a)
+      for (int b = m.csr_ptr[c]; b < m.csr_ptr[c + 1]; ++b)
+        if (a != b) adj[s_of_ref[m.csr_copy[a]]].push_back(s_of_ref[m.csr_copy[b]]);
+  for (auto& v : adj) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
   }
-  std::vector<int> cuts{0};
+  std::vector<int> order;
+  order.reserve(m.S);
+  std::vector<char> seen(m.S, 0);
+  std::vector<int> stack;
+  for (int root = 0; root < m.S; ++root) {
+    if (seen[root]) continue;
+    stack.push_back(root);
+    while (!stack.empty()) {
+      const int u = stack.back();
+      stack.pop_back();
+      if (seen[u]) continue;
+      seen[u] = 1;
+      order.push_back(u);
+      // push in descending id so the lowest-id neighbour is visited first
+      for (auto it = adj[u].rbegin(); it != adj[u].rend(); ++it)
+        if (!seen[*it]) stack.push_back(*it);
+    }
+  }
+  return order;
+}
+
+// Cuts `order` into at most G contiguous pieces of nearly equal cost.
+std::vector<std::vector<int>> split_blocks(const dopf_model_view& m, const std::vector<int>& order,
+                                           int G) {
+  double total = 0;
+  for (int s : order) total += sub_cost(m, s);
+  std::vector<std::vector<int>> out(1);
   double acc = 0;
   int g = 1;
-  for (int s = 0; s < m.S && g < G; ++s) {
-    acc += cost[s];
-    if (acc >= total * g / G) {
-      if (s + 1 > cuts.back()) cuts.push_back(s + 1);
+  for (int s : order) {
+    out.back().push_back(s);
+    acc += sub_cost(m, s);
+    if (g < G && acc >= total * g / G) {
+      out.emplace_back();
       ++g;
     }
   }
-  if (cuts.back() != m.S) cuts.push_back(m.S);
-  return cuts;  // size <= G+1
+  if (out.back().empty()) out.pop_back();
+  return out;
 }
 
 }  // namespace
@@ -40,8 +79,8 @@ std::size_t block_smem_bytes(const BlockDesc& b, bool ops_in_smem) {
   std::size_t doubles = 0;
   if (ops_in_smem) doubles += static_cast<std::size_t>(b.p_len) + b.a_len;
   doubles += 3ull * b.rows;                     // target, z, v
-  doubles += 8ull * b.cols;                     // x (three buffers), c/rho, inv, lo, hi, c
-  doubles += (kThreads / 32ull) * kPartials + 16;  // warp partials + decision ring
+  doubles += 9ull * b.cols;                     // x (four buffers), c/rho, inv, lo, hi, c
+  doubles += 2 * (kThreads / 32ull) * kPartials + 16 + 8;  // warp partials x2, decision ring, phase clock
   doubles += 3ull * b.arows;                    // equality rows: rhs + AMeta (16 B)
   return 8 * doubles + 4ull * b.copy_len + 64;
 }
@@ -94,8 +133,9 @@ int choose_blocks(const dopf_model_view& m, const LayoutOptions& opt) {
 void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOptions& opt) {
   if (!m.has_pre) throw std::invalid_argument("model view lacks precomputed operators");
   const int instance = static_cast<int>(L.inst.size());
-  const std::vector<int> cuts = split_points(m, std::max(1, std::min(G, std::max(1, m.S))));
-  const int nb = static_cast<int>(cuts.size()) - 1;
+  const std::vector<std::vector<int>> parts =
+      split_blocks(m, locality_order(m), std::max(1, std::min(G, std::max(1, m.S))));
+  const int nb = static_cast<int>(parts.size());
   const int32_t inst_row0 = static_cast<int32_t>(L.rows_total);
   const int32_t block0 = static_cast<int32_t>(L.blocks.size());
 
@@ -116,7 +156,7 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
   std::vector<int32_t> block_row0(nb);
   for (int g = 0; g < nb; ++g) {
     auto& ord = order[g];
-    for (int s = cuts[g]; s < cuts[g + 1]; ++s) ord.push_back(s);
+    ord = parts[g];
     std::stable_sort(ord.begin(), ord.end(),
                      [&](int a, int b) { return ns_of(m, a) > ns_of(m, b); });
     block_row0[g] = next_row;
@@ -132,12 +172,14 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
   // owner block of each column = block holding its first (lowest-s) copy
   std::vector<int> block_of_s(m.S, 0);
   for (int g = 0; g < nb; ++g)
-    for (int s = cuts[g]; s < cuts[g + 1]; ++s) block_of_s[s] = g;
+    for (int s : parts[g]) block_of_s[s] = g;
   std::vector<int> s_of_ref(m.N_z);
   for (int s = 0; s < m.S; ++s)
     for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) s_of_ref[k] = s;
 
   std::vector<int> xloc_of(m.n, -1);
+  std::vector<char> exported(next_row - inst_row0, 0);
+  std::vector<int> nbrs;
   for (int g = 0; g < nb; ++g) {
     BlockDesc bd{};
     bd.row0 = block_row0[g];
@@ -155,6 +197,15 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
       for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) cols.push_back(m.l2g[k]);
     std::sort(cols.begin(), cols.end());
     cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+    // interior columns (every copy in this block) first, boundary columns last
+    auto is_boundary = [&](int c) {
+      for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q)
+        if (block_of_s[s_of_ref[m.csr_copy[q]]] != g) return true;
+      return false;
+    };
+    const auto mid = std::stable_partition(cols.begin(), cols.end(),
+                                           [&](int c) { return !is_boundary(c); });
+    bd.cols_int = static_cast<int32_t>(mid - cols.begin());
     for (std::size_t q = 0; q < cols.size(); ++q) xloc_of[cols[q]] = static_cast<int>(q);
 
     int32_t local = 0, pofs = 0, aofs = 0;
@@ -170,7 +221,7 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
       for (int i = 0; i < n; ++i) {
         const int ref = m.z_offsets[s] + i;
         const int32_t dev = bd.row0 + local;
-        L.rmeta[dev] = RowMeta{pofs + i, n, base, xloc_of[m.l2g[ref]]};
+        L.rmeta[dev] = RowMeta{pofs + i, static_cast<int16_t>(n), 0, base, xloc_of[m.l2g[ref]]};
         L.v[dev] = m.v[ref];
         L.z0[dev] = m.z0[ref];
         L.ref_of_dev[dev] = ref;
@@ -193,7 +244,17 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
       cm.gcol = c;
       cm.copy_start = static_cast<int32_t>(L.copies.size()) - bd.copy_off;
       cm.copy_count = m.csr_ptr[c + 1] - m.csr_ptr[c];
-      for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q) L.copies.push_back(dev_of_ref[m.csr_copy[q]]);
+      for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q) {
+        const int32_t dev = dev_of_ref[m.csr_copy[q]];
+        const int g2 = block_of_s[s_of_ref[m.csr_copy[q]]];
+        if (g2 == g) {
+          L.copies.push_back(dev - bd.row0);  // block-local: u from shared memory
+        } else {
+          L.copies.push_back(encode_remote(dev));
+          exported[dev - inst_row0] = 1;
+          nbrs.push_back(g2);
+        }
+      }
       cm.owner = block_of_s[s_of_ref[m.csr_copy[m.csr_ptr[c]]]] == g ? 1 : 0;
       L.cmeta.push_back(cm);
       L.cc.push_back(m.c[c]);
@@ -203,7 +264,24 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     }
     bd.copy_len = static_cast<int32_t>(L.copies.size()) - bd.copy_off;
     for (int c : cols) xloc_of[c] = -1;
+    std::sort(nbrs.begin(), nbrs.end());
+    nbrs.erase(std::unique(nbrs.begin(), nbrs.end()), nbrs.end());
+    bd.nbr_off = static_cast<int32_t>(L.nbrs.size());
+    bd.nbr_cnt = static_cast<int32_t>(nbrs.size());
+    L.nbrs.insert(L.nbrs.end(), nbrs.begin(), nbrs.end());
+    L.max_neighbours = std::max(L.max_neighbours, bd.nbr_cnt);
+    nbrs.clear();
 
+    // the kernel packs per-thread metadata into bit fields (admm_kernels.cu)
+    if (bd.rows >= 4096 || bd.cols >= 4096 || bd.copy_len >= (1 << 23))
+      throw std::invalid_argument("block too large for the resident kernel");
+    if (bd.cols - bd.cols_int > opt.threads - 32)
+      throw std::invalid_argument("block has more boundary columns than compute threads");
+    for (int s : order[g])
+      if (ns_of(m, s) >= 128) throw std::invalid_argument("subsystem with n_s >= 128 columns");
+    for (int c : cols)
+      if (m.csr_ptr[c + 1] - m.csr_ptr[c] >= 256)
+        throw std::invalid_argument("column with 256 or more copies");
     bd.ops_in_smem = block_smem_bytes(bd, true) <= opt.smem_limit ? 1 : 0;
     if (!bd.ops_in_smem) L.all_ops_in_smem = false;
     L.smem_bytes = std::max(L.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
@@ -213,6 +291,7 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     L.K = std::max(L.K, std::max(1, k_need));
     L.blocks.push_back(bd);
   }
+  for (int32_t d = inst_row0; d < next_row; ++d) L.rmeta[d].exported = exported[d - inst_row0];
   L.blocks_per_instance = std::max(L.blocks_per_instance, nb);
   L.bytes_per_iteration += algorithmic_bytes(m);
   L.flops_per_iteration += algorithmic_flops(m);

@@ -24,6 +24,8 @@ struct HostLayout {
   std::vector<double> cc, cinv, clo, chi;
   std::vector<AMeta> ameta;
   std::vector<double> ab;
+  std::vector<int32_t> nbrs;         // per block: instance-local indices of blocks sharing columns
+  int32_t max_neighbours = 0;
   int64_t rows_total = 0;
   int64_t x_total = 0;
   int64_t trace_rows_per_instance = 0;  // filled at solve time

@@ -1,17 +1,23 @@
-"""Per-phase SM-cycle breakdown of the persistent kernel (CTA 0, thread 0).
+"""Per-phase SM-cycle breakdown of the persistent kernel, every CTA.
 
 usage: python tools/phase_clock.py [shape] [seed]
+
+Compute-warp phases are timed by warp 1 lane 0 of each CTA (they include the
+barrier waits that end each phase); service phases by warp 0 lane 0.
 """
 import ctypes as C
 import os
 import sys
+
+import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2501_08293_b200 import _native as N  # noqa: E402
 from paper_2501_08293_b200 import dopf  # noqa: E402
 
-PHASES = ["top-wait", "target", "gemv", "eq+dual", "reduce", "exchange", "x-update", "combine"]
+PHASES = ["target", "gemv", "dual+publish", "eq+partials", "exch-wait", "x-update",
+          "svc:nbr-wait", "svc:all+comb"]
 
 shape = sys.argv[1] if len(sys.argv) > 1 else "ieee8500"
 seed = int(sys.argv[2]) if len(sys.argv) > 2 else 8500
@@ -24,10 +30,17 @@ lib = N.cuda()
 s.solve(dopf.Settings())
 lib.dopf_cuda_set_profiling(s._h, 1)
 r = s.solve(dopf.Settings())
-cyc = (N.i64 * 8)()
-lib.dopf_cuda_phase_cycles(s._h, cyc)
-tot = sum(cyc)
+G = s.info()["blocks"] * s.info()["instances"]
+cyc = (N.i64 * (8 * G))()
+lib.dopf_cuda_phase_cycles(s._h, cyc, G)
+a = np.array(cyc[:], dtype=np.float64).reshape(G, 8) / r.iterations
 print(f"{shape}: {r.iterations} iterations, kernel {1e3 * r.timings['solve']:.3f} ms, "
       f"{1e6 * r.timings['solve'] / r.iterations:.2f} us/iter, info {s.info()}")
-for name, c in zip(PHASES, cyc):
-    print(f"  {name:10s} {c / r.iterations:10.0f} cycles/iter  {100.0 * c / max(tot, 1):5.1f}%")
+print(f"  {'phase':14s} {'CTA0':>8s} {'min':>8s} {'median':>8s} {'max':>8s} {'argmax':>6s}  (cycles/iter)")
+for q, name in enumerate(PHASES):
+    col = a[:, q]
+    print(f"  {name:14s} {col[0]:8.0f} {col.min():8.0f} {np.median(col):8.0f} {col.max():8.0f} "
+          f"{int(col.argmax()):6d}")
+busy = a[:, [0, 1, 2, 3, 5]].sum(axis=1)
+print(f"  compute (no exch-wait): min {busy.min():.0f} median {np.median(busy):.0f} "
+      f"max {busy.max():.0f} (CTA {int(busy.argmax())})")
