@@ -31,12 +31,13 @@
 //   (W) poll the NEIGHBOURS' flag(t) (one relaxed load per lane, then one
 //       acquire fence) and fetch the decision record of t-2, then let the
 //       compute warps start (G);
-//   (S) leader CTA only: once the counter shows every block's slot of t-1,
-//       combine them in a fixed order (residuals, trace row, stop test,
-//       admm.hpp:63) and publish the decision record of t-1. One poller per
-//       instance instead of an all-to-all flag scan keeps L2 quiet. The
-//       compute warps act on the decision for t-2 after the exchange of t, so
-//       the residual reduction never sits on the critical path. State of the
+//   (S) once the counter shows every block's slot of t-1, combine them in a
+//       fixed order (residuals, stop test admm.hpp:63, objective; the leader
+//       CTA writes the trace row). Every CTA combines for itself -- bitwise
+//       identical decisions, no second hop -- and polls ONE counter word
+//       instead of scanning all blocks' flags. The compute warps act on the
+//       decision for t-2 after the exchange of t, so the residual reduction
+//       never sits on the critical path. State of the
 //       last iterations is kept (x in a 3-deep ring, z/lambda in 3 result
 //       buffers), so the output is exactly the iterate of the stopping
 //       iteration.
@@ -63,11 +64,11 @@ namespace {
 
 constexpr int kWarps = kThreads / 32;
 constexpr int kCW = kThreads - 32;  // compute threads (warps 1..)
-constexpr int kSlots = 3;           // partial-slot ring (see header)
+constexpr int kSlots = kSlotRing;  // partial-slot ring (see header)
 constexpr int kDec = 4;             // decision ring (shared memory)
 constexpr int kDecG = 8;            // decision ring (global, written by the leader CTA)
 constexpr int kLine = 16;           // u64 words per 128-byte line: flags are one per line
-enum : int { kBarCompute = 1, kBarPublish = 2, kBarExchanged = 3, kBarPartials = 4 };
+enum : int { kBarCompute = 1, kBarExchanged = 3, kBarPartials = 4 };
 // phase clock slots (per CTA): compute warp 1 lane 0, service lane 0
 enum : int { kPhTarget = 0, kPhGemv, kPhDual, kPhEqRed, kPhWait, kPhGlobal, kPhSvcNbr, kPhSvcAll };
 
@@ -97,18 +98,39 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-
-// Warp 0: wait for the neighbour blocks (lane q watches neighbour q; the
-// layout guarantees at most 32 neighbours).
-__device__ __forceinline__ void wait_nbr_flags(const unsigned long long* flags, int my_nbr, int lane,
-                                               int cnt, unsigned long long value) {
-  if (lane < cnt)
-    while (ld_relaxed_u64(flags + my_nbr) < value) {
-    }
-  fence_acq_rel();
-  __syncwarp();
+// Phase clock read that cannot run ahead of a deferred-blocking bar.sync:
+// the shared-memory load blocks until the barrier completes, and the clock is
+// read in the same asm block after it.
+__device__ __forceinline__ long long clock_after_barrier(const void* smem_word) {
+  long long c;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(smem_word));
+  asm volatile("{ .reg .u32 t; ld.volatile.shared.u32 t, [%1]; mov.u64 %0, %%clock64; }"
+               : "=l"(c) : "r"(a) : "memory");
+  return c;
 }
+
+// Spin-wait watchdog: a protocol bug must fail the launch loudly
+// (cudaErrorLaunchFailure) instead of hanging the device.
+constexpr unsigned kSpinLimit = 1u << 28;
+__device__ __forceinline__ void spin_check(unsigned& spins) {
+  if (++spins > kSpinLimit) __trap();
+}
+
+// Tagged exchange record {iteration, value}: one single-copy-atomic 128-bit
+// access, so a reader that sees the expected tag also sees the value -- no
+// separate flag round trip.
+__device__ __forceinline__ void st_tagged(unsigned long long* rec, unsigned long long tag, double v) {
+  asm volatile("{ .reg .b128 d; mov.b128 d, {%1, %2}; st.relaxed.gpu.global.b128 [%0], d; }"
+               ::"l"(rec), "l"(tag), "l"(__double_as_longlong(v)) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* rec, double& v) {
+  unsigned long long tag, bits;
+  asm volatile("{ .reg .b128 d; ld.relaxed.gpu.global.b128 d, [%2]; mov.b128 {%0, %1}, d; }"
+               : "=l"(tag), "=l"(bits) : "l"(rec) : "memory");
+  v = __longlong_as_double(static_cast<long long>(bits));
+  return tag;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // Sums of 8 values over the 32 lanes of a warp by recursive halving (9
 // double shuffles instead of 40). On return lane L holds the total of value
@@ -242,19 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   int thread_last = 0;                      // compute threads: last iteration executed
   if (warp == 0) {
     // ======================= service warp =======================
-    const bool leader_cta = bd.inst_block == 0;  // the instance's residual combiner
-    const int my_nbr = lane < bd.nbr_cnt ? p.nbrs[bd.nbr_off + lane] : 0;
+    const bool leader_cta = bd.inst_block == 0;  // writes the trace and the scalar results
     const bool tick = clock_on && lane == 0;
     unsigned long long* counter = ctl;            // slots published, G per iteration
-    unsigned long long* decw = ctl + kLine;       // [kDecG] (s << 1) | stop
-    double* dec_obj = reinterpret_cast<double*>(ctl + 2 * kLine);  // [kDecG] objective
-    // (S, leader CTA) combine every block's slot of iteration s in a fixed
-    // order; publish the decision word and the objective of s
+    // (S) combine every block's slot of iteration s in a fixed order (every
+    // CTA does this itself, bitwise identically): residuals, stop test,
+    // objective -> the block's decision ring; the leader writes the trace row
     auto combine = [&](int s) {
       if (exchange) {
-        if (lane == 0)
-          while (ld_acquire_u64(counter) < static_cast<unsigned long long>(G) * s) {
-          }
+        if (lane == 0) {
+          unsigned spins = 0;
+          while (ld_acquire_u64(counter) < static_cast<unsigned long long>(G) * s) spin_check(spins);
+        }
         __syncwarp();
       }
       const double* base = slots + static_cast<int64_t>(s % kSlots) * slot_stride;
@@ -285,9 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
         const double dres = rho * sqrt(tot[1]);
         const double eps_prim = eps * sel_max(sqrt(tot[2]), sqrt(tot[3]));
         const double eps_dual = eps * sqrt(tot[4]);
-        const bool stop = pres <= eps_prim && dres <= eps_dual;
-        dec_obj[s % kDecG] = tot[5];
-        if (trace) {
+        double* rec = dec + (s % kDec) * 4;
+        rec[0] = (pres <= eps_prim && dres <= eps_dual) ? 1.0 : 0.0;
+        rec[1] = tot[5];
+        if (leader_cta && trace) {
           double* row = trace + static_cast<int64_t>(s - 1) * 6;
           row[0] = s;
           row[1] = pres;
@@ -296,35 +318,22 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           row[4] = eps_dual;
           row[5] = tot[5];
         }
-        st_release_u64(decw + s % kDecG, (static_cast<unsigned long long>(s) << 1) | (stop ? 1ull : 0ull));
-      }
-      __syncwarp();
-    };
-    // stop bit of iteration s -> the block's shared-memory ring (lane 0)
-    auto fetch = [&](int s) {
-      if (lane == 0) {
-        unsigned long long w;
-        do {
-          w = ld_acquire_u64(decw + s % kDecG);
-        } while ((w >> 1) != static_cast<unsigned long long>(s));
-        dec[(s % kDec) * 4] = (w & 1ull) ? 1.0 : 0.0;
       }
       __syncwarp();
     };
 
     int t = 1;
     for (;; ++t) {
-      named_sync(kBarPublish, kThreads);  // compute warps: u(t) stored
-      if (exchange && lane == 0) st_release_u64(flags + bd.inst_block * kLine, static_cast<unsigned long long>(t));
-      // (W) every neighbour's u(t) is visible; decision of t-2 -- overlaps the
-      // compute warps' interior update, equality check and reductions
       const long long c0 = tick ? clock64() : 0;
-      if (exchange) wait_nbr_flags(flags, my_nbr * kLine, lane, bd.nbr_cnt, static_cast<unsigned long long>(t));
-      if (t >= 3) fetch(t - 2);
-      const long long c1 = tick ? clock64() : 0;
       named_sync(kBarPartials, kThreads);  // warp partials of t in red[t & 1]
+      const long long c1 = tick ? clock_after_barrier(ph) : 0;
       const bool cw_stop = (t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter;
       named_arrive(kBarExchanged, kThreads);
+      // residuals / stop test of t-1 (read by the compute warps at t+1) --
+      // BEFORE counting slot(t): a block's count for t then also certifies it
+      // finished reading every slot of t-1, so the slot ring cannot be
+      // overwritten under a slower block's combine
+      if (t >= 2) combine(t - 1);
       // (R) fixed-order reduction of the 15 warp partials -> slot(t), counted
       {
         const double* rb = red + (t & 1) * kWarps * kPartials;
@@ -341,7 +350,6 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           red_release_add_u64(counter, 1ull);
         }
       }
-      if (leader_cta && t >= 2) combine(t - 1);  // residuals / stop test of t-1
       if (tick) {
         ph[kPhSvcNbr] += c1 - c0;
         ph[kPhSvcAll] += clock64() - c1;
@@ -352,9 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       stop_at = t - 2;
     } else {
       // reached max_iter: decide between t-1 and t
-      if (leader_cta) combine(t);
-      if (t >= 2) fetch(t - 1);
-      fetch(t);
+      combine(t);
       stop_at = (t >= 2 && dec[((t - 1) % kDec) * 4] != 0.0) ? t - 1 : t;
     }
     if (lane == 0) {
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       if (leader_cta) {
         p.iters[bd.instance] = stop_at;
         p.status[bd.instance] = dec[(stop_at % kDec) * 4] != 0.0 ? 0 : 1;
-        p.objective[bd.instance] = dec_obj[stop_at % kDecG];  // written by this CTA
+        p.objective[bd.instance] = dec[(stop_at % kDec) * 4 + 1];
       }
     }
   } else {
@@ -449,35 +455,58 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       }
       return obj;
     };
-    // (G, boundary) copies of other blocks read from L2 (u_in), own copies
-    // from shared memory; every load of the column is issued before the sum
-    auto global_boundary = [&](const double* u_in, double* xdst) -> double {
+    // (G, boundary) copies of other blocks are tagged records of iteration
+    // `it` in L2 (polled until the tag matches), own copies from shared
+    // memory; the first four loads of the column are issued before any wait
+    auto global_boundary = [&](int it, double* xdst) -> double {
       if (cb >= bd.cols) return 0.0;
+      const unsigned long long* ub = p.ux + static_cast<int64_t>(it & 1) * 2 * p.rows_total;
+      const unsigned long long want = static_cast<unsigned long long>(it);
       const int cnt = col_count(cpkb);
       const int32_t* q = cps + col_start(cpkb);
-      double a[8];
+      double a[4];
+      unsigned long long tg[4];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < 4; ++e) {
         a[e] = 0.0;
+        tg[e] = want;
         if (e < cnt) {
           const int32_t ref = q[e];
-          a[e] = ref >= 0 ? tu[ref] : ld_l2(u_in + decode_remote(ref));
+          if (ref >= 0)
+            a[e] = tu[ref];
+          else
+            tg[e] = ld_tagged(ub + 2 * static_cast<int64_t>(decode_remote(ref)), a[e]);
         }
       }
       double acc = 0.0;
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e < cnt) acc = acc + a[e];
-      for (int e = 8; e < cnt; ++e) {
+      for (int e = 0; e < 4; ++e) {
+        if (e < cnt) {
+          unsigned spins = 0;
+          while (tg[e] != want) {
+            spin_check(spins);
+            tg[e] = ld_tagged(ub + 2 * static_cast<int64_t>(decode_remote(q[e])), a[e]);
+          }
+          acc = acc + a[e];
+        }
+      }
+      for (int e = 4; e < cnt; ++e) {
         const int32_t ref = q[e];
-        acc = acc + (ref >= 0 ? tu[ref] : ld_l2(u_in + decode_remote(ref)));
+        double v;
+        if (ref >= 0) {
+          v = tu[ref];
+        } else {
+          unsigned spins = 0;
+          while (ld_tagged(ub + 2 * static_cast<int64_t>(decode_remote(ref)), v) != want) spin_check(spins);
+        }
+        acc = acc + v;
       }
       return finish_col(cb, cpkb, acc, xdst);
     };
 
-    // x^1 from u^0 = z^0 (tu holds z^0; remote copies from p.u, initialised to z^0)
+    // x^1 from u^0 = z^0 (tu holds z^0; remote copies: records {0, z^0} written by the host)
     double obj = global_interior(xring + bd.cols);
-    obj = obj + global_boundary(p.u, xring + bd.cols);
+    obj = obj + global_boundary(0, xring + bd.cols);
     named_sync(kBarCompute, kCW);
     long long c0 = tick ? clock64() : 0, c1 = 0;
     double m_old = 0.0, m2 = 0.0, m1 = 0.0, m0 = 0.0;  // infeasibility: <= t-3, t-2, t-1, t
@@ -485,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
     for (;; ++t) {
       const double* xt = xring + static_cast<std::size_t>(t % 4) * bd.cols;  // x^t
       double* xnext = xring + static_cast<std::size_t>((t + 1) % 4) * bd.cols;
-      double* u_out = p.u + (t & 1) * p.rows_total;
+      unsigned long long* u_out = p.ux + static_cast<int64_t>(t & 1) * 2 * p.rows_total;
       double* z_res = p.z_out + static_cast<int64_t>(t % 3) * p.rows_total;
       double* l_res = p.lam_out + static_cast<int64_t>(t % 3) * p.rows_total;
 
@@ -497,13 +526,13 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       }
       named_sync(kBarCompute, kCW);
       if (tick) {
-        c1 = clock64();
+        c1 = clock_after_barrier(ph);
         ph[kPhTarget] += c1 - c0;
         c0 = c1;
       }
 
-      // (L2) z = P t + v, one row per thread and slot k, P column-major per
-      // subsystem (consecutive threads read consecutive words). Each row's
+      // (L2) z = P t + v, one row per thread and slot k; P in sliced-ELL order
+      // (entry j of a warp's 32 rows is 256 contiguous bytes). Each row's
       // loads are issued 8 at a time ahead of its sequential-j sum.
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -520,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
               pv[e] = 0.0;
               tv[e] = 0.0;
               if (j0 + e < n) {
-                pv[e] = pr[(j0 + e) * n];
+                pv[e] = pr[(j0 + e) * 32];
                 tv[e] = tb[j0 + e];
               }
             }
@@ -534,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       // every row's target read before (D) overwrites tu; z visible to (A)
       named_sync(kBarCompute, kCW);
       if (tick) {
-        c1 = clock64();
+        c1 = clock_after_barrier(ph);
         ph[kPhGemv] += c1 - c0;
         c0 = c1;
       }
@@ -558,15 +587,15 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           lr[k] = ln / rho;  // reused as lambda/rho by the next target (admm.cpp:136)
           const double u = z - lr[k];
           tu[r] = u;
-          if (row_exported(rpk[k])) u_out[bd.row0 + r] = u;
+          if (row_exported(rpk[k]))
+            st_tagged(u_out + 2 * static_cast<int64_t>(bd.row0 + r), static_cast<unsigned long long>(t), u);
           lam[k] = ln;
           zp[k] = z;
         }
       }
-      named_arrive(kBarPublish, kThreads);
       named_sync(kBarCompute, kCW);  // every u(t) in shared memory
       if (tick) {
-        c1 = clock64();
+        c1 = clock_after_barrier(ph);
         ph[kPhDual] += c1 - c0;
         c0 = c1;
       }
@@ -595,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
               av[e] = 0.0;
               zv[e] = 0.0;
               if (j0 + e < am.n) {
-                av[e] = ar[(j0 + e) * am.m];
+                av[e] = ar[(j0 + e) * 32];
                 zv[e] = zb[j0 + e];
               }
             }
@@ -624,25 +653,25 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       }
       named_arrive(kBarPartials, kThreads);
       if (tick) {
-        c1 = clock64();
+        c1 = clock_after_barrier(ph);
         ph[kPhEqRed] += c1 - c0;
         c0 = c1;
       }
-      named_sync(kBarExchanged, kThreads);
+      // (G, boundary) x^{t+1} of the columns shared with neighbours (waits for
+      // their u(t) records); x^{t+1} is speculative until the stop test
+      obj = obj_next + global_boundary(t, xnext);
       if (tick) {
-        c1 = clock64();
+        c1 = clock_after_barrier(ph);
+        ph[kPhGlobal] += c1 - c0;
+        c0 = c1;
+      }
+      named_sync(kBarExchanged, kThreads);  // decision of t-2 in dec[]; x^{t+1} complete
+      if (tick) {
+        c1 = clock_after_barrier(ph);
         ph[kPhWait] += c1 - c0;
         c0 = c1;
       }
       if ((t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter) break;
-      // (G, boundary) x^{t+1} of the columns shared with neighbours
-      obj = obj_next + global_boundary(u_out, xnext);
-      named_sync(kBarCompute, kCW);
-      if (tick) {
-        c1 = clock64();
-        ph[kPhGlobal] += c1 - c0;
-        c0 = c1;
-      }
     }
     m_fold[0] = m_old;
     m_fold[1] = m2;

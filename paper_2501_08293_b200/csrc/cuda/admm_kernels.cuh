@@ -9,7 +9,8 @@
 
 namespace dopf::cuda {
 
-constexpr int kCtlWords = 64;  // per instance: counter (line 0), decision seq (line 1), ring (lines 2-3)
+constexpr int kCtlWords = 64;
+constexpr int kSlotRing = 4;   // residual-slot ring depth (admm_kernels.cu)  // per instance: counter (line 0), decision seq (line 1), ring (lines 2-3)
 
 enum class SyncMode : int32_t { block = 0, cluster = 1, grid = 2 };
 
@@ -30,11 +31,11 @@ struct KernelParams {
   const AMeta* ameta;
   const double* ab;
   const int32_t* nbrs;  // neighbour lists (BlockDesc::nbr_off / nbr_cnt)
-  double* u;            // [2][rows_total] exchange values u = z - lambda/rho
+  unsigned long long* ux;  // [2][rows_total][2] tagged exchange records {t, u = z - lambda/rho}
   double* z_out;        // [rows_total]
   double* lam_out;      // [rows_total]
   double* x_out;        // [x_total]
-  double* part;         // [instances][3][blocks_per_instance][kPartials] residual slots
+  double* part;         // [instances][kSlotRing][blocks_per_instance][kPartials] residual slots
   unsigned long long* flags;  // [instances][blocks_per_instance][16] "u(t) published", one per 128-B line
   unsigned long long* ctl;    // [instances][kCtlWords]: slot counter, decision seq, decision ring
   double* trace;        // [instances][trace_stride][6] (may be null)

@@ -146,11 +146,11 @@ void upload_layout(dopf_cuda_ctx* c) {
   c->d_ab = c->put(L.ab);
   c->d_nbrs = c->put(L.nbrs);
   const std::size_t I = L.inst.size();
-  c->d_u = c->scratch<double>(2 * static_cast<std::size_t>(L.rows_total));
+  c->d_u = c->scratch<double>(4 * static_cast<std::size_t>(L.rows_total));  // tagged records
   c->d_z = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));    // [t % 3][row]
   c->d_lam = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));
   c->d_x = c->scratch<double>(L.x_total);
-  c->d_part = c->scratch<double>(I * 3 * L.blocks_per_instance * kPartials);
+  c->d_part = c->scratch<double>(I * kSlotRing * L.blocks_per_instance * kPartials);
   c->d_flags = c->scratch<unsigned long long>(I * L.blocks_per_instance * 16);
   c->d_ctl = c->scratch<unsigned long long>(I * kCtlWords);
   c->d_iters = c->scratch<int32_t>(I);
@@ -220,10 +220,12 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
      "memset");
   ck(cudaMemsetAsync(c->d_ctl, 0, I * kCtlWords * sizeof(unsigned long long), c->stream), "memset");
   ck(cudaMemsetAsync(c->d_maxinf, 0, I * sizeof(double), c->stream), "memset");
-  ck(cudaMemsetAsync(c->d_part, 0, I * 3 * L.blocks_per_instance * kPartials * sizeof(double), c->stream),
+  ck(cudaMemsetAsync(c->d_part, 0, I * kSlotRing * L.blocks_per_instance * kPartials * sizeof(double), c->stream),
      "memset");
-  ck(cudaMemcpyAsync(c->d_u, c->d_z0, L.rows_total * sizeof(double), cudaMemcpyDeviceToDevice,
-                     c->stream),
+  // u^0 records {tag 0, z^0} in buffer 0 (tags of buffer 1 = 0 never match t = 1)
+  ck(cudaMemsetAsync(c->d_u, 0, 4 * L.rows_total * sizeof(double), c->stream), "memset");
+  ck(cudaMemcpy2DAsync(c->d_u + 1, 2 * sizeof(double), c->d_z0, sizeof(double), sizeof(double),
+                       L.rows_total, cudaMemcpyDeviceToDevice, c->stream),
      "u0");
 
   KernelParams p{};
@@ -243,7 +245,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.ameta = c->d_ameta;
   p.ab = c->d_ab;
   p.nbrs = c->d_nbrs;
-  p.u = c->d_u;
+  p.ux = reinterpret_cast<unsigned long long*>(c->d_u);
   p.z_out = c->d_z;
   p.lam_out = c->d_lam;
   p.x_out = c->d_x;

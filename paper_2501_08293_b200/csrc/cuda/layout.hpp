@@ -11,9 +11,11 @@
 //    reordered by n_s (descending) so warps see uniform GEMV lengths.
 //  * A "device row" is one local variable (s, i). z, lambda and the exchange
 //    value u = z - lambda/rho are stored in device-row order.
-//  * P_s and A_s are packed per block, column-major per subsystem, so the
-//    threads owning rows i = 0..n_s-1 of a subsystem read consecutive
-//    addresses at every step j (coalesced in HBM, conflict-free in smem).
+//  * P_s and A_s rows are packed per block in sliced-ELL order: the rows a
+//    warp owns in one thread slot form a slice, stored entry-major (entry j
+//    of lane l at slice_off + 32 j + l, zero-padded to the slice's widest
+//    row), so each step j of a warp reads 256 contiguous bytes (coalesced in
+//    HBM, conflict-free in smem).
 //  * Each block computes the global update x_i for every column its rows
 //    reference, from the copies' u values (CSR by column, ascending s, the
 //    reference's summation order): copies held by the block itself are read
@@ -73,7 +75,7 @@ struct InstDesc {
 
 // Row task: z_i = sum_j P(i,j) t_j + v_i for one (s, i).
 struct RowMeta {
-  int32_t pofs;      // offset of P(i, 0) within the block's P (column-major: stride n)
+  int32_t pofs;      // slice_off + lane: entry j of this row at pofs + 32 j in the block's P
   int16_t n;         // n_s
   int16_t exported;  // 1: another block reads this row's u (store it to global memory)
   int32_t base;      // block-local row index of (s, 0)
@@ -96,7 +98,7 @@ struct ColMeta {
 
 // Equality-check task: |A_r z_s - b_r| for one reduced row of a subsystem.
 struct AMeta {
-  int32_t aofs;   // offset of A(r, 0) within the block's A (column-major: stride m)
+  int32_t aofs;   // slice_off + lane: entry j of this row at aofs + 32 j in the block's A
   int32_t m;      // m_s
   int32_t n;      // n_s
   int32_t base;   // block-local row index of (s, 0)

@@ -208,36 +208,58 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     bd.cols_int = static_cast<int32_t>(mid - cols.begin());
     for (std::size_t q = 0; q < cols.size(); ++q) xloc_of[cols[q]] = static_cast<int>(q);
 
-    int32_t local = 0, pofs = 0, aofs = 0;
+    // Rows (and equality rows) go to thread slots r = k * cw + ctid; the 32
+    // rows of one warp and slot k form a "slice" whose operator rows are
+    // stored interleaved: entry j of the slice's lane l at slice_off + 32 j + l
+    // (sliced ELL). Every shared-memory read of a warp is then 256 contiguous
+    // bytes -- conflict-free -- and the kernel's row offsets are immediates.
+    const int cw = opt.threads - 32;
+    struct RowSrc { const double* src; int n; };  // operator row (contiguous, n entries)
+    std::vector<RowSrc> prow, arow;
+    int32_t local = 0;
     for (int s : order[g]) {
       const int n = ns_of(m, s), ms = m.m_s[s];
       const int base = local;
       const double* Ps = m.P + m.p_offsets[s];  // row-major n x n
-      for (int j = 0; j < n; ++j)
-        for (int i = 0; i < n; ++i) L.P.push_back(Ps[i * n + j]);
       const double* As = m.A + m.a_offsets[s];  // row-major ms x n
-      for (int j = 0; j < n; ++j)
-        for (int r = 0; r < ms; ++r) L.A.push_back(As[r * n + j]);
       for (int i = 0; i < n; ++i) {
         const int ref = m.z_offsets[s] + i;
         const int32_t dev = bd.row0 + local;
-        L.rmeta[dev] = RowMeta{pofs + i, static_cast<int16_t>(n), 0, base, xloc_of[m.l2g[ref]]};
+        L.rmeta[dev] = RowMeta{0, static_cast<int16_t>(n), 0, base, xloc_of[m.l2g[ref]]};
         L.v[dev] = m.v[ref];
         L.z0[dev] = m.z0[ref];
         L.ref_of_dev[dev] = ref;
+        prow.push_back(RowSrc{Ps + static_cast<std::size_t>(i) * n, n});
         ++local;
       }
       for (int r = 0; r < ms; ++r) {
-        L.ameta.push_back(AMeta{aofs + r, ms, n, base});
+        L.ameta.push_back(AMeta{0, ms, n, base});
         L.ab.push_back(m.b[m.b_offsets[s] + r]);
+        arow.push_back(RowSrc{As + static_cast<std::size_t>(r) * n, n});
       }
-      pofs += n * n;
-      aofs += ms * n;
     }
+    // pack rows into slices; returns the doubles appended; offs[r] = slice_off + lane
+    auto pack = [&](const std::vector<RowSrc>& rows, std::vector<double>& out, auto&& set_off) {
+      const int count = static_cast<int>(rows.size());
+      int32_t len = 0;
+      for (int k0 = 0; k0 < count; k0 += cw) {
+        for (int w0 = k0; w0 < std::min(count, k0 + cw); w0 += 32) {
+          const int lanes = std::min(32, count - w0);
+          int width = 0;
+          for (int l = 0; l < lanes; ++l) width = std::max(width, rows[w0 + l].n);
+          for (int l = 0; l < lanes; ++l) set_off(w0 + l, len + l);
+          for (int j = 0; j < width; ++j)
+            for (int l = 0; l < 32; ++l)
+              out.push_back(l < lanes && j < rows[w0 + l].n ? rows[w0 + l].src[j] : 0.0);
+          len += 32 * width;
+        }
+      }
+      return len;
+    };
+    bd.p_len = pack(prow, L.P, [&](int r, int32_t o) { L.rmeta[bd.row0 + r].pofs = o; });
+    bd.a_len = pack(arow, L.A, [&](int a, int32_t o) { L.ameta[bd.amet_off + a].aofs = o; });
     bd.rows = local;
     bd.arows = static_cast<int32_t>(L.ameta.size()) - bd.amet_off;
-    bd.p_len = pofs;
-    bd.a_len = aofs;
     bd.cols = static_cast<int32_t>(cols.size());
     for (int c : cols) {
       ColMeta cm{};
@@ -286,7 +308,6 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     if (!bd.ops_in_smem) L.all_ops_in_smem = false;
     L.smem_bytes = std::max(L.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
     // warps 1.. (opt.threads - 32 threads) own rows, columns and equality rows
-    const int cw = opt.threads - 32;
     const int k_need = (std::max(bd.rows, std::max(bd.cols, bd.arows)) + cw - 1) / cw;
     L.K = std::max(L.K, std::max(1, k_need));
     L.blocks.push_back(bd);

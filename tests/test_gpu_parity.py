@@ -146,3 +146,21 @@ def solver_batch(models, settings):
     bs = BatchSolver(0)
     bs.upload(models)
     return bs.solve(settings)
+
+
+@pytest.mark.timeout(600)
+def test_ieee8500_full_solve_bitwise(solver):
+    """The paper's largest case to convergence: identical iteration count and
+    bitwise-identical x, z, lambda (the multi-block exchange protocol at scale)."""
+    f = dopf.synthetic_feeder("ieee8500", 8500)
+    _, _, model = dopf.load_model(f, workers=8)
+    model.precompute(8)
+    settings = dopf.Settings()
+    solver.upload(model)
+    gpu = solver.solve(settings)
+    ref = O.solve(model, dopf.Settings(workers=8))
+    assert gpu.status == dopf.CONVERGED
+    assert_same(gpu, ref, bitwise=True)
+    again = solver.solve(settings)  # run-to-run determinism of the device loop
+    assert again.iterations == gpu.iterations
+    assert np.array_equal(again.trace, gpu.trace)
