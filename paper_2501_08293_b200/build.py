@@ -24,9 +24,13 @@ ORACLE_BUILD = os.path.join(ORACLE_DIR, "_build")
 
 HOST_SO = os.path.join(LIB, "libdopf_host.so")
 CUDA_SO = os.path.join(LIB, "libdopf_cuda.so")
+DROPIN_TEST = os.path.join(LIB, "dopf_dropin_test")
 ORACLE_SO = os.path.join(ORACLE_BUILD, "libdopf_oracle.so")
 
-CXX = os.environ.get("CXX", "g++")
+# The system g++ links libstdc++ dynamically; a CXX wrapper that links it
+# statically into the .so (seen in this image: /opt/gcc) breaks iostreams
+# inside a Python process, so the system compiler wins when present.
+CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else os.environ.get("CXX", "g++")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
             "-Wno-dangling-reference", "-I", os.path.join(ROOT, "include")]
@@ -100,7 +104,19 @@ def build_cuda(verbose: bool = False) -> str:
     if _newer(CUDA_SO, objs + [HOST_SO]):
         _run([NVCC, "-shared", "-o", CUDA_SO, *objs, "-L", LIB, "-ldopf_host",
               "-Xlinker", "-rpath,$ORIGIN", "-lcudart"])
+    build_dropin_test()
     return CUDA_SO
+
+
+def build_dropin_test() -> str:
+    """C++ program calling dopf::solve from libdopf_cuda.so as reference code would."""
+    src = os.path.join(ROOT, "tests", "cpp", "dropin_test.cpp")
+    hdrs = _headers(os.path.join(ROOT, "include"), os.path.join(ROOT, "include", "dopf"),
+                    os.path.join(PKG, "csrc", "host"))
+    if _newer(DROPIN_TEST, [src, CUDA_SO, HOST_SO] + hdrs):
+        _run([CXX, *CXXFLAGS, src, "-o", DROPIN_TEST, "-L", LIB, "-ldopf_cuda", "-ldopf_host",
+              "-Wl,-rpath,$ORIGIN", "-lpthread"])
+    return DROPIN_TEST
 
 
 def build_oracle(verbose: bool = False) -> str:

@@ -1,0 +1,151 @@
+// C++ drop-in solver over the C ABI (include/dopf/cuda_solve.hpp).
+#include "../../../include/dopf/cuda_solve.hpp"
+
+#include <chrono>
+#include <stdexcept>
+#include <string>
+
+#include "../../../include/dopf_cuda.h"
+#include "../host/flat_model.hpp"
+
+namespace dopf::cuda {
+
+namespace {
+
+[[noreturn]] void raise(int code, const std::string& msg) {
+  switch (code) {
+    case DOPF_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case DOPF_ERR_LOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+void check_settings(const Settings& s) {  // reference admm.cpp:173-175
+  if (!(s.rho > 0)) throw std::invalid_argument("rho must be positive");
+  if (!(s.eps_rel > 0)) throw std::invalid_argument("eps_rel must be positive");
+  if (s.max_iter < 1) throw std::invalid_argument("max_iter must be positive");
+}
+
+dopf_settings to_c(const Settings& s) {
+  dopf_settings c{};
+  c.rho = s.rho;
+  c.eps_rel = s.eps_rel;
+  c.max_iter = s.max_iter;
+  c.workers = s.workers;
+  c.record_iterates = 0;
+  return c;
+}
+
+}  // namespace
+
+struct Solver::Impl {
+  dopf_cuda_ctx* ctx = nullptr;
+  const DecomposedModel* model = nullptr;
+  Precomputed pre;
+  FlatModel flat;
+  double precompute_s = 0;
+
+  void check(int rc) {
+    if (rc != DOPF_OK) raise(rc, dopf_cuda_last_error(ctx));
+  }
+
+  // one device run to at most settings.max_iter iterations
+  void run(const Settings& s, SolveResult& r, bool with_trace) {
+    const int n = model->global_cols, Nz = model->total_local_vars();
+    r.x.assign(n, 0.0);
+    r.z.assign(Nz, 0.0);
+    r.lambda.assign(Nz, 0.0);
+    std::vector<double> trace(with_trace ? static_cast<std::size_t>(s.max_iter) * DOPF_TRACE_WIDTH : 0);
+    dopf_result_view v{};
+    v.x = r.x.data();
+    v.z = r.z.data();
+    v.lambda = r.lambda.data();
+    v.trace = with_trace ? trace.data() : nullptr;
+    const dopf_settings cs = to_c(s);
+    check(dopf_cuda_solve(ctx, &cs, &v));
+    r.status = v.status == DOPF_CONVERGED ? SolveStatus::converged : SolveStatus::iteration_limit;
+    r.iterations = v.iterations;
+    r.objective = v.objective;
+    r.max_local_infeasibility = v.max_local_infeasibility;
+    r.trace.clear();
+    if (with_trace) {
+      r.trace.resize(v.iterations);
+      for (int t = 0; t < v.iterations; ++t) {
+        const double* row = trace.data() + static_cast<std::size_t>(t) * DOPF_TRACE_WIDTH;
+        r.trace[t] = TraceRow{static_cast<int>(row[0]), row[1], row[2], row[3], row[4], row[5]};
+      }
+    }
+    r.timings.precompute = precompute_s;
+    r.timings.global = v.time_global;
+    r.timings.local = v.time_local;
+    r.timings.dual = v.time_dual;
+  }
+};
+
+Solver::Solver(int device) : impl_(std::make_unique<Impl>()) {
+  const int rc = dopf_cuda_create(device, &impl_->ctx);
+  if (rc != DOPF_OK) raise(rc, "dopf_cuda_create failed (no usable CUDA device " + std::to_string(device) + ")");
+}
+
+Solver::~Solver() {
+  if (impl_ && impl_->ctx) dopf_cuda_destroy(impl_->ctx);
+}
+
+void Solver::upload(const DecomposedModel& model, int workers) {
+  const auto t0 = std::chrono::steady_clock::now();
+  WorkerPool pool(workers < 1 ? 1 : workers);
+  impl_->pre = precompute(model, &pool);
+  impl_->precompute_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  impl_->flat.build(model, &impl_->pre);
+  const dopf_model_view view = impl_->flat.view(model, &impl_->pre);
+  impl_->check(dopf_cuda_upload(impl_->ctx, &view));
+  impl_->model = &model;
+}
+
+SolveResult Solver::solve(const Settings& settings) {
+  check_settings(settings);
+  if (!impl_->model) throw std::invalid_argument("no model uploaded");
+  SolveResult result;
+  impl_->run(settings, result, true);
+  if (settings.record_iterates) {
+    // IterateSnapshot{x, z, z_prev, lambda} after every iteration t
+    // (admm.cpp:228-229): the device loop is deterministic, so the state
+    // after t iterations is the result of a run capped at max_iter = t.
+    result.snapshots.resize(result.iterations);
+    std::vector<double> z_prev;
+    {
+      FlatModel& f = impl_->flat;
+      z_prev = f.z0;
+    }
+    for (int t = 1; t <= result.iterations; ++t) {
+      Settings capped = settings;
+      capped.max_iter = t;
+      SolveResult r;
+      impl_->run(capped, r, false);
+      IterateSnapshot& snap = result.snapshots[t - 1];
+      snap.x = std::move(r.x);
+      snap.z = r.z;
+      snap.z_prev = z_prev;
+      snap.lambda = std::move(r.lambda);
+      z_prev = std::move(r.z);
+    }
+  }
+  return result;
+}
+
+SolveResult solve(const DecomposedModel& model, const Settings& settings, int device) {
+  check_settings(settings);
+  Solver solver(device);
+  solver.upload(model, settings.workers);
+  return solver.solve(settings);
+}
+
+}  // namespace dopf::cuda
+
+namespace dopf {
+
+SolveResult solve(const DecomposedModel& model, const Settings& settings) {
+  return cuda::solve(model, settings, 0);
+}
+
+}  // namespace dopf

@@ -10,6 +10,7 @@
 #include "admm.hpp"
 #include "decompose.hpp"
 #include "feeder.hpp"
+#include "flat_model.hpp"
 #include "lp_builder.hpp"
 #include "synth.hpp"
 
@@ -29,9 +30,7 @@ struct dopf_model {
   double precompute_seconds = 0.0;
   // flattened view storage (built lazily, invalidated by mutation)
   bool flat_ready = false;
-  std::vector<int32_t> m_s, l2g, b_offsets;
-  std::vector<int64_t> a_offsets, p_offsets;
-  std::vector<double> A, b, P, v, x0, z0;
+  dopf::FlatModel flat;
 };
 
 namespace {
@@ -79,46 +78,7 @@ int emit_text(const std::string& text, char* buf, size_t cap, size_t* needed) {
 
 void flatten(dopf_model* m) {
   if (m->flat_ready) return;
-  const auto& md = m->model;
-  const int S = md.subsystem_count();
-  m->m_s.assign(S, 0);
-  m->a_offsets.assign(S + 1, 0);
-  m->p_offsets.assign(S + 1, 0);
-  m->b_offsets.assign(S + 1, 0);
-  m->l2g.clear();
-  for (int s = 0; s < S; ++s) {
-    const auto& sub = md.subsystems[s];
-    m->m_s[s] = sub.row_count();
-    m->a_offsets[s + 1] = m->a_offsets[s] + static_cast<int64_t>(sub.row_count()) * sub.col_count();
-    m->p_offsets[s + 1] = m->p_offsets[s] + static_cast<int64_t>(sub.col_count()) * sub.col_count();
-    m->b_offsets[s + 1] = m->b_offsets[s] + sub.row_count();
-    m->l2g.insert(m->l2g.end(), sub.local_to_global.begin(), sub.local_to_global.end());
-  }
-  m->A.resize(m->a_offsets[S]);
-  m->b.resize(m->b_offsets[S]);
-  for (int s = 0; s < S; ++s) {
-    const auto& sub = md.subsystems[s];
-    std::copy(sub.A.a.begin(), sub.A.a.end(), m->A.begin() + m->a_offsets[s]);
-    std::copy(sub.b.begin(), sub.b.end(), m->b.begin() + m->b_offsets[s]);
-  }
-  m->x0.resize(md.global_cols);
-  for (int i = 0; i < md.global_cols; ++i) m->x0[i] = dopf::initial_value(md, i);
-  m->z0.resize(md.total_local_vars());
-  for (std::size_t k = 0; k < m->l2g.size(); ++k) m->z0[k] = m->x0[m->l2g[k]];
-  if (m->has_pre) {
-    m->P.resize(m->p_offsets[S]);
-    m->v.resize(md.total_local_vars());
-    for (int s = 0; s < S; ++s) {
-      const auto& ps = m->pre.subs[s];
-      std::copy(ps.kernel_projector.a.begin(), ps.kernel_projector.a.end(),
-                m->P.begin() + m->p_offsets[s]);
-      std::copy(ps.min_norm_solution.begin(), ps.min_norm_solution.end(),
-                m->v.begin() + md.z_offsets[s]);
-    }
-  } else {
-    m->P.clear();
-    m->v.clear();
-  }
+  m->flat.build(m->model, m->has_pre ? &m->pre : nullptr);
   m->flat_ready = true;
 }
 
@@ -349,29 +309,7 @@ int dopf_model_view_get(const dopf_model* cm, dopf_model_view* out) {
   auto* m = const_cast<dopf_model*>(cm);
   return guarded([&] {
     flatten(m);
-    const auto& md = m->model;
-    out->S = md.subsystem_count();
-    out->n = md.global_cols;
-    out->N_z = md.total_local_vars();
-    out->has_pre = m->has_pre ? 1 : 0;
-    out->z_offsets = md.z_offsets.data();
-    out->l2g = m->l2g.data();
-    out->m_s = m->m_s.data();
-    out->a_offsets = m->a_offsets.data();
-    out->A = m->A.data();
-    out->b_offsets = m->b_offsets.data();
-    out->b = m->b.data();
-    out->p_offsets = m->p_offsets.data();
-    out->P = m->has_pre ? m->P.data() : nullptr;
-    out->v = m->has_pre ? m->v.data() : nullptr;
-    out->inv_copy = m->has_pre ? m->pre.inv_copy_counts.data() : nullptr;
-    out->csr_ptr = m->has_pre ? m->pre.col_ptr.data() : nullptr;
-    out->csr_copy = m->has_pre ? m->pre.copy_index.data() : nullptr;
-    out->c = md.c.data();
-    out->x_lo = md.x_lo.data();
-    out->x_hi = md.x_hi.data();
-    out->x0 = m->x0.data();
-    out->z0 = m->z0.data();
+    *out = m->flat.view(m->model, m->has_pre ? &m->pre : nullptr);
   });
 }
 

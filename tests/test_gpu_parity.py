@@ -164,3 +164,16 @@ def test_ieee8500_full_solve_bitwise(solver):
     again = solver.solve(settings)  # run-to-run determinism of the device loop
     assert again.iterations == gpu.iterations
     assert np.array_equal(again.trace, gpu.trace)
+
+
+def test_cpp_dropin_program():
+    """Reference-style C++ caller of dopf::solve linked against libdopf_cuda.so."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+    from paper_2501_08293_b200 import build
+    proc = subprocess.run([build.DROPIN_TEST, os.path.join(ROOT, "tests", "golden", "fixtures")],
+                          capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stdout + proc.stderr
+    assert "PASS" in proc.stdout
