@@ -2,25 +2,36 @@
 time-to-converge, IEEE 8500-bus; HBM GB/s vs peak).
 
 A "step" is one complete solve to convergence (reference dopf::solve,
-admm.cpp:172-244) of the synthetic IEEE-8500-shape feeder (SURVEY.md section
-8d; seed 8500, rho = 100, eps_rel = 1e-3, max_iter = 50000).
+admm.cpp:172-244) of the configured workload (rho = 100, eps_rel = 1e-3,
+max_iter = 50000, the paper's settings):
 
-  value  iterations / second on the device: sum of iterations over the K timed
-         solves / sum of their kernel times (CUDA events on the launching
-         stream), inputs resident in HBM; L2 flushed (256 MiB write) between
-         solves.
-  e2e    the same metric through the reference-facing C ABI with HOST buffers:
-         dopf_cuda_upload (host model -> HBM layout) + dopf_cuda_solve (results
-         copied back into host x / z / lambda / trace) per step.
-  roofline  algorithmic bytes of one launch (B_iter x iterations, BASELINE.md
-         section 3) / kernel time, against MEASURED_PEAKS.json hbm_gbs.
-  cpu_baseline  the CPU oracle (restatement of the reference loop, all host
-         threads) on a bounded sample of the same workload.
+  --config ieee8500  (default) the synthetic IEEE-8500-shape feeder, one
+                     instance per GPU (BASELINE configs[2], the metric's case)
+  --config ieee123 / ieee13   single instances of the smaller shapes
+  --config batch123  --scenarios K independent load scenarios of the
+                     IEEE-123 shape (configs[4]), sharded over ranks
 
---impl reference times the reference's CPU path (the oracle port: the C++
-reference cannot be built here) on the same config and metric.
-Multi-GPU (torchrun, N > 1): independent load scenarios of the 8500 feeder,
-one per rank (scenario sharding, no per-iteration collective; "weak").
+Line keys:
+  value     ADMM iterations / second on the device: iterations of the K timed
+            solves (summed over scenarios for a batch) / their kernel time
+            (CUDA events on the launching stream); inputs resident in HBM;
+            L2 flushed (256 MiB write) between solves. N > 1: whole job, time =
+            max over ranks.
+  e2e       the same metric through the reference-facing C ABI with HOST
+            buffers: dopf_cuda_upload(_batch) (host model -> HBM layout) +
+            dopf_cuda_solve(_batch) (x / z / lambda / trace copied back into
+            host buffers) per step.
+  roofline  algorithmic bytes (B_iter per iteration x
+            iterations of one launch) / kernel time, against
+            MEASURED_PEAKS.json hbm_gbs; traffic = ncu DRAM bytes per launch.
+  cpu_baseline  the CPU oracle (C++ restatement of the reference loop, all
+            host threads) on a bounded sample of the same workload.
+
+--impl reference times the reference's CPU path (the oracle port -- the C++
+reference cannot be built here) on the same config and
+metric. Multi-GPU (torchrun, N > 1): ieee8500 runs one independent load
+scenario per rank; batch123 shards the scenarios (no per-iteration
+collective; "weak" for ieee8500, "strong" for a fixed batch).
 """
 from __future__ import annotations
 
@@ -36,6 +47,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SINGLE = {"ieee8500": 8500, "ieee123": 123, "ieee13": 13}
+
 
 def parse_args():
     ap = argparse.ArgumentParser()
@@ -43,12 +56,19 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--shape", default="ieee8500")
-    ap.add_argument("--seed", type=int, default=8500)
+    ap.add_argument("--config", default="ieee8500", choices=sorted(SINGLE) + ["batch123"])
+    ap.add_argument("--shape", default=None, help="alias of --config for single instances")
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--scenarios", type=int, default=4096, help="batch123: total scenarios")
     ap.add_argument("--cpu-sample-iters", type=int, default=0,
                     help="iterations per CPU sample (0: auto, ~10-30 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.shape:
+        args.config = args.shape
+    if args.seed is None:
+        args.seed = SINGLE.get(args.config, 123)
+    return args
 
 
 def dist_env():
@@ -80,7 +100,7 @@ class ClockSampler:
                     self.samples.append([s.strip() for s in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -104,30 +124,67 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def build_model(shape: str, seed: int, rank: int, workers: int):
-    from paper_2501_08293_b200 import dopf
-    f = dopf.synthetic_feeder(shape, seed)
-    if rank > 0:  # scenario sharding: rank r solves load scenario r
-        f = dopf.scale_loads(f, seed * 1000 + rank)
-    _, ls, model = dopf.load_model(f, workers=workers)
+# ------------------------------------------------------------------ workloads
+
+
+def build_models(args, rank, world, workers):
+    """The rank's models: [one instance] or [its shard of the scenarios]."""
+    from paper_2501_08293_b200 import dopf, scenarios
+    if args.config == "batch123":
+        b, e = scenarios.shard(args.scenarios, world, rank)
+        return scenarios.build_scenarios("ieee123", args.seed, range(b, e), workers)
+    f = dopf.synthetic_feeder(args.config, args.seed)
+    if rank > 0:  # weak scaling: rank r solves load scenario r of the same feeder
+        f = dopf.scale_loads(f, scenarios.scenario_seed(args.seed, rank))
+    _, _, model = dopf.load_model(f, workers=workers)
     model.precompute(workers)
-    return ls, model
+    return [model]
 
 
-def cpu_sample(model, settings_kw, sample_iters, workers):
-    """Oracle (restated reference CPU path) on a bounded sample."""
+def metric_name(args):
+    return "admm_iterations_per_second_" + ("batch4096_ieee123" if args.config == "batch123"
+                                            else args.config)
+
+
+def config_of(args, world):
+    if args.config == "batch123":
+        w = (f"{args.scenarios} independent load scenarios of the synthetic ieee123 feeder "
+             f"(seed {args.seed}, loads scaled U[0.5,1.5]), each solved to convergence "
+             "(rho=100, eps_rel=1e-3, max_iter=50000); value = scenario-iterations/s")
+        par = f"scenario-sharded over {world} rank(s)" if world > 1 else "single-gpu"
+    else:
+        w = (f"{args.config} synthetic feeder (seed {args.seed}), single instance per GPU, "
+             "solve to convergence (rho=100, eps_rel=1e-3, max_iter=50000)")
+        par = "independent scenario per rank" if world > 1 else "single-gpu"
+    return {"workload": w, "parallelism": par, "l2": "flushed (256 MiB write) between timed solves"}
+
+
+def cpu_sample(models, settings_kw, sample_iters, workers):
+    """Oracle (restated reference CPU path): iterations/s on a bounded sample.
+    A batch is sampled scenario-parallel (one thread per scenario)."""
+    import concurrent.futures as cf
+
     from oracle import oracle_py as O
     from paper_2501_08293_b200 import dopf
-    st = dopf.Settings(**{**settings_kw, "max_iter": sample_iters, "workers": workers})
+    if len(models) == 1:
+        st = dopf.Settings(**{**settings_kw, "max_iter": sample_iters, "workers": workers})
+        t0 = time.perf_counter()
+        r = O.solve(models[0], st)
+        dt = time.perf_counter() - t0
+        return r.iterations / dt, r.iterations, dt, 1
+    sample = models[:workers]
+    st = dopf.Settings(**{**settings_kw, "max_iter": sample_iters, "workers": 1})
     t0 = time.perf_counter()
-    r = O.solve(model, st)
+    with cf.ThreadPoolExecutor(max_workers=len(sample)) as ex:
+        its = sum(r.iterations for r in ex.map(lambda m: O.solve(m, st), sample))
     dt = time.perf_counter() - t0
-    return r.iterations / dt, r.iterations, dt
+    return its / dt, its, dt, len(sample)
 
 
-def auto_cpu_iters(model, workers, settings_kw, target_s=12.0):
-    it_s, _, _ = cpu_sample(model, settings_kw, 20, workers)
-    return max(20, min(50000, int(it_s * target_s)))
+def auto_cpu_iters(models, workers, settings_kw, target_s=12.0):
+    it_s, its, dt, n = cpu_sample(models, settings_kw, 20, workers)
+    per_scen = it_s / max(1, n)
+    return max(20, min(50000, int(per_scen * target_s)))
 
 
 def read_peaks():
@@ -140,41 +197,53 @@ def read_peaks():
 
 
 def run_reference(args, rank, world):
+    """The reference's CPU path (oracle port) on this config: rank 0 only."""
     if rank != 0:
         return
     workers = os.cpu_count() or 1
     settings_kw = dict(rho=100.0, eps_rel=1e-3)
-    _, model = build_model(args.shape, args.seed, 0, workers)
-    iters = args.cpu_sample_iters or auto_cpu_iters(model, workers, settings_kw, target_s=8.0)
+    if args.config == "batch123":
+        from paper_2501_08293_b200 import scenarios
+        models = scenarios.build_scenarios("ieee123", args.seed, range(workers), workers)
+    else:
+        models = build_models(args, 0, 1, workers)
+    iters = args.cpu_sample_iters or auto_cpu_iters(models, workers, settings_kw, target_s=8.0)
     for _ in range(args.warmup):
-        cpu_sample(model, settings_kw, max(5, iters // 10), workers)
-    tot_it, tot_t = 0, 0.0
+        cpu_sample(models, settings_kw, max(5, iters // 10), workers)
+    tot_it, tot_t, n = 0, 0.0, 1
     for _ in range(args.steps):
-        _, it, dt = cpu_sample(model, settings_kw, iters, workers)
+        _, it, dt, n = cpu_sample(models, settings_kw, iters, workers)
         tot_it += it
         tot_t += dt
     value = tot_it / tot_t
+    what = (f"{iters} ADMM iterations of each of {n} scenarios (one thread per scenario)"
+            if n > 1 else f"{iters} ADMM iterations of the {args.config} solve (WorkerPool of {workers} threads)")
     line = {
         "impl": "reference",
-        "metric": "admm_iterations_per_second_ieee8500",
+        "metric": metric_name(args),
         "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_of(args, world),
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": workers, "kind": "port",
-                         "sample": f"{iters} ADMM iterations of the {args.shape} solve per step "
-                                   f"(C++ oracle restating admm.cpp:172-244, WorkerPool of "
-                                   f"{workers} threads)"},
+                         "sample": what + " per step; C++ oracle restating admm.cpp:172-244"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_of(args, world):
-    return {"workload": f"{args.shape} synthetic feeder (seed {args.seed}), single instance per GPU, "
-                        "solve to convergence (rho=100, eps_rel=1e-3, max_iter=50000)",
-            "parallelism": "scenario-sharded" if world > 1 else "single-gpu",
-            "l2": "flushed (256 MiB write) between timed solves"}
+def upload_bytes(models) -> int:
+    """Bytes dopf_cuda_upload copies host -> device (the device layout)."""
+    tot = 0
+    for model in models:
+        st = model.stats()
+        Nz = st["N_z"]
+        ops = 8 * (st["sum_n2"] + st["sum_mn"])
+        rows = Nz * (16 + 8 + 8)            # RowMeta + v + z0
+        cols = Nz * (16 + 32) + 4 * Nz      # column metadata (upper bound) + copies
+        arow = st["sum_m"] * (16 + 8)
+        tot += int(ops + rows + cols + arow + 80 * 148)
+    return tot
 
 
 def main():
@@ -202,22 +271,38 @@ def main():
     device = local
     torch.cuda.set_device(device)
     workers = max(1, (os.cpu_count() or 1) // max(1, world))
-    ls, model = build_model(args.shape, args.seed, rank, workers)
+    models = build_models(args, rank, world, workers)
+    batch = args.config == "batch123"
     settings = dopf.Settings(rho=100.0, eps_rel=1e-3, max_iter=50000)
     st = settings.to_c()
     lib = N.cuda()
     solver = dopf.CudaSolver(device)
-    solver.upload(model)
+    views = (N.ModelView_t * len(models))(*[m.view() for m in models])
+
+    def upload():
+        if batch:
+            return lib.dopf_cuda_upload_batch(solver._h, views, len(models))
+        return lib.dopf_cuda_upload(solver._h, C.byref(views[0]))
+
+    rc = upload()
+    if rc != 0:
+        raise RuntimeError(lib.dopf_cuda_last_error(solver._h).decode())
     info = solver.info()
-    b_iter = solver.bytes_per_iteration()
+    b_iter = solver.bytes_per_iteration() / len(models)   # one instance
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{device}")  # 256 MiB
+    K = len(models)
 
     def device_solve():
-        r = N.ResultView_t()
-        rc = lib.dopf_cuda_solve_device(solver._h, C.byref(st), C.byref(r))
+        rs = (N.ResultView_t * K)()
+        if batch:
+            rc = lib.dopf_cuda_solve_batch(solver._h, C.byref(st), rs, K)  # scalars only (null vectors)
+        else:
+            rc = lib.dopf_cuda_solve_device(solver._h, C.byref(st), rs)
         if rc != 0:
             raise RuntimeError(lib.dopf_cuda_last_error(solver._h).decode())
-        return r.iterations, r.status, lib.dopf_cuda_last_kernel_seconds(solver._h), r.objective
+        its = [rs[i].iterations for i in range(K)]
+        return its, [rs[i].status for i in range(K)], lib.dopf_cuda_last_kernel_seconds(solver._h), \
+            rs[0].objective
 
     for _ in range(max(3, args.warmup)):
         device_solve()
@@ -238,7 +323,7 @@ def main():
             per_step.append(device_solve())
         barrier()
     launches = solver.kernel_launches() - launches0
-    iters = [p[0] for p in per_step]
+    iters = [sum(p[0]) for p in per_step]
     ktime = [p[2] for p in per_step]
     tot_it, tot_t = sum(iters), sum(ktime)
     max_t = tot_t
@@ -252,31 +337,33 @@ def main():
     value = tot_it / max_t
 
     # end-to-end through the C ABI with host buffers (upload + solve + copies)
-    v = model.view()
-    n, Nz = v.n, v.N_z
-    x, z, lam = np.zeros(n), np.zeros(Nz), np.zeros(Nz)
-    trace = np.zeros((settings.max_iter, 6))
+    outs = []
+    for m in models:
+        v = m.view()
+        outs.append((np.zeros(v.n), np.zeros(v.N_z), np.zeros(v.N_z), np.zeros((settings.max_iter, 6))))
     e2e_t, e2e_it = 0.0, 0
-    h2d = 0
     for step in range(args.steps + 1):
-        r = N.ResultView_t()
-        r.x = x.ctypes.data_as(C.POINTER(C.c_double))
-        r.z = z.ctypes.data_as(C.POINTER(C.c_double))
-        r.lambda_ = lam.ctypes.data_as(C.POINTER(C.c_double))
-        r.trace = trace.ctypes.data_as(C.POINTER(C.c_double))
+        rs = (N.ResultView_t * K)()
+        for i, (x, z, lam, tr) in enumerate(outs):
+            rs[i].x = x.ctypes.data_as(C.POINTER(C.c_double))
+            rs[i].z = z.ctypes.data_as(C.POINTER(C.c_double))
+            rs[i].lambda_ = lam.ctypes.data_as(C.POINTER(C.c_double))
+            rs[i].trace = tr.ctypes.data_as(C.POINTER(C.c_double))
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rc = lib.dopf_cuda_upload(solver._h, C.byref(v))
-        rc = rc or lib.dopf_cuda_solve(solver._h, C.byref(st), C.byref(r))
+        rc = upload()
+        if rc == 0:
+            rc = (lib.dopf_cuda_solve_batch(solver._h, C.byref(st), rs, K) if batch
+                  else lib.dopf_cuda_solve(solver._h, C.byref(st), rs))
         dt = time.perf_counter() - t0
         if rc != 0:
             raise RuntimeError(lib.dopf_cuda_last_error(solver._h).decode())
         if step > 0:  # first pass warms the host allocator
             e2e_t += dt
-            e2e_it += r.iterations
-    h2d = upload_bytes(model)
-    d2h = 8 * (n + 2 * Nz) + 48 * int(np.mean(iters)) + 32
+            e2e_it += sum(rs[i].iterations for i in range(K))
+    h2d = upload_bytes(models)
+    d2h = sum(8 * (m.view().n + 2 * m.view().N_z) + 32 for m in models) + 48 * int(np.mean(iters))
     e2e_value = e2e_it / e2e_t
     if world > 1:
         import torch.distributed as td
@@ -286,7 +373,6 @@ def main():
         e2e_value = sum(float(a[1]) for a in all_t) / max(float(a[0]) for a in all_t)
 
     peak, peak_kind = read_peaks()
-    mean_it = tot_it / (args.steps * world)
     kernel_avg = tot_t / args.steps
     achieved = b_iter * (sum(iters) / args.steps) / kernel_avg / 1e9
     traffic = None
@@ -294,20 +380,21 @@ def main():
     if os.path.exists(tp):
         try:
             with open(tp) as fh:
-                traffic = json.load(fh).get(args.shape)
+                traffic = json.load(fh).get(args.config)
         except Exception:
             traffic = None
+    last_its, last_status = per_step[-1][0], per_step[-1][1]
 
     if rank == 0:
         line = {
-            "metric": "admm_iterations_per_second_ieee8500",
+            "metric": metric_name(args),
             "value": value, "unit": "iter/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": 1e3 * max_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_of(args, world),
+            "higher_is_better": True, "scaling": "strong" if (batch and world > 1) else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_of(args, world),
             "time_to_converge_ms": 1e3 * kernel_avg,
-            "iterations_to_converge": int(round(mean_it)),
-            "status": "converged" if all(p[1] == 0 for p in per_step) else "iteration_limit",
+            "iterations_to_converge": int(round(np.median(last_its))) if batch else int(last_its[0]),
+            "status": "converged" if all(s == 0 for s in last_status) else "iteration_limit",
             "objective": per_step[-1][3],
             "e2e": {"value": e2e_value, "unit": "iter/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
@@ -316,37 +403,30 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_iteration": b_iter,
-                         "note": "algorithmic bytes (BASELINE.md s3) x iterations / kernel time; "
+                         "note": "algorithmic bytes (DESIGN.md s4) x iterations / kernel time; "
                                  "operators are staged in shared memory once per launch, so "
                                  "DRAM traffic is far below the algorithmic bytes"},
-            "kernel": {"name": "admm_persistent", "ctas": info["blocks"], "threads": info["threads"],
+            "kernel": {"name": "admm_persistent", "ctas_per_instance": info["blocks"],
+                       "instances": info["instances"], "threads": info["threads"],
                        "smem_bytes": info["smem_bytes"], "resident": info["resident"],
                        "sync": info["sync"]},
             "clocks": clocks.summary(),
         }
+        if batch:
+            line["iterations_range"] = [int(min(last_its)), int(max(last_its))]
         if not args.no_cpu_baseline and world == 1:
             cores = os.cpu_count() or 1
             kw = dict(rho=100.0, eps_rel=1e-3)
-            it_n = args.cpu_sample_iters or auto_cpu_iters(model, cores, kw)
-            cps, cit, cdt = cpu_sample(model, kw, it_n, cores)
+            it_n = args.cpu_sample_iters or auto_cpu_iters(models, cores, kw)
+            cps, cit, cdt, n = cpu_sample(models, kw, it_n, cores)
+            what = (f"{it_n} ADMM iterations of each of {n} scenarios, one thread per scenario"
+                    if n > 1 else f"{cit} ADMM iterations of the {args.config} solve, {cores} threads")
             line["cpu_baseline"] = {"value": cps, "unit": "iter/s", "cores": cores, "kind": "port",
-                                    "sample": f"{cit} ADMM iterations of the {args.shape} solve "
-                                              f"({cdt:.1f} s, C++ oracle, {cores} threads)"}
+                                    "sample": f"{what} ({cdt:.1f} s, C++ oracle)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as td
         td.destroy_process_group()
-
-
-def upload_bytes(model) -> int:
-    """Bytes dopf_cuda_upload copies host -> device (the device layout)."""
-    st = model.stats()
-    S, n, Nz = st["S"], st["n"], st["N_z"]
-    ops = 8 * (st["sum_n2"] + st["sum_mn"])
-    rows = Nz * (16 + 8 + 8)            # RowMeta + v + z0
-    cols = Nz * (16 + 32) + 4 * Nz      # column metadata (upper bound) + copies
-    arow = st["sum_m"] * (16 + 8)
-    return int(ops + rows + cols + arow + 64 * 148)
 
 
 if __name__ == "__main__":

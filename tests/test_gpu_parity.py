@@ -177,3 +177,19 @@ def test_cpp_dropin_program():
                           capture_output=True, text=True, timeout=600)
     assert proc.returncode == 0, proc.stdout + proc.stderr
     assert "PASS" in proc.stdout
+
+
+@pytest.mark.timeout(900)
+def test_batch_ieee123_scenarios_bitwise():
+    """Config 5 shape: independent IEEE-123 load scenarios, each a multi-CTA
+    cluster instance with its own iteration count, bitwise equal to the oracle."""
+    from paper_2501_08293_b200 import scenarios
+    models = scenarios.build_scenarios("ieee123", 123, range(6))
+    settings = dopf.Settings()
+    results = solver_batch(models, settings)
+    its = set()
+    for m, gpu in zip(models, results):
+        ref = O.solve(m, dopf.Settings(workers=8))
+        assert_same(gpu, ref, bitwise=True)
+        its.add(gpu.iterations)
+    assert len(its) > 1  # scenarios really converge independently
