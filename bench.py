@@ -353,10 +353,15 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         rc = upload()
+        t_up = time.perf_counter() - t0
         if rc == 0:
             rc = (lib.dopf_cuda_solve_batch(solver._h, C.byref(st), rs, K) if batch
                   else lib.dopf_cuda_solve(solver._h, C.byref(st), rs))
         dt = time.perf_counter() - t0
+        if rank == 0 and step == args.steps:
+            print(f"e2e step: upload {1e3 * t_up:.1f} ms, solve+copies {1e3 * (dt - t_up):.1f} ms "
+                  f"(kernel {1e3 * lib.dopf_cuda_last_kernel_seconds(solver._h):.1f} ms)",
+                  file=sys.stderr, flush=True)
         if rc != 0:
             raise RuntimeError(lib.dopf_cuda_last_error(solver._h).decode())
         if step > 0:  # first pass warms the host allocator

@@ -92,6 +92,10 @@ typedef struct dopf_layout_stats {
 } dopf_layout_stats;
 int dopf_layout_probe(const dopf_model_view* model, int32_t max_blocks, int64_t smem_limit,
                       dopf_layout_stats* out);
+/* Same for a scenario batch (dopf_cuda_upload_batch's layout: one shared
+ * structure plan, <= 8 CTAs per scenario). */
+int dopf_layout_probe_batch(const dopf_model_view* models, int32_t count, int64_t smem_limit,
+                            dopf_layout_stats* out);
 
 #ifdef __cplusplus
 }

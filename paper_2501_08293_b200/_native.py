@@ -133,6 +133,7 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_set_profiling", C.c_int, vp, i32)
     _sig(lib, "dopf_cuda_phase_cycles", C.c_int, vp, P(i64), i32)
     _sig(lib, "dopf_layout_probe", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))
+    _sig(lib, "dopf_layout_probe_batch", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))
     _cuda = lib
     return lib
 

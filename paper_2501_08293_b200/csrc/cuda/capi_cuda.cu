@@ -3,6 +3,7 @@
 
 #include <chrono>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -43,7 +44,13 @@ struct dopf_cuda_ctx {
   int num_blocks = 0;
   std::vector<int32_t> inst_nz, inst_n;
 
-  std::vector<void*> allocs;  // model-lifetime device buffers
+  // Device buffers grow only: a re-upload of a model of the same (or
+  // smaller) size reuses them -- no cudaFree/cudaMalloc on the e2e path.
+  struct Buf {
+    void* p = nullptr;
+    std::size_t cap = 0;  // bytes
+  };
+  std::vector<Buf> bufs = std::vector<Buf>(32);
   BlockDesc* d_blocks = nullptr;
   InstDesc* d_inst = nullptr;
   double *d_P = nullptr, *d_A = nullptr, *d_v = nullptr, *d_z0 = nullptr;
@@ -61,6 +68,11 @@ struct dopf_cuda_ctx {
   double *d_maxinf = nullptr, *d_obj = nullptr;
   double* d_trace = nullptr;
   std::size_t trace_cap = 0;  // doubles
+  // cached layout plans (structure only), reused while the structure repeats
+  std::shared_ptr<InstancePlan> plan, batch_plan;
+  // pinned staging for results copied back to the host
+  void* h_stage = nullptr;
+  std::size_t h_stage_cap = 0;
 
   int64_t launches = 0;
   double last_kernel_s = 0;
@@ -69,30 +81,50 @@ struct dopf_cuda_ctx {
   std::size_t prof_cap = 0;
 
   void free_model() {
-    for (void* p : allocs) cudaFree(p);
-    allocs.clear();
+    for (Buf& b : bufs) {
+      if (b.p) cudaFree(b.p);
+      b = Buf{};
+    }
     if (d_trace) cudaFree(d_trace);
     d_trace = nullptr;
     trace_cap = 0;
     uploaded = false;
   }
 
-  template <typename T>
-  T* put(const std::vector<T>& h) {
-    void* p = nullptr;
-    const std::size_t bytes = std::max<std::size_t>(sizeof(T), h.size() * sizeof(T));
-    ck(cudaMalloc(&p, bytes), "cudaMalloc");
-    allocs.push_back(p);
-    if (!h.empty()) ck(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, stream), "upload");
-    return static_cast<T*>(p);
+  void* ensure(int slot, std::size_t bytes) {
+    Buf& b = bufs.at(slot);
+    bytes = std::max<std::size_t>(bytes, 16);
+    if (b.cap < bytes) {
+      if (b.p) cudaFree(b.p);
+      b.p = nullptr;
+      b.cap = 0;
+      ck(cudaMalloc(&b.p, bytes), "cudaMalloc");
+      b.cap = bytes;
+    }
+    return b.p;
   }
 
   template <typename T>
-  T* scratch(std::size_t count) {
-    void* p = nullptr;
-    ck(cudaMalloc(&p, std::max<std::size_t>(1, count) * sizeof(T)), "cudaMalloc");
-    allocs.push_back(p);
-    return static_cast<T*>(p);
+  T* put(int slot, const std::vector<T>& h) {
+    T* p = static_cast<T*>(ensure(slot, h.size() * sizeof(T)));
+    if (!h.empty()) ck(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, stream), "upload");
+    return p;
+  }
+
+  template <typename T>
+  T* scratch(int slot, std::size_t count) {
+    return static_cast<T*>(ensure(slot, count * sizeof(T)));
+  }
+
+  void* stage(std::size_t bytes) {
+    if (h_stage_cap < bytes) {
+      if (h_stage) cudaFreeHost(h_stage);
+      h_stage = nullptr;
+      h_stage_cap = 0;
+      ck(cudaMallocHost(&h_stage, bytes), "cudaMallocHost");
+      h_stage_cap = bytes;
+    }
+    return h_stage;
   }
 };
 
@@ -129,34 +161,36 @@ void check_settings(const dopf_settings* s) {
 
 void upload_layout(dopf_cuda_ctx* c) {
   HostLayout& L = c->L;
-  c->d_blocks = c->put(L.blocks);
-  c->d_inst = c->put(L.inst);
-  c->d_P = c->put(L.P);
-  c->d_A = c->put(L.A);
-  c->d_copies = c->put(L.copies);
-  c->d_rmeta = c->put(L.rmeta);
-  c->d_v = c->put(L.v);
-  c->d_z0 = c->put(L.z0);
-  c->d_cmeta = c->put(L.cmeta);
-  c->d_cc = c->put(L.cc);
-  c->d_cinv = c->put(L.cinv);
-  c->d_clo = c->put(L.clo);
-  c->d_chi = c->put(L.chi);
-  c->d_ameta = c->put(L.ameta);
-  c->d_ab = c->put(L.ab);
-  c->d_nbrs = c->put(L.nbrs);
+  int k = 0;
+  c->d_blocks = c->put(k++, L.blocks);
+  c->d_inst = c->put(k++, L.inst);
+  c->d_P = c->put(k++, L.P);
+  c->d_A = c->put(k++, L.A);
+  c->d_copies = c->put(k++, L.copies);
+  c->d_rmeta = c->put(k++, L.rmeta);
+  c->d_v = c->put(k++, L.v);
+  c->d_z0 = c->put(k++, L.z0);
+  c->d_cmeta = c->put(k++, L.cmeta);
+  c->d_cc = c->put(k++, L.cc);
+  c->d_cinv = c->put(k++, L.cinv);
+  c->d_clo = c->put(k++, L.clo);
+  c->d_chi = c->put(k++, L.chi);
+  c->d_ameta = c->put(k++, L.ameta);
+  c->d_ab = c->put(k++, L.ab);
+  c->d_nbrs = c->put(k++, L.nbrs);
   const std::size_t I = L.inst.size();
-  c->d_u = c->scratch<double>(4 * static_cast<std::size_t>(L.rows_total));  // tagged records
-  c->d_z = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));    // [t % 3][row]
-  c->d_lam = c->scratch<double>(3 * static_cast<std::size_t>(L.rows_total));
-  c->d_x = c->scratch<double>(L.x_total);
-  c->d_part = c->scratch<double>(I * kSlotRing * L.blocks_per_instance * kPartials);
-  c->d_flags = c->scratch<unsigned long long>(I * L.blocks_per_instance * 16);
-  c->d_ctl = c->scratch<unsigned long long>(I * kCtlWords);
-  c->d_iters = c->scratch<int32_t>(I);
-  c->d_status = c->scratch<int32_t>(I);
-  c->d_maxinf = c->scratch<double>(I);
-  c->d_obj = c->scratch<double>(I);
+  const std::size_t R = static_cast<std::size_t>(L.rows_total);
+  c->d_u = c->scratch<double>(k++, 4 * R);    // tagged records {t, u}, two buffers
+  c->d_z = c->scratch<double>(k++, 3 * R);    // [t % 3][row]
+  c->d_lam = c->scratch<double>(k++, 3 * R);
+  c->d_x = c->scratch<double>(k++, L.x_total);
+  c->d_part = c->scratch<double>(k++, I * kSlotRing * L.blocks_per_instance * kPartials);
+  c->d_flags = c->scratch<unsigned long long>(k++, I * L.blocks_per_instance * 16);
+  c->d_ctl = c->scratch<unsigned long long>(k++, I * kCtlWords);
+  c->d_iters = c->scratch<int32_t>(k++, I);
+  c->d_status = c->scratch<int32_t>(k++, I);
+  c->d_maxinf = c->scratch<double>(k++, I);
+  c->d_obj = c->scratch<double>(k++, I);
   ck(cudaStreamSynchronize(c->stream), "upload sync");
 }
 
@@ -291,18 +325,25 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   ck(cudaMemcpy(status.data(), c->d_status, I * sizeof(int32_t), cudaMemcpyDeviceToHost), "d2h");
   ck(cudaMemcpy(maxinf.data(), c->d_maxinf, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
   ck(cudaMemcpy(obj.data(), c->d_obj, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
-  std::vector<double> zdev, ldev, xall;
   bool any_vec = false;
   for (int i = 0; i < count; ++i)
     any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
+  // results: a single instance needs only ring buffer iters % 3; a batch
+  // copies all three (instances stop at different iterations)
+  const std::size_t R = static_cast<std::size_t>(L.rows_total);
+  const bool one = I == 1;
+  const std::size_t nbuf = one ? 1 : 3;
+  double *zdev = nullptr, *ldev = nullptr, *xall = nullptr;
   if (copy_vectors && any_vec) {
-    // all three result buffers: instance i's final iterate sits in buffer iters[i] % 3
-    zdev.resize(3 * static_cast<std::size_t>(L.rows_total));
-    ldev.resize(3 * static_cast<std::size_t>(L.rows_total));
-    xall.resize(L.x_total);
-    ck(cudaMemcpy(zdev.data(), c->d_z, zdev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
-    ck(cudaMemcpy(ldev.data(), c->d_lam, ldev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
-    ck(cudaMemcpy(xall.data(), c->d_x, xall.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    double* st = static_cast<double*>(c->stage((2 * nbuf * R + L.x_total) * sizeof(double)));
+    zdev = st;
+    ldev = st + nbuf * R;
+    xall = st + 2 * nbuf * R;
+    const std::size_t from = one ? (iters[0] % 3) * R : 0;
+    ck(cudaMemcpyAsync(zdev, c->d_z + from, nbuf * R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(ldev, c->d_lam + from, nbuf * R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(xall, c->d_x, L.x_total * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "d2h");
   }
   for (int i = 0; i < count; ++i) {
     dopf_result_view& r = results[i];
@@ -314,8 +355,8 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     r.time_solve = c->last_kernel_s;
     r.time_global = r.time_local = r.time_dual = 0.0;
     if (copy_vectors && any_vec) {
-      if (r.x) std::memcpy(r.x, xall.data() + id.x_off, sizeof(double) * id.n);
-      const std::size_t base = (iters[i] % 3) * static_cast<std::size_t>(L.rows_total);
+      if (r.x) std::memcpy(r.x, xall + id.x_off, sizeof(double) * id.n);
+      const std::size_t base = one ? 0 : (iters[i] % 3) * R;
       for (int32_t d = id.row0; d < id.row0 + id.rows; ++d) {
         const int32_t ref = L.ref_of_dev[d];
         if (r.z) r.z[ref] = zdev[base + d];
@@ -323,12 +364,16 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
       }
     }
     if (r.trace && iters[i] > 0)
-      ck(cudaMemcpy(r.trace, c->d_trace + static_cast<std::size_t>(i) * s->max_iter * 6,
-                    static_cast<std::size_t>(iters[i]) * 6 * sizeof(double), cudaMemcpyDeviceToHost),
+      ck(cudaMemcpyAsync(r.trace, c->d_trace + static_cast<std::size_t>(i) * s->max_iter * 6,
+                         static_cast<std::size_t>(iters[i]) * 6 * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream),
          "trace d2h");
-    r.time_download =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t_dn0).count();
-    r.time_upload = std::chrono::duration<double>(t_dn0 - t_up0).count() - c->last_kernel_s;
+  }
+  ck(cudaStreamSynchronize(c->stream), "trace d2h");
+  const double t_dn = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_dn0).count();
+  for (int i = 0; i < count; ++i) {
+    results[i].time_download = t_dn;
+    results[i].time_upload = std::chrono::duration<double>(t_dn0 - t_up0).count() - c->last_kernel_s;
   }
 }
 
@@ -368,11 +413,12 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
   if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    c->free_model();
-    c->L = HostLayout();
+    c->uploaded = false;
+    c->L.reset();
     const LayoutOptions opt = options_for(c);
-    const int G = choose_blocks(*m, opt);
-    add_instance(c->L, *m, G, opt);
+    if (!c->plan || !c->plan->same_structure(*m, opt))
+      c->plan = std::make_shared<InstancePlan>(plan_instance(*m, choose_blocks(*m, opt), opt));
+    append_instance(c->L, *c->plan, *m);
     c->inst_nz = {m->N_z};
     c->inst_n = {m->n};
     finish_upload(c);
@@ -383,21 +429,20 @@ int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t 
   if (!c || !ms || count < 1) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    c->free_model();
-    c->L = HostLayout();
+    c->uploaded = false;
     LayoutOptions opt = options_for(c);
     opt.max_blocks = 8;  // one cluster per scenario
-    const int G = choose_blocks(ms[0], opt);
+    if (!c->batch_plan || !c->batch_plan->same_structure(ms[0], opt))
+      c->batch_plan = std::make_shared<InstancePlan>(plan_instance(ms[0], choose_blocks(ms[0], opt), opt));
     c->inst_nz.clear();
     c->inst_n.clear();
     for (int i = 0; i < count; ++i) {
-      add_instance(c->L, ms[i], G, opt);
+      if (!c->batch_plan->same_structure(ms[i], opt))
+        throw std::invalid_argument("batched scenarios must share the subsystem structure");
       c->inst_nz.push_back(ms[i].N_z);
       c->inst_n.push_back(ms[i].n);
     }
-    for (const auto& id : c->L.inst)
-      if (id.blocks != c->L.blocks_per_instance)
-        throw std::invalid_argument("batched scenarios must share the subsystem structure");
+    build_batch(c->L, *c->batch_plan, ms, count);
     finish_upload(c);
   });
 }
@@ -424,6 +469,7 @@ void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   c->free_model();
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -473,6 +519,32 @@ int dopf_layout_probe(const dopf_model_view* m, int32_t max_blocks, int64_t smem
     return DOPF_OK;
   } catch (const std::invalid_argument&) {
     return DOPF_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return DOPF_ERR_RUNTIME;
+  }
+}
+
+int dopf_layout_probe_batch(const dopf_model_view* ms, int32_t count, int64_t smem_limit,
+                            dopf_layout_stats* out) {
+  if (!ms || count < 1 || !out) return DOPF_ERR_INVALID_ARGUMENT;
+  try {
+    LayoutOptions opt;
+    opt.smem_limit = static_cast<std::size_t>(smem_limit);
+    opt.max_blocks = 8;
+    const InstancePlan plan = plan_instance(ms[0], choose_blocks(ms[0], opt), opt);
+    for (int i = 0; i < count; ++i)
+      if (!plan.same_structure(ms[i], opt)) return DOPF_ERR_INVALID_ARGUMENT;
+    HostLayout L;
+    build_batch(L, plan, ms, count);
+    out->blocks = L.blocks_per_instance;
+    out->rows_per_thread = L.K;
+    out->resident = L.all_ops_in_smem ? 1 : 0;
+    out->max_neighbours = L.max_neighbours;
+    out->smem_bytes = static_cast<int64_t>(L.smem_bytes);
+    out->remote_copies = out->local_copies = out->exported_rows = 0;
+    for (int32_t c : L.copies) (c < 0 ? out->remote_copies : out->local_copies) += 1;
+    out->bytes_per_iteration = L.bytes_per_iteration;
+    return DOPF_OK;
   } catch (const std::exception&) {
     return DOPF_ERR_RUNTIME;
   }

@@ -1,6 +1,8 @@
 #include "layout_builder.hpp"
 
 #include <algorithm>
+#include <cstring>
+#include <thread>
 #include <numeric>
 #include <stdexcept>
 
@@ -123,51 +125,57 @@ int choose_blocks(const dopf_model_view& m, const LayoutOptions& opt) {
   g0 = std::max(g0, (m.N_z + rows_cap - 1) / rows_cap);
   g0 = std::max(1, std::min(g0, std::max(1, m.S)));
   for (int G = g0; G <= 8 && G <= m.S; ++G) {
-    HostLayout trial;
-    add_instance(trial, m, G, opt);
+    const InstancePlan trial = plan_instance(m, G, opt);
     if (trial.all_ops_in_smem && trial.K <= 2) return G;
   }
   return std::min(opt.max_blocks, std::max(1, m.S));
 }
 
-void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOptions& opt) {
+bool InstancePlan::same_structure(const dopf_model_view& m, const LayoutOptions& o) const {
+  auto eq = [](const std::vector<int32_t>& v, const int32_t* p, std::size_t n) {
+    return v.size() == n && (n == 0 || std::memcmp(v.data(), p, n * sizeof(int32_t)) == 0);
+  };
+  return m.has_pre && S == m.S && n == m.n && Nz == m.N_z && o.smem_limit == opt.smem_limit &&
+         o.max_blocks == opt.max_blocks && o.threads == opt.threads &&
+         o.blocks_per_instance == opt.blocks_per_instance && eq(z_offsets, m.z_offsets, m.S + 1) &&
+         eq(m_s, m.m_s, m.S) && eq(l2g, m.l2g, m.N_z) && eq(csr_ptr, m.csr_ptr, m.n + 1) &&
+         eq(csr_copy, m.csr_copy, m.N_z);
+}
+
+InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions& opt) {
   if (!m.has_pre) throw std::invalid_argument("model view lacks precomputed operators");
-  const int instance = static_cast<int>(L.inst.size());
+  InstancePlan P;
+  P.S = m.S;
+  P.n = m.n;
+  P.Nz = m.N_z;
+  P.G = G;
+  P.opt = opt;
+  P.z_offsets.assign(m.z_offsets, m.z_offsets + m.S + 1);
+  P.m_s.assign(m.m_s, m.m_s + m.S);
+  P.l2g.assign(m.l2g, m.l2g + m.N_z);
+  P.csr_ptr.assign(m.csr_ptr, m.csr_ptr + m.n + 1);
+  P.csr_copy.assign(m.csr_copy, m.csr_copy + m.N_z);
+
   const std::vector<std::vector<int>> parts =
       split_blocks(m, locality_order(m), std::max(1, std::min(G, std::max(1, m.S))));
   const int nb = static_cast<int>(parts.size());
-  const int32_t inst_row0 = static_cast<int32_t>(L.rows_total);
-  const int32_t block0 = static_cast<int32_t>(L.blocks.size());
-
-  InstDesc id{};
-  id.x_off = L.x_total;
-  id.n = m.n;
-  id.blocks = std::max(nb, 1);
-  id.block0 = block0;
-  id.rows = m.N_z;
-  id.row0 = inst_row0;
-  L.inst.push_back(id);
-  L.x_total += m.n;
+  const int cw = opt.threads - 32;
 
   // Pass 1: device rows (subsystems by n_s descending inside each block).
   std::vector<int32_t> dev_of_ref(m.N_z, -1);
   std::vector<std::vector<int>> order(nb);
-  int32_t next_row = inst_row0;
+  int32_t next_row = 0;
   std::vector<int32_t> block_row0(nb);
   for (int g = 0; g < nb; ++g) {
     auto& ord = order[g];
     ord = parts[g];
-    std::stable_sort(ord.begin(), ord.end(),
-                     [&](int a, int b) { return ns_of(m, a) > ns_of(m, b); });
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return ns_of(m, a) > ns_of(m, b); });
     block_row0[g] = next_row;
     for (int s : ord)
       for (int i = 0; i < ns_of(m, s); ++i) dev_of_ref[m.z_offsets[s] + i] = next_row++;
   }
-  L.rows_total = next_row;
-  L.rmeta.resize(next_row);
-  L.v.resize(next_row);
-  L.z0.resize(next_row);
-  L.ref_of_dev.resize(next_row);
+  P.rmeta.resize(next_row);
+  P.ref_of_dev.resize(next_row);
 
   // owner block of each column = block holding its first (lowest-s) copy
   std::vector<int> block_of_s(m.S, 0);
@@ -178,33 +186,32 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) s_of_ref[k] = s;
 
   std::vector<int> xloc_of(m.n, -1);
-  std::vector<char> exported(next_row - inst_row0, 0);
+  std::vector<char> exported(next_row, 0);
   std::vector<int> nbrs;
+  std::size_t p_len_total = 0, a_len_total = 0;
   for (int g = 0; g < nb; ++g) {
     BlockDesc bd{};
     bd.row0 = block_row0[g];
-    bd.instance = instance;
     bd.inst_block = g;
-    bd.p_off = static_cast<int64_t>(L.P.size());
-    bd.a_off = static_cast<int64_t>(L.A.size());
-    bd.copy_off = static_cast<int32_t>(L.copies.size());
-    bd.col_off = static_cast<int32_t>(L.cmeta.size());
-    bd.amet_off = static_cast<int32_t>(L.ameta.size());
+    bd.p_off = static_cast<int64_t>(p_len_total);
+    bd.a_off = static_cast<int64_t>(a_len_total);
+    bd.copy_off = static_cast<int32_t>(P.copies.size());
+    bd.col_off = static_cast<int32_t>(P.cmeta.size());
+    bd.amet_off = static_cast<int32_t>(P.ameta.size());
 
-    // columns referenced by this block, ascending
+    // columns referenced by this block, ascending; interior columns (every
+    // copy in this block) first, boundary columns last
     std::vector<int> cols;
     for (int s : order[g])
       for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) cols.push_back(m.l2g[k]);
     std::sort(cols.begin(), cols.end());
     cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
-    // interior columns (every copy in this block) first, boundary columns last
     auto is_boundary = [&](int c) {
       for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q)
         if (block_of_s[s_of_ref[m.csr_copy[q]]] != g) return true;
       return false;
     };
-    const auto mid = std::stable_partition(cols.begin(), cols.end(),
-                                           [&](int c) { return !is_boundary(c); });
+    const auto mid = std::stable_partition(cols.begin(), cols.end(), [&](int c) { return !is_boundary(c); });
     bd.cols_int = static_cast<int32_t>(mid - cols.begin());
     for (std::size_t q = 0; q < cols.size(); ++q) xloc_of[cols[q]] = static_cast<int>(q);
 
@@ -213,33 +220,27 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
     // stored interleaved: entry j of the slice's lane l at slice_off + 32 j + l
     // (sliced ELL). Every shared-memory read of a warp is then 256 contiguous
     // bytes -- conflict-free -- and the kernel's row offsets are immediates.
-    const int cw = opt.threads - 32;
-    struct RowSrc { const double* src; int n; };  // operator row (contiguous, n entries)
+    struct RowSrc { int64_t src; int n; };  // operator row: offset into m.P / m.A, n entries
     std::vector<RowSrc> prow, arow;
     int32_t local = 0;
     for (int s : order[g]) {
       const int n = ns_of(m, s), ms = m.m_s[s];
       const int base = local;
-      const double* Ps = m.P + m.p_offsets[s];  // row-major n x n
-      const double* As = m.A + m.a_offsets[s];  // row-major ms x n
       for (int i = 0; i < n; ++i) {
         const int ref = m.z_offsets[s] + i;
         const int32_t dev = bd.row0 + local;
-        L.rmeta[dev] = RowMeta{0, static_cast<int16_t>(n), 0, base, xloc_of[m.l2g[ref]]};
-        L.v[dev] = m.v[ref];
-        L.z0[dev] = m.z0[ref];
-        L.ref_of_dev[dev] = ref;
-        prow.push_back(RowSrc{Ps + static_cast<std::size_t>(i) * n, n});
+        P.rmeta[dev] = RowMeta{0, static_cast<int16_t>(n), 0, base, xloc_of[m.l2g[ref]]};
+        P.ref_of_dev[dev] = ref;
+        prow.push_back(RowSrc{m.p_offsets[s] + static_cast<int64_t>(i) * n, n});
         ++local;
       }
       for (int r = 0; r < ms; ++r) {
-        L.ameta.push_back(AMeta{0, ms, n, base});
-        L.ab.push_back(m.b[m.b_offsets[s] + r]);
-        arow.push_back(RowSrc{As + static_cast<std::size_t>(r) * n, n});
+        P.ameta.push_back(AMeta{0, ms, n, base});
+        P.ab_src.push_back(m.b_offsets[s] + r);
+        arow.push_back(RowSrc{m.a_offsets[s] + static_cast<int64_t>(r) * n, n});
       }
     }
-    // pack rows into slices; returns the doubles appended; offs[r] = slice_off + lane
-    auto pack = [&](const std::vector<RowSrc>& rows, std::vector<double>& out, auto&& set_off) {
+    auto pack = [&](const std::vector<RowSrc>& rows, std::vector<int64_t>& out, auto&& set_off) {
       const int count = static_cast<int>(rows.size());
       int32_t len = 0;
       for (int k0 = 0; k0 < count; k0 += cw) {
@@ -250,72 +251,298 @@ void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOp
           for (int l = 0; l < lanes; ++l) set_off(w0 + l, len + l);
           for (int j = 0; j < width; ++j)
             for (int l = 0; l < 32; ++l)
-              out.push_back(l < lanes && j < rows[w0 + l].n ? rows[w0 + l].src[j] : 0.0);
+              out.push_back(l < lanes && j < rows[w0 + l].n ? rows[w0 + l].src + j : -1);
           len += 32 * width;
         }
       }
       return len;
     };
-    bd.p_len = pack(prow, L.P, [&](int r, int32_t o) { L.rmeta[bd.row0 + r].pofs = o; });
-    bd.a_len = pack(arow, L.A, [&](int a, int32_t o) { L.ameta[bd.amet_off + a].aofs = o; });
+    bd.p_len = pack(prow, P.p_src, [&](int r, int32_t o) { P.rmeta[bd.row0 + r].pofs = o; });
+    bd.a_len = pack(arow, P.a_src, [&](int a, int32_t o) { P.ameta[bd.amet_off + a].aofs = o; });
+    p_len_total += bd.p_len;
+    a_len_total += bd.a_len;
     bd.rows = local;
-    bd.arows = static_cast<int32_t>(L.ameta.size()) - bd.amet_off;
+    bd.arows = static_cast<int32_t>(P.ameta.size()) - bd.amet_off;
     bd.cols = static_cast<int32_t>(cols.size());
     for (int c : cols) {
       ColMeta cm{};
       cm.gcol = c;
-      cm.copy_start = static_cast<int32_t>(L.copies.size()) - bd.copy_off;
+      cm.copy_start = static_cast<int32_t>(P.copies.size()) - bd.copy_off;
       cm.copy_count = m.csr_ptr[c + 1] - m.csr_ptr[c];
       for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q) {
         const int32_t dev = dev_of_ref[m.csr_copy[q]];
         const int g2 = block_of_s[s_of_ref[m.csr_copy[q]]];
         if (g2 == g) {
-          L.copies.push_back(dev - bd.row0);  // block-local: u from shared memory
+          P.copies.push_back(dev - bd.row0);  // block-local: u from shared memory
         } else {
-          L.copies.push_back(encode_remote(dev));
-          exported[dev - inst_row0] = 1;
+          P.copies.push_back(encode_remote(dev));  // instance-relative; rebased on append
+          exported[dev] = 1;
           nbrs.push_back(g2);
         }
       }
       cm.owner = block_of_s[s_of_ref[m.csr_copy[m.csr_ptr[c]]]] == g ? 1 : 0;
-      L.cmeta.push_back(cm);
-      L.cc.push_back(m.c[c]);
-      L.cinv.push_back(m.inv_copy[c]);
-      L.clo.push_back(m.x_lo[c]);
-      L.chi.push_back(m.x_hi[c]);
+      P.cmeta.push_back(cm);
     }
-    bd.copy_len = static_cast<int32_t>(L.copies.size()) - bd.copy_off;
+    bd.copy_len = static_cast<int32_t>(P.copies.size()) - bd.copy_off;
     for (int c : cols) xloc_of[c] = -1;
     std::sort(nbrs.begin(), nbrs.end());
     nbrs.erase(std::unique(nbrs.begin(), nbrs.end()), nbrs.end());
-    bd.nbr_off = static_cast<int32_t>(L.nbrs.size());
+    bd.nbr_off = static_cast<int32_t>(P.nbrs.size());
     bd.nbr_cnt = static_cast<int32_t>(nbrs.size());
-    L.nbrs.insert(L.nbrs.end(), nbrs.begin(), nbrs.end());
-    L.max_neighbours = std::max(L.max_neighbours, bd.nbr_cnt);
+    P.nbrs.insert(P.nbrs.end(), nbrs.begin(), nbrs.end());
+    P.max_neighbours = std::max(P.max_neighbours, bd.nbr_cnt);
     nbrs.clear();
 
     // the kernel packs per-thread metadata into bit fields (admm_kernels.cu)
     if (bd.rows >= 4096 || bd.cols >= 4096 || bd.copy_len >= (1 << 23))
       throw std::invalid_argument("block too large for the resident kernel");
-    if (bd.cols - bd.cols_int > opt.threads - 32)
+    if (bd.cols - bd.cols_int > cw)
       throw std::invalid_argument("block has more boundary columns than compute threads");
     for (int s : order[g])
       if (ns_of(m, s) >= 128) throw std::invalid_argument("subsystem with n_s >= 128 columns");
     for (int c : cols)
-      if (m.csr_ptr[c + 1] - m.csr_ptr[c] >= 256)
-        throw std::invalid_argument("column with 256 or more copies");
+      if (m.csr_ptr[c + 1] - m.csr_ptr[c] >= 256) throw std::invalid_argument("column with 256 or more copies");
     bd.ops_in_smem = block_smem_bytes(bd, true) <= opt.smem_limit ? 1 : 0;
-    if (!bd.ops_in_smem) L.all_ops_in_smem = false;
-    L.smem_bytes = std::max(L.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
-    // warps 1.. (opt.threads - 32 threads) own rows, columns and equality rows
-    const int k_need = (std::max(bd.rows, std::max(bd.cols, bd.arows)) + cw - 1) / cw;
-    L.K = std::max(L.K, std::max(1, k_need));
+    if (!bd.ops_in_smem) P.all_ops_in_smem = false;
+    P.smem_bytes = std::max(P.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
+    // warps 1.. (cw threads) own rows, interior columns and equality rows
+    const int k_need = (std::max(bd.rows, std::max(bd.cols_int, bd.arows)) + cw - 1) / cw;
+    P.K = std::max(P.K, std::max(1, k_need));
+    P.blocks.push_back(bd);
+  }
+  for (int32_t d = 0; d < next_row; ++d) P.rmeta[d].exported = exported[d];
+  P.bytes_per_iteration = algorithmic_bytes(m);
+  P.flops_per_iteration = algorithmic_flops(m);
+  return P;
+}
+
+namespace {
+
+// out[i] = src[idx[i]] (0 for idx < 0), split over threads for large arrays
+void gather(std::vector<double>& out, std::size_t at, const std::vector<int64_t>& idx, const double* src) {
+  const std::size_t n = idx.size();
+  auto body = [&](std::size_t b, std::size_t e) {
+    for (std::size_t i = b; i < e; ++i) out[at + i] = idx[i] >= 0 ? src[idx[i]] : 0.0;
+  };
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (n < (1u << 18) || hw == 1) {
+    body(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < hw; ++t) th.emplace_back(body, n * t / hw, n * (t + 1) / hw);
+  for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+void append_instance(HostLayout& L, const InstancePlan& P, const dopf_model_view& m) {
+  const int instance = static_cast<int>(L.inst.size());
+  const int32_t row_base = static_cast<int32_t>(L.rows_total);
+  const int64_t p_base = static_cast<int64_t>(L.P.size()), a_base = static_cast<int64_t>(L.A.size());
+  const int32_t copy_base = static_cast<int32_t>(L.copies.size());
+  const int32_t col_base = static_cast<int32_t>(L.cmeta.size());
+  const int32_t amet_base = static_cast<int32_t>(L.ameta.size());
+  const int32_t nbr_base = static_cast<int32_t>(L.nbrs.size());
+
+  InstDesc id{};
+  id.x_off = L.x_total;
+  id.n = P.n;
+  id.blocks = static_cast<int32_t>(P.blocks.size());
+  id.block0 = static_cast<int32_t>(L.blocks.size());
+  id.rows = P.Nz;
+  id.row0 = row_base;
+  L.inst.push_back(id);
+  L.x_total += P.n;
+
+  for (BlockDesc bd : P.blocks) {
+    bd.row0 += row_base;
+    bd.p_off += p_base;
+    bd.a_off += a_base;
+    bd.copy_off += copy_base;
+    bd.col_off += col_base;
+    bd.amet_off += amet_base;
+    bd.nbr_off += nbr_base;
+    bd.instance = instance;
     L.blocks.push_back(bd);
   }
-  for (int32_t d = inst_row0; d < next_row; ++d) L.rmeta[d].exported = exported[d - inst_row0];
-  L.blocks_per_instance = std::max(L.blocks_per_instance, nb);
-  L.bytes_per_iteration += algorithmic_bytes(m);
-  L.flops_per_iteration += algorithmic_flops(m);
+  const std::size_t rows = P.rmeta.size();
+  L.rmeta.insert(L.rmeta.end(), P.rmeta.begin(), P.rmeta.end());
+  L.ref_of_dev.insert(L.ref_of_dev.end(), P.ref_of_dev.begin(), P.ref_of_dev.end());
+  L.v.resize(row_base + rows);
+  L.z0.resize(row_base + rows);
+  for (std::size_t d = 0; d < rows; ++d) {
+    L.v[row_base + d] = m.v[P.ref_of_dev[d]];
+    L.z0[row_base + d] = m.z0[P.ref_of_dev[d]];
+  }
+  L.rows_total += static_cast<int64_t>(rows);
+  for (int32_t c : P.copies) L.copies.push_back(c >= 0 ? c : encode_remote(decode_remote(c) + row_base));
+  L.cmeta.insert(L.cmeta.end(), P.cmeta.begin(), P.cmeta.end());
+  for (const ColMeta& cm : P.cmeta) {
+    L.cc.push_back(m.c[cm.gcol]);
+    L.cinv.push_back(m.inv_copy[cm.gcol]);
+    L.clo.push_back(m.x_lo[cm.gcol]);
+    L.chi.push_back(m.x_hi[cm.gcol]);
+  }
+  L.ameta.insert(L.ameta.end(), P.ameta.begin(), P.ameta.end());
+  for (int64_t k : P.ab_src) L.ab.push_back(m.b[k]);
+  L.nbrs.insert(L.nbrs.end(), P.nbrs.begin(), P.nbrs.end());
+  L.P.resize(p_base + P.p_src.size());
+  gather(L.P, p_base, P.p_src, m.P);
+  L.A.resize(a_base + P.a_src.size());
+  gather(L.A, a_base, P.a_src, m.A);
+
+  L.max_neighbours = std::max(L.max_neighbours, P.max_neighbours);
+  L.all_ops_in_smem = L.all_ops_in_smem && P.all_ops_in_smem;
+  L.smem_bytes = std::max(L.smem_bytes, P.smem_bytes);
+  L.K = std::max(L.K, P.K);
+  L.blocks_per_instance = std::max(L.blocks_per_instance, static_cast<int>(P.blocks.size()));
+  L.bytes_per_iteration += P.bytes_per_iteration;
+  L.flops_per_iteration += P.flops_per_iteration;
+}
+
+void HostLayout::reset() {
+  blocks.clear();
+  inst.clear();
+  P.clear();
+  A.clear();
+  copies.clear();
+  rmeta.clear();
+  v.clear();
+  z0.clear();
+  ref_of_dev.clear();
+  cmeta.clear();
+  cc.clear();
+  cinv.clear();
+  clo.clear();
+  chi.clear();
+  ameta.clear();
+  ab.clear();
+  nbrs.clear();
+  max_neighbours = 0;
+  rows_total = 0;
+  x_total = 0;
+  trace_rows_per_instance = 0;
+  K = 1;
+  smem_bytes = 0;
+  blocks_per_instance = 1;
+  all_ops_in_smem = true;
+  bytes_per_iteration = 0;
+  flops_per_iteration = 0;
+}
+
+void build_batch(HostLayout& L, const InstancePlan& P, const dopf_model_view* ms, int count) {
+  // every instance has the plan's sizes, so instance i's slices sit at i x size:
+  // size once, then fill the instances in parallel
+  L.reset();
+  const std::size_t I = static_cast<std::size_t>(count);
+  const std::size_t nb = P.blocks.size(), rows = P.rmeta.size(), ncp = P.copies.size();
+  const std::size_t ncol = P.cmeta.size(), nam = P.ameta.size(), nnb = P.nbrs.size();
+  const std::size_t np = P.p_src.size(), na = P.a_src.size();
+  L.blocks.resize(I * nb);
+  L.inst.resize(I);
+  L.rmeta.resize(I * rows);
+  L.ref_of_dev.resize(I * rows);
+  L.v.resize(I * rows);
+  L.z0.resize(I * rows);
+  L.copies.resize(I * ncp);
+  L.cmeta.resize(I * ncol);
+  for (auto* vec : {&L.cc, &L.cinv, &L.clo, &L.chi}) vec->resize(I * ncol);
+  L.ameta.resize(I * nam);
+  L.ab.resize(I * nam);
+  L.nbrs.resize(I * nnb);
+  L.P.resize(I * np);
+  L.A.resize(I * na);
+  auto fill = [&](std::size_t i0, std::size_t i1) {
+    for (std::size_t i = i0; i < i1; ++i) {
+      const dopf_model_view& m = ms[i];
+      const int32_t row_base = static_cast<int32_t>(i * rows);
+      InstDesc id{};
+      id.x_off = static_cast<int64_t>(i) * P.n;
+      id.n = P.n;
+      id.blocks = static_cast<int32_t>(nb);
+      id.block0 = static_cast<int32_t>(i * nb);
+      id.rows = P.Nz;
+      id.row0 = row_base;
+      L.inst[i] = id;
+      for (std::size_t b = 0; b < nb; ++b) {
+        BlockDesc bd = P.blocks[b];
+        bd.row0 += row_base;
+        bd.p_off += static_cast<int64_t>(i * np);
+        bd.a_off += static_cast<int64_t>(i * na);
+        bd.copy_off += static_cast<int32_t>(i * ncp);
+        bd.col_off += static_cast<int32_t>(i * ncol);
+        bd.amet_off += static_cast<int32_t>(i * nam);
+        bd.nbr_off += static_cast<int32_t>(i * nnb);
+        bd.instance = static_cast<int32_t>(i);
+        L.blocks[i * nb + b] = bd;
+      }
+      for (std::size_t d = 0; d < rows; ++d) {
+        L.rmeta[i * rows + d] = P.rmeta[d];
+        L.ref_of_dev[i * rows + d] = P.ref_of_dev[d];
+        L.v[i * rows + d] = m.v[P.ref_of_dev[d]];
+        L.z0[i * rows + d] = m.z0[P.ref_of_dev[d]];
+      }
+      for (std::size_t k = 0; k < ncp; ++k) {
+        const int32_t c = P.copies[k];
+        L.copies[i * ncp + k] = c >= 0 ? c : encode_remote(decode_remote(c) + row_base);
+      }
+      for (std::size_t k = 0; k < ncol; ++k) {
+        const int g = P.cmeta[k].gcol;
+        L.cmeta[i * ncol + k] = P.cmeta[k];
+        L.cc[i * ncol + k] = m.c[g];
+        L.cinv[i * ncol + k] = m.inv_copy[g];
+        L.clo[i * ncol + k] = m.x_lo[g];
+        L.chi[i * ncol + k] = m.x_hi[g];
+      }
+      for (std::size_t k = 0; k < nam; ++k) {
+        L.ameta[i * nam + k] = P.ameta[k];
+        L.ab[i * nam + k] = m.b[P.ab_src[k]];
+      }
+      for (std::size_t k = 0; k < nnb; ++k) L.nbrs[i * nnb + k] = P.nbrs[k];
+      for (std::size_t k = 0; k < np; ++k) L.P[i * np + k] = P.p_src[k] >= 0 ? m.P[P.p_src[k]] : 0.0;
+      for (std::size_t k = 0; k < na; ++k) L.A[i * na + k] = P.a_src[k] >= 0 ? m.A[P.a_src[k]] : 0.0;
+    }
+  };
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = static_cast<unsigned>(std::min<std::size_t>(hw, (I + 7) / 8));
+  if (nt <= 1) {
+    fill(0, I);
+  } else {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) th.emplace_back(fill, I * t / nt, I * (t + 1) / nt);
+    for (auto& t : th) t.join();
+  }
+  L.rows_total = static_cast<int64_t>(I * rows);
+  L.x_total = static_cast<int64_t>(I) * P.n;
+  L.max_neighbours = P.max_neighbours;
+  L.all_ops_in_smem = P.all_ops_in_smem;
+  L.smem_bytes = P.smem_bytes;
+  L.K = P.K;
+  L.blocks_per_instance = static_cast<int>(nb);
+  L.bytes_per_iteration = P.bytes_per_iteration * count;
+  L.flops_per_iteration = P.flops_per_iteration * count;
+}
+
+void reserve_instances(HostLayout& L, const InstancePlan& P, std::size_t count) {
+  L.blocks.reserve(L.blocks.size() + count * P.blocks.size());
+  L.inst.reserve(L.inst.size() + count);
+  L.rmeta.reserve(L.rmeta.size() + count * P.rmeta.size());
+  L.ref_of_dev.reserve(L.ref_of_dev.size() + count * P.ref_of_dev.size());
+  L.v.reserve(L.v.size() + count * P.rmeta.size());
+  L.z0.reserve(L.z0.size() + count * P.rmeta.size());
+  L.copies.reserve(L.copies.size() + count * P.copies.size());
+  L.cmeta.reserve(L.cmeta.size() + count * P.cmeta.size());
+  for (auto* v : {&L.cc, &L.cinv, &L.clo, &L.chi}) v->reserve(v->size() + count * P.cmeta.size());
+  L.ameta.reserve(L.ameta.size() + count * P.ameta.size());
+  L.ab.reserve(L.ab.size() + count * P.ab_src.size());
+  L.nbrs.reserve(L.nbrs.size() + count * P.nbrs.size());
+  L.P.reserve(L.P.size() + count * P.p_src.size());
+  L.A.reserve(L.A.size() + count * P.a_src.size());
+}
+
+void add_instance(HostLayout& L, const dopf_model_view& m, int G, const LayoutOptions& opt) {
+  append_instance(L, plan_instance(m, G, opt), m);
 }
 
 }  // namespace dopf::cuda

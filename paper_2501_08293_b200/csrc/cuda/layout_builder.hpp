@@ -35,6 +35,8 @@ struct HostLayout {
   bool all_ops_in_smem = true;
   double bytes_per_iteration = 0;  // algorithmic (BASELINE.md formula), sum over instances
   double flops_per_iteration = 0;
+
+  void reset();  // empty, keeping capacity (re-uploads reuse the host memory)
 };
 
 struct LayoutOptions {
@@ -43,6 +45,38 @@ struct LayoutOptions {
   int max_blocks = 148;               // co-resident CTA budget (1 per SM)
   int threads = kThreads;
 };
+
+/// Index structure of one instance's device layout (instance-relative
+/// offsets) plus the gather maps that fill its numeric arrays. Depends only on
+/// the model's sparsity structure, so it is reused across uploads of models
+/// with the same structure (re-solves with new data, scenario batches).
+struct InstancePlan {
+  int S = 0, n = 0, Nz = 0, G = 0;
+  LayoutOptions opt;
+  std::vector<int32_t> z_offsets, m_s, l2g, csr_ptr, csr_copy;  // structure signature
+  std::vector<BlockDesc> blocks;
+  std::vector<RowMeta> rmeta;
+  std::vector<int32_t> ref_of_dev, copies, nbrs;
+  std::vector<ColMeta> cmeta;
+  std::vector<AMeta> ameta;
+  std::vector<int64_t> ab_src, p_src, a_src;  // indices into the view's b / P / A (-1: zero pad)
+  int K = 1;
+  int max_neighbours = 0;
+  std::size_t smem_bytes = 0;
+  bool all_ops_in_smem = true;
+  double bytes_per_iteration = 0, flops_per_iteration = 0;
+
+  bool same_structure(const dopf_model_view& m, const LayoutOptions& o) const;
+};
+
+InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions& opt);
+/// The whole layout of `count` instances sharing `plan`'s structure
+/// (scenario batches), filled in parallel.
+void build_batch(HostLayout& L, const InstancePlan& plan, const dopf_model_view* ms, int count);
+/// Reserves room for `count` more instances of this plan.
+void reserve_instances(HostLayout& L, const InstancePlan& plan, std::size_t count);
+/// Appends one instance: rebased index structure + values gathered from m.
+void append_instance(HostLayout& L, const InstancePlan& plan, const dopf_model_view& m);
 
 /// Picks the CTA count for one instance: enough CTAs that every block's
 /// operators fit in shared memory and rows fit kMaxK per thread.
