@@ -10,6 +10,9 @@ max_iter = 50000, the paper's settings):
   --config ieee123 / ieee13   single instances of the smaller shapes
   --config batch123  --scenarios K independent load scenarios of the
                      IEEE-123 shape (configs[4]), sharded over ranks
+  --config tiled     --tiles T copies of the IEEE-8500 shape tied to one root
+                     (configs[3], T = 64: ~0.76M nodes, 10.8M local variables),
+                     solved on the HBM-streaming path
 
 Line keys:
   value     ADMM iterations / second on the device: iterations of the K timed
@@ -56,7 +59,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="ieee8500", choices=sorted(SINGLE) + ["batch123"])
+    ap.add_argument("--config", default="ieee8500", choices=sorted(SINGLE) + ["batch123", "tiled"])
+    ap.add_argument("--tiles", type=int, default=64, help="tiled: IEEE-8500 copies")
     ap.add_argument("--shape", default=None, help="alias of --config for single instances")
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--scenarios", type=int, default=4096, help="batch123: total scenarios")
@@ -67,7 +71,7 @@ def parse_args():
     if args.shape:
         args.config = args.shape
     if args.seed is None:
-        args.seed = SINGLE.get(args.config, 123)
+        args.seed = SINGLE.get(args.config, 850064 if args.config == "tiled" else 123)
     return args
 
 
@@ -133,7 +137,10 @@ def build_models(args, rank, world, workers):
     if args.config == "batch123":
         b, e = scenarios.shard(args.scenarios, world, rank)
         return scenarios.build_scenarios("ieee123", args.seed, range(b, e), workers)
-    f = dopf.synthetic_feeder(args.config, args.seed)
+    if args.config == "tiled":
+        f = dopf.tiled_feeder("ieee8500", args.tiles, args.seed)
+    else:
+        f = dopf.synthetic_feeder(args.config, args.seed)
     if rank > 0:  # weak scaling: rank r solves load scenario r of the same feeder
         f = dopf.scale_loads(f, scenarios.scenario_seed(args.seed, rank))
     _, _, model = dopf.load_model(f, workers=workers)
@@ -142,8 +149,11 @@ def build_models(args, rank, world, workers):
 
 
 def metric_name(args):
-    return "admm_iterations_per_second_" + ("batch4096_ieee123" if args.config == "batch123"
-                                            else args.config)
+    if args.config == "batch123":
+        return "admm_iterations_per_second_batch4096_ieee123"
+    if args.config == "tiled":
+        return f"admm_iterations_per_second_ieee8500_tiled{args.tiles}"
+    return "admm_iterations_per_second_" + args.config
 
 
 def config_of(args, world):
@@ -152,6 +162,11 @@ def config_of(args, world):
              f"(seed {args.seed}, loads scaled U[0.5,1.5]), each solved to convergence "
              "(rho=100, eps_rel=1e-3, max_iter=50000); value = scenario-iterations/s")
         par = f"scenario-sharded over {world} rank(s)" if world > 1 else "single-gpu"
+    elif args.config == "tiled":
+        w = (f"{args.tiles} synthetic ieee8500 feeders (seed {args.seed}) tied by 3-phase tie lines "
+             "to one root bus, one instance, solve to convergence (rho=100, eps_rel=1e-3, "
+             "max_iter=50000), HBM-streaming CUDA-graph path")
+        par = "independent scenario per rank" if world > 1 else "single-gpu"
     else:
         w = (f"{args.config} synthetic feeder (seed {args.seed}), single instance per GPU, "
              "solve to convergence (rho=100, eps_rel=1e-3, max_iter=50000)")
@@ -314,6 +329,7 @@ def main():
         torch.cuda.synchronize()
 
     launches0 = solver.kernel_launches()
+    kernels0 = solver.kernels_executed()
     per_step = []
     with ClockSampler(device) as clocks:
         barrier()
@@ -323,6 +339,7 @@ def main():
             per_step.append(device_solve())
         barrier()
     launches = solver.kernel_launches() - launches0
+    kernels = solver.kernels_executed() - kernels0
     iters = [sum(p[0]) for p in per_step]
     ktime = [p[2] for p in per_step]
     tot_it, tot_t = sum(iters), sum(ktime)
@@ -404,14 +421,17 @@ def main():
             "e2e": {"value": e2e_value, "unit": "iter/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "time_to_converge_ms": 1e3 * e2e_t / args.steps},
-            "gpu_launches": int(launches),
+            "gpu_launches": int(kernels),
+            "graph_or_kernel_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_iteration": b_iter,
                          "note": "algorithmic bytes (DESIGN.md s4) x iterations / kernel time; "
                                  "operators are staged in shared memory once per launch, so "
                                  "DRAM traffic is far below the algorithmic bytes"},
-            "kernel": {"name": "admm_persistent", "ctas_per_instance": info["blocks"],
+            "kernel": {"name": "admm_persistent" if info["sync"] != "stream-graph"
+                       else "k_global+k_local+k_final (graph while-node)",
+                       "ctas_per_instance": info["blocks"],
                        "instances": info["instances"], "threads": info["threads"],
                        "smem_bytes": info["smem_bytes"], "resident": info["resident"],
                        "sync": info["sync"]},

@@ -39,7 +39,7 @@ typedef struct dopf_cuda_info_t {
   int32_t threads;     /* threads per CTA                         */
   int32_t smem_bytes;  /* dynamic shared memory per CTA           */
   int32_t resident;    /* 1: all operators staged in shared memory */
-  int32_t sync_mode;   /* 0 block, 1 cluster, 2 grid barrier      */
+  int32_t sync_mode;   /* 0 block, 1 cluster, 2 grid, 3 streaming graph */
 } dopf_cuda_info_t;
 
 int dopf_cuda_create(int device, dopf_cuda_ctx** out);
@@ -60,6 +60,13 @@ int dopf_cuda_solve_batch(dopf_cuda_ctx* ctx, const dopf_settings* settings,
                           dopf_result_view* results, int32_t count);
 
 int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
+/* Solver path for the next uploads: 0 auto (default: shared-memory-resident
+ * persistent kernel when the operators fit the CTAs' shared memory, else the
+ * HBM-streaming CUDA graph), 1 resident, 2 streaming. */
+int dopf_cuda_set_path(dopf_cuda_ctx* ctx, int32_t path);
+/* Kernels executed so far (a streaming solve runs 3 per iteration inside one
+ * graph launch). */
+int64_t dopf_cuda_kernels_executed(const dopf_cuda_ctx* ctx);
 /* Number of kernels this context launched so far (evidence for benchmarks). */
 int64_t dopf_cuda_kernel_launches(const dopf_cuda_ctx* ctx);
 /* Algorithmic HBM bytes of one iteration, summed over uploaded instances

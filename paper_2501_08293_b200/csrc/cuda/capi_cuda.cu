@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -12,6 +13,7 @@
 #include "../../../include/dopf_cuda.h"
 #include "admm_kernels.cuh"
 #include "layout_builder.hpp"
+#include "stream_kernels.cuh"
 
 using namespace dopf::cuda;
 
@@ -50,7 +52,7 @@ struct dopf_cuda_ctx {
     void* p = nullptr;
     std::size_t cap = 0;  // bytes
   };
-  std::vector<Buf> bufs = std::vector<Buf>(32);
+  std::vector<Buf> bufs = std::vector<Buf>(64);
   BlockDesc* d_blocks = nullptr;
   InstDesc* d_inst = nullptr;
   double *d_P = nullptr, *d_A = nullptr, *d_v = nullptr, *d_z0 = nullptr;
@@ -70,6 +72,27 @@ struct dopf_cuda_ctx {
   std::size_t trace_cap = 0;  // doubles
   // cached layout plans (structure only), reused while the structure repeats
   std::shared_ptr<InstancePlan> plan, batch_plan;
+  // HBM-streaming path (instances too large for shared-memory residency)
+  int path_request = 0;      // 0 auto, 1 resident persistent kernel, 2 streaming graph
+  bool streaming = false;    // path of the uploaded model
+  StreamLayout SL;
+  struct StreamDev {
+    StreamChunk* chunks = nullptr;
+    StreamRow* rmeta = nullptr;
+    int64_t *pslice = nullptr, *aslice = nullptr;
+    StreamARow* ameta = nullptr;
+    double *P = nullptr, *A = nullptr, *ab = nullptr, *v = nullptr, *z0 = nullptr;
+    int32_t *col_ptr = nullptr, *copies = nullptr;
+    double *cost = nullptr, *inv = nullptr, *lo = nullptr, *hi = nullptr;
+    uint8_t* owner = nullptr;
+    double *x = nullptr, *z = nullptr, *lam = nullptr, *u = nullptr, *u_remote = nullptr;
+    double *part = nullptr, *objp = nullptr, *partials = nullptr;
+    StreamCtl* ctl = nullptr;
+  } sd;
+  cudaGraphExec_t graph = nullptr;
+  double graph_key[3] = {0, 0, 0};  // rho, eps, max_iter the graph was built for
+  const double* graph_trace = nullptr;
+  int64_t kernels = 0;       // kernels launched (graph iterations x 3 + persistent launches)
   // pinned staging for results copied back to the host
   void* h_stage = nullptr;
   std::size_t h_stage_cap = 0;
@@ -80,7 +103,13 @@ struct dopf_cuda_ctx {
   long long* d_prof = nullptr;  // [blocks][8] phase cycles
   std::size_t prof_cap = 0;
 
+  void drop_graph() {
+    if (graph) cudaGraphExecDestroy(graph);
+    graph = nullptr;
+  }
+
   void free_model() {
+    drop_graph();
     for (Buf& b : bufs) {
       if (b.p) cudaFree(b.p);
       b = Buf{};
@@ -312,6 +341,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
      "launch");
   ck(cudaEventRecord(c->ev1, c->stream), "event");
   ++c->launches;
+  ++c->kernels;
   ck(cudaEventSynchronize(c->ev1), "kernel");
   ck(cudaGetLastError(), "kernel");
   float ms = 0;
@@ -409,6 +439,186 @@ int dopf_cuda_create(int device, dopf_cuda_ctx** out) {
   return DOPF_OK;
 }
 
+namespace {
+
+bool needs_streaming(const dopf_model_view& m, const LayoutOptions& opt) {
+  // resident kernel: <= 148 CTAs x 480 threads x kMaxK rows, operators in smem
+  const int64_t cap_rows = static_cast<int64_t>(opt.max_blocks) * (opt.threads - 32) * kMaxK;
+  if (m.N_z > cap_rows) return true;
+  double bytes = 0;
+  for (int s = 0; s < m.S; ++s) {
+    const double n = m.z_offsets[s + 1] - m.z_offsets[s];
+    bytes += 8.0 * (n * n + m.m_s[s] * n);
+  }
+  return bytes > 0.8 * static_cast<double>(opt.max_blocks) * static_cast<double>(opt.smem_limit);
+}
+
+void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m) {
+  c->SL = build_stream_layout(m);
+  const StreamLayout& L = c->SL;
+  auto& d = c->sd;
+  int k = 32;  // slots 32.. (the resident path uses 0..31)
+  d.chunks = c->put(k++, L.chunks);
+  d.rmeta = c->put(k++, L.rmeta);
+  d.pslice = c->put(k++, L.pslice);
+  d.aslice = c->put(k++, L.aslice);
+  d.ameta = c->put(k++, L.ameta);
+  d.P = c->put(k++, L.P);
+  d.A = c->put(k++, L.A);
+  d.ab = c->put(k++, L.ab);
+  d.v = c->put(k++, L.v);
+  d.z0 = c->put(k++, L.z0);
+  d.col_ptr = c->put(k++, L.col_ptr);
+  d.copies = c->put(k++, L.copies);
+  d.cost = c->put(k++, L.c);
+  d.inv = c->put(k++, L.inv);
+  d.lo = c->put(k++, L.lo);
+  d.hi = c->put(k++, L.hi);
+  d.owner = c->put(k++, L.owner);
+  d.x = c->scratch<double>(k++, L.cols);
+  d.z = c->scratch<double>(k++, L.rows);
+  d.lam = c->scratch<double>(k++, L.rows);
+  d.u = c->scratch<double>(k++, L.rows);
+  d.u_remote = c->scratch<double>(k++, std::max(1, L.remote_slots));
+  d.part = c->scratch<double>(k++, static_cast<std::size_t>(L.chunks.size()) * 8);
+  d.objp = c->scratch<double>(k++, (L.cols + kStreamRows - 1) / kStreamRows);
+  d.partials = c->scratch<double>(k++, 8);
+  d.ctl = c->scratch<StreamCtl>(k++, 1);
+  ck(cudaStreamSynchronize(c->stream), "upload sync");
+  c->drop_graph();
+}
+
+StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* trace) {
+  const StreamLayout& L = c->SL;
+  auto& d = c->sd;
+  StreamParams p{};
+  p.chunks = d.chunks;
+  p.rmeta = d.rmeta;
+  p.pslice = d.pslice;
+  p.aslice = d.aslice;
+  p.ameta = d.ameta;
+  p.P = d.P;
+  p.A = d.A;
+  p.ab = d.ab;
+  p.v = d.v;
+  p.col_ptr = d.col_ptr;
+  p.copies = d.copies;
+  p.cost = d.cost;
+  p.inv = d.inv;
+  p.lo = d.lo;
+  p.hi = d.hi;
+  p.owner = d.owner;
+  p.x = d.x;
+  p.z = d.z;
+  p.lam = d.lam;
+  p.u = d.u;
+  p.u_remote = d.u_remote;
+  p.part = d.part;
+  p.objp = d.objp;
+  p.trace = trace;
+  p.ctl = d.ctl;
+  p.partials_out = nullptr;
+  p.rho = s->rho;
+  p.eps = s->eps_rel;
+  p.max_iter = s->max_iter;
+  p.nchunks = static_cast<int32_t>(L.chunks.size());
+  p.cols = L.cols;
+  p.col_blocks = (L.cols + kStreamRows - 1) / kStreamRows;
+  return p;
+}
+
+// state of iteration 0: z = z^0, lambda = 0, u = z^0 - 0/rho = z^0, loop counters cleared
+void stream_reset(dopf_cuda_ctx* c) {
+  const StreamLayout& L = c->SL;
+  auto& d = c->sd;
+  ck(cudaMemcpyAsync(d.z, d.z0, L.rows * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "z0");
+  ck(cudaMemcpyAsync(d.u, d.z0, L.rows * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "u0");
+  ck(cudaMemsetAsync(d.lam, 0, L.rows * sizeof(double), c->stream), "lambda0");
+  ck(cudaMemsetAsync(d.ctl, 0, sizeof(StreamCtl), c->stream), "ctl");
+}
+
+void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, bool copy_vectors) {
+  check_settings(s);
+  if (!c->uploaded) throw std::invalid_argument("no model uploaded");
+  const StreamLayout& L = c->SL;
+  auto& d = c->sd;
+  const std::size_t need = r->trace ? static_cast<std::size_t>(s->max_iter) * 6 : 0;
+  if (need > c->trace_cap) {
+    if (c->d_trace) cudaFree(c->d_trace);
+    c->d_trace = nullptr;
+    ck(cudaMalloc(&c->d_trace, need * sizeof(double)), "trace alloc");
+    c->trace_cap = need;
+    c->drop_graph();
+  }
+  double* trace = r->trace ? c->d_trace : nullptr;
+  if (!c->graph || c->graph_key[0] != s->rho || c->graph_key[1] != s->eps_rel ||
+      c->graph_key[2] != s->max_iter || c->graph_trace != trace) {
+    c->drop_graph();
+    ck(stream_build_graph(stream_params(c, s, trace), &c->graph), "graph build");
+    c->graph_key[0] = s->rho;
+    c->graph_key[1] = s->eps_rel;
+    c->graph_key[2] = s->max_iter;
+    c->graph_trace = trace;
+  }
+  const auto t_up0 = std::chrono::steady_clock::now();
+  stream_reset(c);
+  // DOPF_STREAM_NOGRAPH=1: stream-ordered launches with a host stop check per
+  // iteration (profilers that do not descend into conditional graph nodes)
+  const char* nograph = std::getenv("DOPF_STREAM_NOGRAPH");
+  ck(cudaEventRecord(c->ev0, c->stream), "event");
+  if (nograph && nograph[0] == '1') {
+    const StreamParams p = stream_params(c, s, trace);
+    StreamCtl h{};
+    do {
+      stream_launch_iteration(p, c->stream);
+      ck(cudaMemcpyAsync(&h, d.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost, c->stream), "ctl");
+      ck(cudaStreamSynchronize(c->stream), "iteration");
+    } while (!h.done);
+  } else {
+    ck(cudaGraphLaunch(c->graph, c->stream), "graph launch");
+  }
+  ck(cudaEventRecord(c->ev1, c->stream), "event");
+  ck(cudaEventSynchronize(c->ev1), "graph");
+  ck(cudaGetLastError(), "graph");
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "elapsed");
+  c->last_kernel_s = ms * 1e-3;
+  ++c->launches;
+  const auto t_dn0 = std::chrono::steady_clock::now();
+  StreamCtl ctl{};
+  ck(cudaMemcpy(&ctl, d.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost), "d2h");
+  c->kernels += 3ll * ctl.t;
+  r->status = ctl.status;
+  r->iterations = ctl.t;
+  r->objective = ctl.objective;
+  r->max_local_infeasibility = ctl.maxinf;
+  r->time_solve = c->last_kernel_s;
+  r->time_global = r->time_local = r->time_dual = 0.0;
+  if (copy_vectors && (r->x || r->z || r->lambda)) {
+    const std::size_t R = static_cast<std::size_t>(L.rows);
+    double* st = static_cast<double*>(c->stage((2 * R + L.cols) * sizeof(double)));
+    ck(cudaMemcpyAsync(st, d.z, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(st + R, d.lam, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(st + 2 * R, d.x, L.cols * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "d2h");
+    if (r->x)
+      for (int32_t q = 0; q < L.cols; ++q) r->x[L.gcol[q]] = st[2 * R + q];
+    for (std::size_t dd = 0; dd < R; ++dd) {
+      const int32_t ref = L.ref_of_dev[dd];
+      if (r->z) r->z[ref] = st[dd];
+      if (r->lambda) r->lambda[ref] = st[R + dd];
+    }
+  }
+  if (r->trace && ctl.t > 0)
+    ck(cudaMemcpy(r->trace, c->d_trace, static_cast<std::size_t>(ctl.t) * 6 * sizeof(double),
+                  cudaMemcpyDeviceToHost),
+       "trace d2h");
+  r->time_download = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_dn0).count();
+  r->time_upload = std::chrono::duration<double>(t_dn0 - t_up0).count() - c->last_kernel_s;
+}
+
+}  // namespace
+
 int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
   if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
@@ -416,11 +626,19 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
     c->uploaded = false;
     c->L.reset();
     const LayoutOptions opt = options_for(c);
+    if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
+    c->streaming = c->path_request == 2 || (c->path_request == 0 && needs_streaming(*m, opt));
+    c->inst_nz = {m->N_z};
+    c->inst_n = {m->n};
+    if (c->streaming) {
+      upload_stream(c, *m);
+      c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
+      c->uploaded = true;
+      return;
+    }
     if (!c->plan || !c->plan->same_structure(*m, opt))
       c->plan = std::make_shared<InstancePlan>(plan_instance(*m, choose_blocks(*m, opt), opt));
     append_instance(c->L, *c->plan, *m);
-    c->inst_nz = {m->N_z};
-    c->inst_n = {m->n};
     finish_upload(c);
   });
 }
@@ -430,6 +648,7 @@ int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t 
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->uploaded = false;
+    c->streaming = false;
     LayoutOptions opt = options_for(c);
     opt.max_blocks = 8;  // one cluster per scenario
     if (!c->batch_plan || !c->batch_plan->same_structure(ms[0], opt))
@@ -449,18 +668,33 @@ int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t 
 
 int dopf_cuda_solve(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r) {
   if (!c || !r) return DOPF_ERR_INVALID_ARGUMENT;
-  return guarded(c, [&] { run(c, s, r, 1, true); });
+  return guarded(c, [&] {
+    if (c->streaming) run_stream(c, s, r, true);
+    else run(c, s, r, 1, true);
+  });
 }
 
 int dopf_cuda_solve_device(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r) {
   if (!c || !r) return DOPF_ERR_INVALID_ARGUMENT;
-  return guarded(c, [&] { run(c, s, r, 1, false); });
+  return guarded(c, [&] {
+    if (c->streaming) run_stream(c, s, r, false);
+    else run(c, s, r, 1, false);
+  });
+}
+
+int dopf_cuda_set_path(dopf_cuda_ctx* c, int32_t path) {
+  if (!c || path < 0 || path > 2) return DOPF_ERR_INVALID_ARGUMENT;
+  c->path_request = path;
+  return DOPF_OK;
 }
 
 int dopf_cuda_solve_batch(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r,
                           int32_t count) {
   if (!c || !r) return DOPF_ERR_INVALID_ARGUMENT;
-  return guarded(c, [&] { run(c, s, r, count, true); });
+  return guarded(c, [&] {
+    if (c->streaming) throw std::invalid_argument("no batch uploaded");
+    run(c, s, r, count, true);
+  });
 }
 
 const char* dopf_cuda_last_error(const dopf_cuda_ctx* c) { return c ? c->err.c_str() : ""; }
@@ -478,6 +712,15 @@ void dopf_cuda_destroy(dopf_cuda_ctx* c) {
 
 int dopf_cuda_info(const dopf_cuda_ctx* c, dopf_cuda_info_t* out) {
   if (!c || !out) return DOPF_ERR_INVALID_ARGUMENT;
+  if (c->streaming) {
+    out->instances = 1;
+    out->blocks = static_cast<int32_t>(c->SL.chunks.size());
+    out->threads = kStreamRows;
+    out->smem_bytes = 0;
+    out->resident = 0;
+    out->sync_mode = 3;  // streaming graph (while-node)
+    return DOPF_OK;
+  }
   out->instances = static_cast<int32_t>(c->L.inst.size());
   out->blocks = c->L.blocks_per_instance;
   out->threads = kThreads;
@@ -488,6 +731,8 @@ int dopf_cuda_info(const dopf_cuda_ctx* c, dopf_cuda_info_t* out) {
 }
 
 int64_t dopf_cuda_kernel_launches(const dopf_cuda_ctx* c) { return c ? c->launches : 0; }
+
+int64_t dopf_cuda_kernels_executed(const dopf_cuda_ctx* c) { return c ? c->kernels : 0; }
 
 double dopf_cuda_bytes_per_iteration(const dopf_cuda_ctx* c) {
   return c ? c->L.bytes_per_iteration : 0.0;

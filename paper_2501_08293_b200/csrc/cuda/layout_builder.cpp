@@ -20,7 +20,7 @@ double sub_cost(const dopf_model_view& m, int s) {
 // Depth-first order of the component graph: subsystems s and s' are adjacent
 // when they hold copies of one global column. Cutting this walk into
 // contiguous pieces keeps most copies of a column inside one block.
-std::vector<int> locality_order(const dopf_model_view& m) {
+std::vector<int> locality_order_impl(const dopf_model_view& m) {
   std::vector<int> s_of_ref(m.N_z);
   for (int s = 0; s < m.S; ++s)
     for (int k = m.z_offsets[s]; k < m.z_offsets[s + 1]; ++k) s_of_ref[k] = s;
@@ -75,6 +75,8 @@ std::vector<std::vector<int>> split_blocks(const dopf_model_view& m, const std::
 }
 
 }  // namespace
+
+std::vector<int> locality_order(const dopf_model_view& m) { return locality_order_impl(m); }
 
 std::size_t block_smem_bytes(const BlockDesc& b, bool ops_in_smem) {
   // must match the carve-up at the top of admm_persistent
@@ -157,7 +159,7 @@ InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions&
   P.csr_copy.assign(m.csr_copy, m.csr_copy + m.N_z);
 
   const std::vector<std::vector<int>> parts =
-      split_blocks(m, locality_order(m), std::max(1, std::min(G, std::max(1, m.S))));
+      split_blocks(m, locality_order_impl(m), std::max(1, std::min(G, std::max(1, m.S))));
   const int nb = static_cast<int>(parts.size());
   const int cw = opt.threads - 32;
 

@@ -78,6 +78,10 @@ void reserve_instances(HostLayout& L, const InstancePlan& plan, std::size_t coun
 /// Appends one instance: rebased index structure + values gathered from m.
 void append_instance(HostLayout& L, const InstancePlan& plan, const dopf_model_view& m);
 
+/// Depth-first order of the component graph (subsystems adjacent when they
+/// share a global column): cutting it into pieces keeps copies together.
+std::vector<int> locality_order(const dopf_model_view& m);
+
 /// Picks the CTA count for one instance: enough CTAs that every block's
 /// operators fit in shared memory and rows fit kMaxK per thread.
 int choose_blocks(const dopf_model_view& m, const LayoutOptions& opt);

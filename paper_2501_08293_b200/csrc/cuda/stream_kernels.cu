@@ -1,0 +1,291 @@
+// HBM-streaming fp64 ADMM iteration for instances whose operators do not fit
+// shared memory (the tiled 0.5M-bus feeder). Three kernels per iteration,
+// replayed by ONE CUDA-graph launch with a conditional while-node whose
+// condition the finalize kernel clears at the stop test -- no host round trip
+// per iteration:
+//
+//  k_global   (thread per column)  admm.cpp:118-129: acc = sum over the
+//             column's copies (CSR, ascending s) of u = z - lambda/rho;
+//             x = clamp((acc - c/rho) * inv_count, lo, hi); c'x partials.
+//  k_local    (CTA per chunk of whole subsystems, thread per row)
+//             admm.cpp:131-143, 203-205, 150-163: target in shared memory,
+//             z = P target + v with P streamed from HBM (sliced ELL: 256
+//             contiguous bytes per warp load), dual update, u, ||A z - b||_inf,
+//             residual partials.
+//  k_final    (one CTA) admm.cpp:164-169, 223-234: fixed-order combine of the
+//             partials, trace row, running max, stop test.
+//
+// Bitwise parity with the oracle: --fmad=false and the reference's operation
+// forms and summation orders for every iterate; only the residual/objective
+// reductions are trees (stop test and trace only).
+#include "stream_kernels.cuh"
+
+namespace dopf::cuda {
+
+namespace {
+
+__device__ __forceinline__ double sel_max(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double sel_min(double a, double b) { return (b < a) ? b : a; }
+
+// fixed-shape block reduction of `V` values (sum; index `imax` uses max)
+template <int V, int T>
+__device__ __forceinline__ void block_reduce(double (&v)[V], double* sh, int imax) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int q = 0; q < V; ++q)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v[q], off);
+      v[q] = q == imax ? sel_max(v[q], o) : v[q] + o;
+    }
+  constexpr int W = T / 32;
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < V; ++q) sh[q * W + warp] = v[q];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      double x = lane < W ? sh[q * W + lane] : (q == imax ? 0.0 : 0.0);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, x, off);
+        x = q == imax ? sel_max(x, o) : x + o;
+      }
+      v[q] = x;
+    }
+  }
+}
+
+__device__ __forceinline__ void finalize_iteration(const StreamParams& p, const double (&v)[7]) {
+  StreamCtl* ctl = p.ctl;
+  const int t = ctl->t + 1;
+  const double pres = sqrt(v[0]);
+  const double dres = p.rho * sqrt(v[1]);
+  const double eps_prim = p.eps * sel_max(sqrt(v[2]), sqrt(v[3]));
+  const double eps_dual = p.eps * sqrt(v[4]);
+  const bool stop = pres <= eps_prim && dres <= eps_dual;
+  ctl->t = t;
+  ctl->maxinf = sel_max(ctl->maxinf, v[5]);
+  ctl->objective = v[6];
+  if (p.trace) {
+    double* row = p.trace + static_cast<int64_t>(t - 1) * 6;
+    row[0] = t;
+    row[1] = pres;
+    row[2] = dres;
+    row[3] = eps_prim;
+    row[4] = eps_dual;
+    row[5] = v[6];
+  }
+  if (stop || t >= p.max_iter) {
+    ctl->status = stop ? 0 : 1;
+    ctl->done = 1;
+    if (p.use_cond) cudaGraphSetConditional(p.cond, 0);
+  }
+}
+
+__global__ void __launch_bounds__(kStreamRows) k_global(const StreamParams p) {
+  __shared__ double sh[8];
+  const int c = blockIdx.x * kStreamRows + threadIdx.x;
+  double o[1] = {0.0};
+  if (c < p.cols) {
+    double acc = 0.0;
+    for (int q = p.col_ptr[c]; q < p.col_ptr[c + 1]; ++q) {
+      const int32_t ref = p.copies[q];
+      acc = acc + (ref >= 0 ? p.u[ref] : p.u_remote[-ref - 1]);
+    }
+    const double unclamped = (acc - p.cost[c] / p.rho) * p.inv[c];
+    const double xv = sel_min(sel_max(unclamped, p.lo[c]), p.hi[c]);
+    p.x[c] = xv;
+    if (p.owner[c]) o[0] = p.cost[c] * xv;
+  }
+  block_reduce<1, kStreamRows>(o, sh, -1);
+  if (threadIdx.x == 0) p.objp[blockIdx.x] = o[0];
+}
+
+__global__ void __launch_bounds__(kStreamRows) k_local(const StreamParams p) {
+  __shared__ double tgt[kStreamRows];
+  __shared__ double zsh[kStreamRows];
+  __shared__ double sh[6 * (kStreamRows / 32)];
+  const StreamChunk ch = p.chunks[blockIdx.x];
+  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+  const double rho = p.rho;
+  const bool on = r < ch.rows;
+  const int d = ch.row0 + r;
+  StreamRow rm{0, 0, 0, 0};
+  double bx = 0.0, lamv = 0.0;
+  if (on) {
+    rm = p.rmeta[d];
+    bx = p.x[rm.xcol];
+    lamv = p.lam[d];
+    tgt[r] = bx + lamv / rho;  // admm.cpp:136
+  }
+  __syncthreads();
+  double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (on) {
+    const double* pr = p.P + p.pslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
+    const double* tb = tgt + rm.base;
+    double acc = 0.0;
+    for (int j0 = 0; j0 < rm.n; j0 += 8) {
+      double pv[8], tv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        pv[e] = 0.0;
+        tv[e] = 0.0;
+        if (j0 + e < rm.n) {
+          pv[e] = __ldcs(pr + 32 * (j0 + e));  // streamed once per iteration
+          tv[e] = tb[j0 + e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (j0 + e < rm.n) acc = acc + pv[e] * tv[e];
+    }
+    const double z = acc + p.v[d];
+    const double zprev = p.z[d];
+    const double dd = bx - z;
+    const double ln = lamv + rho * dd;  // admm.cpp:142
+    p.z[d] = z;
+    p.lam[d] = ln;
+    p.u[d] = z - ln / rho;  // the next global update's z - lambda/rho
+    zsh[r] = z;
+    v[0] = dd * dd;
+    const double dz = z - zprev;
+    v[1] = dz * dz;
+    v[2] = bx * bx;
+    v[3] = z * z;
+    v[4] = ln * ln;
+  }
+  __syncthreads();
+  if (r < ch.arows) {
+    const StreamARow am = p.ameta[blockIdx.x * kStreamRows + r];
+    const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
+    const double* zb = zsh + am.base;
+    double acc = 0.0;
+    for (int j = 0; j < am.n; ++j) acc = acc + __ldcs(ar + 32 * j) * zb[j];
+    v[5] = fabs(acc - p.ab[ch.arow0 + r]);
+  }
+  block_reduce<6, kStreamRows>(v, sh, 5);
+  if (threadIdx.x == 0) {
+    double* out = p.part + static_cast<int64_t>(blockIdx.x) * 8;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) out[q] = v[q];
+  }
+}
+
+constexpr int kFinalThreads = 1024;
+
+__global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
+  __shared__ double sh[7 * (kFinalThreads / 32)];
+  double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gap, step, bx2, z2, lam2, maxinf, objective
+  // loads of 4 strided partials in flight per step, summed in the same fixed order
+  constexpr int U = 4;
+  for (int k0 = threadIdx.x; k0 < p.nchunks; k0 += U * kFinalThreads) {
+    double q[U][6];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * kFinalThreads;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) q[u][i] = k < p.nchunks ? __ldcg(p.part + static_cast<int64_t>(k) * 8 + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < 5; ++i) v[i] = v[i] + q[u][i];
+      v[5] = sel_max(v[5], q[u][5]);
+    }
+  }
+  for (int k0 = threadIdx.x; k0 < p.col_blocks; k0 += U * kFinalThreads) {
+    double q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * kFinalThreads;
+      q[u] = k < p.col_blocks ? __ldcg(p.objp + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[6] = v[6] + q[u];
+  }
+  block_reduce<7, kFinalThreads>(v, sh, 5);
+  if (threadIdx.x == 0) {
+    if (p.partials_out) {  // partitioned: the host combines ranks, then calls k_decide
+#pragma unroll
+      for (int q = 0; q < 7; ++q) p.partials_out[q] = v[q];
+      return;
+    }
+    finalize_iteration(p, v);
+  }
+}
+
+__global__ void k_decide(const StreamParams p, const double* ranks, int nranks) {
+  // rank partials combined in rank order: identical decision on every rank
+  double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int r = 0; r < nranks; ++r) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) v[q] = v[q] + ranks[r * 8 + q];
+    v[5] = sel_max(v[5], ranks[r * 8 + 5]);
+    v[6] = v[6] + ranks[r * 8 + 6];
+  }
+  finalize_iteration(p, v);
+}
+
+}  // namespace
+
+void stream_launch_iteration(const StreamParams& p, cudaStream_t s) {
+  k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
+  k_local<<<p.nchunks, kStreamRows, 0, s>>>(p);
+  k_final<<<1, kFinalThreads, 0, s>>>(p);
+}
+
+void stream_launch_global(const StreamParams& p, cudaStream_t s) {
+  k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
+}
+void stream_launch_local(const StreamParams& p, cudaStream_t s) {
+  k_local<<<p.nchunks, kStreamRows, 0, s>>>(p);
+  k_final<<<1, kFinalThreads, 0, s>>>(p);
+}
+void stream_launch_decide(const StreamParams& p, const double* ranks, int nranks, cudaStream_t s) {
+  k_decide<<<1, 1, 0, s>>>(p, ranks, nranks);
+}
+
+cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaGraphCreate(&g, 0);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle h;
+  e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) return e;
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+  if (e != cudaSuccess) return e;
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  p.cond = h;
+  p.use_cond = 1;
+  p.partials_out = nullptr;
+  void* args[] = {&p};
+  cudaKernelNodeParams kg = {}, kl = {}, kf = {};
+  kg.func = reinterpret_cast<void*>(k_global);
+  kg.gridDim = dim3(p.col_blocks);
+  kg.blockDim = dim3(kStreamRows);
+  kg.kernelParams = args;
+  kl = kg;
+  kl.func = reinterpret_cast<void*>(k_local);
+  kl.gridDim = dim3(p.nchunks);
+  kf = kg;
+  kf.func = reinterpret_cast<void*>(k_final);
+  kf.gridDim = dim3(1);
+  kf.blockDim = dim3(kFinalThreads);
+  cudaGraphNode_t ng, nl, nf;
+  if ((e = cudaGraphAddKernelNode(&ng, body, nullptr, 0, &kg)) != cudaSuccess) return e;
+  if ((e = cudaGraphAddKernelNode(&nl, body, &ng, 1, &kl)) != cudaSuccess) return e;
+  if ((e = cudaGraphAddKernelNode(&nf, body, &nl, 1, &kf)) != cudaSuccess) return e;
+  e = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  return e;
+}
+
+}  // namespace dopf::cuda

@@ -1,6 +1,9 @@
 #include "synth.hpp"
 
 #include <algorithm>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -346,10 +349,32 @@ Feeder generate_tiled_feeder(const ShapeSpec& shape, int copies, std::uint64_t s
   root.g_sh = {0.0, 0.0, 0.0};
   root.b_sh = {0.0, 0.0, 0.0};
   all.buses.push_back(root);
+  // tiles are independent (own seed and id prefix): generate them in parallel
+  std::vector<Feeder> tiles(copies);
+  {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nt = std::min<unsigned>(hw, static_cast<unsigned>(copies));
+    std::vector<std::thread> th;
+    std::exception_ptr err;
+    std::mutex mu;
+    for (unsigned w = 0; w < nt; ++w)
+      th.emplace_back([&, w] {
+        for (int t = static_cast<int>(w); t < copies; t += static_cast<int>(nt)) {
+          try {
+            ShapeSpec spec = shape;
+            spec.id_prefix = padded("t", t, 2) + "_";
+            tiles[t] = generate_feeder(spec, seed * 131ull + static_cast<std::uint64_t>(t));
+          } catch (...) {
+            std::lock_guard<std::mutex> lk(mu);
+            err = std::current_exception();
+          }
+        }
+      });
+    for (auto& x : th) x.join();
+    if (err) std::rethrow_exception(err);
+  }
   for (int t = 0; t < copies; ++t) {
-    ShapeSpec spec = shape;
-    spec.id_prefix = padded("t", t, 2) + "_";
-    Feeder tile = generate_feeder(spec, seed * 131ull + static_cast<std::uint64_t>(t));
+    Feeder& tile = tiles[t];
     // the tile root is no longer pinned: the tie line couples it to r_root
     Bus& troot = tile.buses.front();
     for (std::size_t k = 0; k < troot.w_lo.size(); ++k) {

@@ -533,7 +533,14 @@ class CudaSolver:
         self._err(self._lib.dopf_cuda_info(self._h, C.byref(i)))
         return {"instances": i.instances, "blocks": i.blocks, "threads": i.threads,
                 "smem_bytes": i.smem_bytes, "resident": bool(i.resident),
-                "sync": {0: "block", 1: "cluster", 2: "grid"}.get(i.sync_mode, "?")}
+                "sync": {0: "block", 1: "cluster", 2: "grid", 3: "stream-graph"}.get(i.sync_mode, "?")}
+
+    def set_path(self, path: str) -> None:
+        """'auto' | 'resident' | 'stream' for the next upload."""
+        self._err(self._lib.dopf_cuda_set_path(self._h, {"auto": 0, "resident": 1, "stream": 2}[path]))
+
+    def kernels_executed(self) -> int:
+        return int(self._lib.dopf_cuda_kernels_executed(self._h))
 
     def kernel_launches(self) -> int:
         return int(self._lib.dopf_cuda_kernel_launches(self._h))

@@ -193,3 +193,53 @@ def test_batch_ieee123_scenarios_bitwise():
         assert_same(gpu, ref, bitwise=True)
         its.add(gpu.iterations)
     assert len(its) > 1  # scenarios really converge independently
+
+
+# ------------------------------------------------------------ HBM-streaming path
+
+
+@pytest.fixture(scope="module")
+def stream_solver():
+    s = dopf.CudaSolver(0)
+    s.set_path("stream")
+    return s
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_stream_path_fixtures_bitwise(stream_solver, name):
+    _, model = model_of_fixture(name)
+    settings = dopf.Settings(rho=100.0, eps_rel=1e-4)
+    stream_solver.upload(model)
+    assert stream_solver.info()["sync"] == "stream-graph"
+    gpu = stream_solver.solve(settings)
+    ref = O.solve(model, settings)
+    assert gpu.status == dopf.CONVERGED
+    assert_same(gpu, ref, bitwise=True)
+
+
+@pytest.mark.parametrize("shape,seed,max_iter", [("ieee123", 123, 50000), ("ieee8500", 8500, 200)])
+def test_stream_path_synthetic_bitwise(stream_solver, shape, seed, max_iter):
+    f = dopf.synthetic_feeder(shape, seed)
+    _, _, model = dopf.load_model(f, workers=8)
+    model.precompute(8)
+    settings = dopf.Settings(max_iter=max_iter)
+    stream_solver.upload(model)
+    gpu = stream_solver.solve(settings)
+    ref = O.solve(model, dopf.Settings(max_iter=max_iter, workers=8))
+    assert_same(gpu, ref, bitwise=True)
+
+
+@pytest.mark.timeout(900)
+def test_tiled_feeder_auto_streams_bitwise():
+    """Tiled IEEE-8500 copies under one root (config 4 shape): too large for
+    shared-memory residency, so the auto path streams from HBM."""
+    f = dopf.tiled_feeder("ieee8500", 4, 850064)
+    _, _, model = dopf.load_model(f, workers=8)
+    model.precompute(8)
+    s = dopf.CudaSolver(0)
+    s.upload(model)
+    assert s.info()["sync"] == "stream-graph"
+    settings = dopf.Settings(max_iter=300)
+    gpu = s.solve(settings)
+    ref = O.solve(model, dopf.Settings(max_iter=300, workers=8))
+    assert_same(gpu, ref, bitwise=True)
