@@ -34,7 +34,8 @@ Line keys:
 reference cannot be built here) on the same config and
 metric. Multi-GPU (torchrun, N > 1): ieee8500 runs one independent load
 scenario per rank; batch123 shards the scenarios (no per-iteration
-collective; "weak" for ieee8500, "strong" for a fixed batch).
+collective); tiled splits ONE instance by subtree over the ranks with an NCCL
+all-gather of the boundary copies every iteration ("strong").
 """
 from __future__ import annotations
 
@@ -79,6 +80,8 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("DOPF_SHARE_GPU") == "1":  # test knob: every rank on device 0 (gloo)
+        local = 0
     return rank, world, local
 
 
@@ -261,19 +264,109 @@ def upload_bytes(models) -> int:
     return tot
 
 
+def run_partitioned(args, rank, world, local):
+    """Tiled feeder split by subtree over `world` GPUs (strong scaling): one
+    instance, boundary copies exchanged with NCCL every iteration."""
+    import numpy as np
+    import torch
+    import torch.distributed as td
+
+    from paper_2501_08293_b200 import dopf
+    from paper_2501_08293_b200.partition import PartitionedSolver
+    torch.cuda.set_device(local)
+    workers = max(1, (os.cpu_count() or 1) // max(1, world))
+    f = dopf.tiled_feeder("ieee8500", args.tiles, args.seed)
+    _, _, model = dopf.load_model(f, workers=workers)
+    model.precompute(workers)
+    ps = PartitionedSolver(local)
+    ps.upload(model)
+    settings = dopf.Settings(rho=100.0, eps_rel=1e-3, max_iter=50000)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(max(3, args.warmup)):
+        ps.solve(settings, trace=False)
+    times, its = [], []
+    k0 = ps.solver.kernels_executed()
+    with ClockSampler(local) as clocks:
+        td.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ps.stream)
+            r = ps.solve(settings, trace=False)
+            e1.record(ps.stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e-3)
+            its.append(r.iterations)
+        td.barrier()
+        torch.cuda.synchronize()
+    kernels = ps.solver.kernels_executed() - k0
+    t = torch.tensor([sum(times), ps.bytes_per_iteration()], dtype=torch.float64, device=f"cuda:{local}")
+    allt = [torch.zeros_like(t) for _ in range(world)]
+    td.all_gather(allt, t)
+    max_t = max(float(a[0]) for a in allt)
+    bytes_job = sum(float(a[1]) for a in allt)
+    value = sum(its) / max_t
+    # e2e: upload (host layout + H2D) + solve + assembled host results, per step
+    e2e_t, e2e_it = 0.0, 0
+    for step in range(args.steps + 1):
+        td.barrier()
+        t0 = time.perf_counter()
+        ps.upload(model)
+        r = ps.assemble(ps.solve(settings, trace=True))
+        dt = time.perf_counter() - t0
+        if step > 0:
+            e2e_t += dt
+            e2e_it += r.iterations
+    tt = torch.tensor([e2e_t], dtype=torch.float64, device=f"cuda:{local}")
+    td.all_reduce(tt, op=td.ReduceOp.MAX)
+    peak, peak_kind = read_peaks()
+    achieved = bytes_job * (sum(its) / args.steps) / (max_t / args.steps) / 1e9
+    if rank == 0:
+        st = model.stats()
+        line = {
+            "metric": metric_name(args), "value": value, "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * max_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {**config_of(args, world), "parallelism": f"subtree-partitioned over {world} GPUs "
+                       "(NCCL all-gather of boundary copies + residual partials per iteration)"},
+            "time_to_converge_ms": 1e3 * max_t / args.steps, "iterations_to_converge": int(its[-1]),
+            "status": "converged" if r.status == 0 else "iteration_limit", "objective": r.objective,
+            "e2e": {"value": e2e_it / float(tt[0]), "unit": "iter/s",
+                    "h2d_bytes_per_step": int(8 * (st["sum_n2"] + st["sum_mn"]) + 40 * st["N_z"]),
+                    "d2h_bytes_per_step": int(8 * (st["n"] + 2 * st["N_z"])),
+                    "time_to_converge_ms": 1e3 * float(tt[0]) / args.steps},
+            "gpu_launches": int(kernels),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+                         "frac": achieved / (peak * world), "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_iteration": bytes_job,
+                         "note": "whole job: algorithmic bytes of all ranks / max rank time vs world x HBM peak"},
+            "kernel": {"name": "k_global+k_local+k_pack+k_final+k_decide per iteration", "ranks": world},
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     rank, world, local = dist_env()
     import torch
     if world > 1:
         import torch.distributed as td
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("DOPF_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         td.init_process_group(backend=backend)
     if args.impl == "reference":
         run_reference(args, rank, world)
         if world > 1:
             import torch.distributed as td
             td.destroy_process_group()
+        return
+    if args.config == "tiled" and world > 1:
+        run_partitioned(args, rank, world, local)
+        import torch.distributed as td
+        td.destroy_process_group()
         return
 
     import ctypes as C

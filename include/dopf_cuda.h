@@ -83,6 +83,45 @@ double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* ctx);
 int dopf_cuda_set_profiling(dopf_cuda_ctx* ctx, int32_t on);
 int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out, int32_t max_blocks);
 
+/* ---- Partitioned solve over several ranks (one process per GPU) ----------
+ * Subsystem s lives on rank part_of_s[s]. Each rank updates the columns its
+ * rows reference; copies held by other ranks arrive through the caller's
+ * collective: after step 1 of every iteration, gather every rank's `send`
+ * (max_export doubles) into `recv` (nparts * max_export, rank order) and every
+ * rank's `partials` (8 doubles) into `ranks` (nparts * 8, rank order), then
+ * run step 2 (the identical stop decision on every rank). Before iteration 1,
+ * step 3 packs u^0 and the same gather fills `recv`. Loop:
+ *   begin; step 3; gather(send); repeat { step 0; step 1; gather(send, partials); step 2 }
+ *   until poll says done (kernels after the stop are no-ops, so polling may be lazy); finish.
+ * Iterates are bitwise identical to the single-GPU solve (same summation orders). */
+typedef struct dopf_part_info {
+  int32_t nparts, part, rows, cols, n_export, max_export;
+  void* send;      /* device double[max_export]        */
+  void* recv;      /* device double[nparts*max_export] */
+  void* partials;  /* device double[8]                 */
+  void* ranks;     /* device double[nparts*8]          */
+  double bytes_per_iteration;  /* algorithmic bytes of this rank's share */
+} dopf_part_info;
+int dopf_cuda_upload_part(dopf_cuda_ctx* ctx, const dopf_model_view* model, int32_t nparts,
+                          int32_t part, const int32_t* part_of_s);
+int dopf_cuda_part_info(const dopf_cuda_ctx* ctx, dopf_part_info* out);
+/* Launch on an external stream (e.g. the collective library's), NULL: own stream. */
+int dopf_cuda_set_stream(dopf_cuda_ctx* ctx, void* stream);
+int dopf_cuda_part_begin(dopf_cuda_ctx* ctx, const dopf_settings* settings, int32_t with_trace);
+int dopf_cuda_part_step(dopf_cuda_ctx* ctx, int32_t phase);
+int dopf_cuda_part_poll(dopf_cuda_ctx* ctx, int32_t* done, int32_t* iterations);
+/* Fills x at the columns this rank owns and z / lambda at its rows (masks
+ * set to 1 there), trace, status, iterations, objective, infeasibility. */
+int dopf_cuda_part_finish(dopf_cuda_ctx* ctx, dopf_result_view* result, uint8_t* x_mask,
+                          uint8_t* z_mask);
+
+/* Host-only helpers of the partitioned solve: the subsystem -> rank map
+ * (contiguous, cost-balanced pieces of the depth-first component walk; every
+ * rank computes the same), and one rank's layout sizes. */
+int dopf_partition_subsystems(const dopf_model_view* model, int32_t nparts, int32_t* part_of_s);
+int dopf_layout_probe_part(const dopf_model_view* model, int32_t nparts, int32_t part,
+                           const int32_t* part_of_s, dopf_part_info* out);
+
 /* Device layout of one model, computed on the host only (no GPU needed):
  * what dopf_cuda_upload would build for a device with `max_blocks` SMs and
  * `smem_limit` bytes of opt-in shared memory per CTA. */

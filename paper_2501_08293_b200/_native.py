@@ -53,6 +53,12 @@ class LayoutStats_t(C.Structure):
                 ("local_copies", i64), ("exported_rows", i64), ("bytes_per_iteration", f64)]
 
 
+class PartInfo_t(C.Structure):
+    _fields_ = [("nparts", i32), ("part", i32), ("rows", i32), ("cols", i32), ("n_export", i32),
+                ("max_export", i32), ("send", vp), ("recv", vp), ("partials", vp), ("ranks", vp),
+                ("bytes_per_iteration", f64)]
+
+
 class BatchInfo_t(C.Structure):
     _fields_ = [("instances", i32), ("blocks", i32), ("threads", i32), ("smem_bytes", i32),
                 ("resident", i32), ("sync_mode", i32)]
@@ -136,6 +142,15 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_phase_cycles", C.c_int, vp, P(i64), i32)
     _sig(lib, "dopf_layout_probe", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))
     _sig(lib, "dopf_layout_probe_batch", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))
+    _sig(lib, "dopf_partition_subsystems", C.c_int, P(ModelView_t), i32, P(i32))
+    _sig(lib, "dopf_layout_probe_part", C.c_int, P(ModelView_t), i32, i32, P(i32), P(PartInfo_t))
+    _sig(lib, "dopf_cuda_upload_part", C.c_int, vp, P(ModelView_t), i32, i32, P(i32))
+    _sig(lib, "dopf_cuda_part_info", C.c_int, vp, P(PartInfo_t))
+    _sig(lib, "dopf_cuda_set_stream", C.c_int, vp, vp)
+    _sig(lib, "dopf_cuda_part_begin", C.c_int, vp, P(Settings_t), i32)
+    _sig(lib, "dopf_cuda_part_step", C.c_int, vp, i32)
+    _sig(lib, "dopf_cuda_part_poll", C.c_int, vp, P(i32), P(i32))
+    _sig(lib, "dopf_cuda_part_finish", C.c_int, vp, P(ResultView_t), P(C.c_uint8), P(C.c_uint8))
     _cuda = lib
     return lib
 

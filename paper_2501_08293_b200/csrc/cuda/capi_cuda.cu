@@ -88,7 +88,13 @@ struct dopf_cuda_ctx {
     double *x = nullptr, *z = nullptr, *lam = nullptr, *u = nullptr, *u_remote = nullptr;
     double *part = nullptr, *objp = nullptr, *partials = nullptr;
     StreamCtl* ctl = nullptr;
+    int32_t* export_rows = nullptr;
+    double *send = nullptr, *ranks = nullptr;
   } sd;
+  bool partitioned = false;
+  StreamParams part_params{};
+  bool part_trace = false;
+  cudaStream_t own_stream = nullptr;  // the context's stream (set_stream may point elsewhere)
   cudaGraphExec_t graph = nullptr;
   double graph_key[3] = {0, 0, 0};  // rho, eps, max_iter the graph was built for
   const double* graph_trace = nullptr;
@@ -424,7 +430,8 @@ int dopf_cuda_create(int device, dopf_cuda_ctx** out) {
     c->device = device;
     ck(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
     c->smem_optin = max_dynamic_smem(device);
-    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "stream");
+    c->stream = c->own_stream;
     ck(cudaEventCreate(&c->ev0), "event");
     ck(cudaEventCreate(&c->ev1), "event");
   });
@@ -453,8 +460,9 @@ bool needs_streaming(const dopf_model_view& m, const LayoutOptions& opt) {
   return bytes > 0.8 * static_cast<double>(opt.max_blocks) * static_cast<double>(opt.smem_limit);
 }
 
-void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m) {
-  c->SL = build_stream_layout(m);
+void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, int part = 0,
+                   const int32_t* part_of_s = nullptr) {
+  c->SL = nparts > 1 ? build_stream_layout_part(m, nparts, part, part_of_s) : build_stream_layout(m);
   const StreamLayout& L = c->SL;
   auto& d = c->sd;
   int k = 32;  // slots 32.. (the resident path uses 0..31)
@@ -484,6 +492,9 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m) {
   d.objp = c->scratch<double>(k++, (L.cols + kStreamRows - 1) / kStreamRows);
   d.partials = c->scratch<double>(k++, 8);
   d.ctl = c->scratch<StreamCtl>(k++, 1);
+  d.export_rows = c->put(k++, L.export_rows);
+  d.send = c->scratch<double>(k++, std::max(1, L.max_export));
+  d.ranks = c->scratch<double>(k++, static_cast<std::size_t>(L.nparts) * 8);
   ck(cudaStreamSynchronize(c->stream), "upload sync");
   c->drop_graph();
 }
@@ -518,6 +529,10 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   p.trace = trace;
   p.ctl = d.ctl;
   p.partials_out = nullptr;
+  p.export_rows = d.export_rows;
+  p.send = d.send;
+  p.n_export = static_cast<int32_t>(L.export_rows.size());
+  p.max_export = L.max_export;
   p.rho = s->rho;
   p.eps = s->eps_rel;
   p.max_iter = s->max_iter;
@@ -630,6 +645,7 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
     c->streaming = c->path_request == 2 || (c->path_request == 0 && needs_streaming(*m, opt));
     c->inst_nz = {m->N_z};
     c->inst_n = {m->n};
+    c->partitioned = false;
     if (c->streaming) {
       upload_stream(c, *m);
       c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
@@ -649,6 +665,7 @@ int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t 
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->uploaded = false;
     c->streaming = false;
+    c->partitioned = false;
     LayoutOptions opt = options_for(c);
     opt.max_blocks = 8;  // one cluster per scenario
     if (!c->batch_plan || !c->batch_plan->same_structure(ms[0], opt))
@@ -682,6 +699,138 @@ int dopf_cuda_solve_device(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result
   });
 }
 
+int dopf_cuda_set_stream(dopf_cuda_ctx* c, void* stream) {
+  if (!c) return DOPF_ERR_INVALID_ARGUMENT;
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  return DOPF_OK;
+}
+
+int dopf_cuda_upload_part(dopf_cuda_ctx* c, const dopf_model_view* m, int32_t nparts, int32_t part,
+                          const int32_t* part_of_s) {
+  if (!c || !m || nparts < 1 || part < 0 || part >= nparts || !part_of_s) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
+    c->uploaded = false;
+    c->L.reset();
+    c->streaming = true;
+    c->partitioned = true;
+    upload_stream(c, *m, nparts, part, part_of_s);
+    c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
+    c->inst_nz = {m->N_z};
+    c->inst_n = {m->n};
+    c->uploaded = true;
+  });
+}
+
+int dopf_cuda_part_info(const dopf_cuda_ctx* c, dopf_part_info* out) {
+  if (!c || !out || !c->partitioned) return DOPF_ERR_INVALID_ARGUMENT;
+  out->nparts = c->SL.nparts;
+  out->part = c->SL.part;
+  out->rows = c->SL.rows;
+  out->cols = c->SL.cols;
+  out->n_export = static_cast<int32_t>(c->SL.export_rows.size());
+  out->max_export = c->SL.max_export;
+  out->send = c->sd.send;
+  out->recv = c->sd.u_remote;
+  out->partials = c->sd.partials;
+  out->ranks = c->sd.ranks;
+  out->bytes_per_iteration = c->SL.bytes_per_iteration;
+  return DOPF_OK;
+}
+
+int dopf_cuda_part_begin(dopf_cuda_ctx* c, const dopf_settings* s, int32_t with_trace) {
+  if (!c || !c->partitioned) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    check_settings(s);
+    const std::size_t need = with_trace ? static_cast<std::size_t>(s->max_iter) * 6 : 0;
+    if (need > c->trace_cap) {
+      if (c->d_trace) cudaFree(c->d_trace);
+      c->d_trace = nullptr;
+      ck(cudaMalloc(&c->d_trace, need * sizeof(double)), "trace alloc");
+      c->trace_cap = need;
+    }
+    c->part_trace = with_trace != 0;
+    c->part_params = stream_params(c, s, with_trace ? c->d_trace : nullptr);
+    c->part_params.partials_out = c->sd.partials;
+    stream_reset(c);
+    // u^0 of the exported rows for the first global update: pack z^0
+    ck(cudaEventRecord(c->ev0, c->stream), "event");
+  });
+}
+
+int dopf_cuda_part_step(dopf_cuda_ctx* c, int32_t phase) {
+  if (!c || !c->partitioned || phase < 0 || phase > 3) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    const StreamParams& p = c->part_params;
+    if (phase == 0) {
+      stream_launch_global(p, c->stream);
+      c->kernels += 1;
+    } else if (phase == 1) {
+      stream_launch_local(p, c->stream);
+      c->kernels += p.max_export > 0 ? 3 : 2;
+    } else if (phase == 2) {
+      stream_launch_decide(p, c->sd.ranks, c->SL.nparts, c->stream);
+      c->kernels += 1;
+    } else {
+      stream_launch_pack(p, c->stream);  // exports of the current u (u^0 before iteration 1)
+      c->kernels += 1;
+    }
+    ck(cudaGetLastError(), "launch");
+  });
+}
+
+int dopf_cuda_part_poll(dopf_cuda_ctx* c, int32_t* done, int32_t* iterations) {
+  if (!c || !c->partitioned) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    StreamCtl h{};
+    ck(cudaMemcpyAsync(&h, c->sd.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost, c->stream), "ctl");
+    ck(cudaStreamSynchronize(c->stream), "poll");
+    if (done) *done = h.done;
+    if (iterations) *iterations = h.t;
+  });
+}
+
+int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask, uint8_t* z_mask) {
+  if (!c || !c->partitioned || !r) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaEventRecord(c->ev1, c->stream), "event");
+    ck(cudaEventSynchronize(c->ev1), "solve");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "elapsed");
+    c->last_kernel_s = ms * 1e-3;
+    ++c->launches;
+    const StreamLayout& L = c->SL;
+    StreamCtl h{};
+    ck(cudaMemcpy(&h, c->sd.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost), "d2h");
+    r->status = h.status;
+    r->iterations = h.t;
+    r->objective = h.objective;
+    r->max_local_infeasibility = h.maxinf;
+    r->time_solve = c->last_kernel_s;
+    const std::size_t R = static_cast<std::size_t>(L.rows);
+    std::vector<double> z(R), lam(R), x(L.cols);
+    ck(cudaMemcpy(z.data(), c->sd.z, R * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    ck(cudaMemcpy(lam.data(), c->sd.lam, R * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    ck(cudaMemcpy(x.data(), c->sd.x, L.cols * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    for (int32_t q = 0; q < L.cols; ++q) {
+      if (!L.owner[q]) continue;
+      if (r->x) r->x[L.gcol[q]] = x[q];
+      if (x_mask) x_mask[L.gcol[q]] = 1;
+    }
+    for (std::size_t d = 0; d < R; ++d) {
+      const int32_t ref = L.ref_of_dev[d];
+      if (r->z) r->z[ref] = z[d];
+      if (r->lambda) r->lambda[ref] = lam[d];
+      if (z_mask) z_mask[ref] = 1;
+    }
+    if (r->trace && c->part_trace && h.t > 0)
+      ck(cudaMemcpy(r->trace, c->d_trace, static_cast<std::size_t>(h.t) * 6 * sizeof(double),
+                    cudaMemcpyDeviceToHost),
+         "trace d2h");
+  });
+}
+
 int dopf_cuda_set_path(dopf_cuda_ctx* c, int32_t path) {
   if (!c || path < 0 || path > 2) return DOPF_ERR_INVALID_ARGUMENT;
   c->path_request = path;
@@ -706,7 +855,7 @@ void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
 }
 
@@ -760,6 +909,52 @@ int dopf_layout_probe(const dopf_model_view* m, int32_t max_blocks, int64_t smem
     out->remote_copies = remote;
     out->local_copies = local;
     out->exported_rows = exported;
+    out->bytes_per_iteration = L.bytes_per_iteration;
+    return DOPF_OK;
+  } catch (const std::invalid_argument&) {
+    return DOPF_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return DOPF_ERR_RUNTIME;
+  }
+}
+
+int dopf_partition_subsystems(const dopf_model_view* m, int32_t nparts, int32_t* part_of_s) {
+  if (!m || nparts < 1 || !part_of_s) return DOPF_ERR_INVALID_ARGUMENT;
+  try {
+    // contiguous pieces of the depth-first walk, balanced by operator cost:
+    // for the tiled feeder every piece is a run of whole tiles (subtrees)
+    const std::vector<int> order = locality_order(*m);
+    double total = 0;
+    std::vector<double> cost(m->S);
+    for (int s = 0; s < m->S; ++s) {
+      const double n = m->z_offsets[s + 1] - m->z_offsets[s];
+      cost[s] = n * n + m->m_s[s] * n + 6.0 * n + 4.0;
+      total += cost[s];
+    }
+    double acc = 0;
+    for (int s : order) {
+      const int p = std::min<int>(nparts - 1, static_cast<int>(acc * nparts / total));
+      part_of_s[s] = p;
+      acc += cost[s];
+    }
+    return DOPF_OK;
+  } catch (const std::exception&) {
+    return DOPF_ERR_RUNTIME;
+  }
+}
+
+int dopf_layout_probe_part(const dopf_model_view* m, int32_t nparts, int32_t part,
+                           const int32_t* part_of_s, dopf_part_info* out) {
+  if (!m || !out || !part_of_s) return DOPF_ERR_INVALID_ARGUMENT;
+  try {
+    const StreamLayout L = build_stream_layout_part(*m, nparts, part, part_of_s);
+    *out = dopf_part_info{};
+    out->nparts = nparts;
+    out->part = part;
+    out->rows = L.rows;
+    out->cols = L.cols;
+    out->n_export = static_cast<int32_t>(L.export_rows.size());
+    out->max_export = L.max_export;
     out->bytes_per_iteration = L.bytes_per_iteration;
     return DOPF_OK;
   } catch (const std::invalid_argument&) {

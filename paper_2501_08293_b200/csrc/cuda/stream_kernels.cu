@@ -86,6 +86,7 @@ __device__ __forceinline__ void finalize_iteration(const StreamParams& p, const 
 
 __global__ void __launch_bounds__(kStreamRows) k_global(const StreamParams p) {
   __shared__ double sh[8];
+  if (p.ctl->done) return;  // partitioned loops may run past the stop (lazy host check)
   const int c = blockIdx.x * kStreamRows + threadIdx.x;
   double o[1] = {0.0};
   if (c < p.cols) {
@@ -103,10 +104,11 @@ __global__ void __launch_bounds__(kStreamRows) k_global(const StreamParams p) {
   if (threadIdx.x == 0) p.objp[blockIdx.x] = o[0];
 }
 
-__global__ void __launch_bounds__(kStreamRows) k_local(const StreamParams p) {
+__global__ void __launch_bounds__(kStreamRows, 3) k_local(const StreamParams p) {
   __shared__ double tgt[kStreamRows];
   __shared__ double zsh[kStreamRows];
   __shared__ double sh[6 * (kStreamRows / 32)];
+  if (p.ctl->done) return;
   const StreamChunk ch = p.chunks[blockIdx.x];
   const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
   const double rho = p.rho;
@@ -162,7 +164,14 @@ __global__ void __launch_bounds__(kStreamRows) k_local(const StreamParams p) {
     const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
     const double* zb = zsh + am.base;
     double acc = 0.0;
-    for (int j = 0; j < am.n; ++j) acc = acc + __ldcs(ar + 32 * j) * zb[j];
+    for (int j0 = 0; j0 < am.n; j0 += 8) {
+      double av[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? __ldcs(ar + 32 * (j0 + e)) : 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (j0 + e < am.n) acc = acc + av[e] * zb[j0 + e];
+    }
     v[5] = fabs(acc - p.ab[ch.arow0 + r]);
   }
   block_reduce<6, kStreamRows>(v, sh, 5);
@@ -177,6 +186,7 @@ constexpr int kFinalThreads = 1024;
 
 __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
   __shared__ double sh[7 * (kFinalThreads / 32)];
+  if (p.ctl->done) return;
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gap, step, bx2, z2, lam2, maxinf, objective
   // loads of 4 strided partials in flight per step, summed in the same fixed order
   constexpr int U = 4;
@@ -216,7 +226,14 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
   }
 }
 
+__global__ void k_pack(const StreamParams p) {
+  // this rank's exported u values -> its send slots (zero padded)
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < p.max_export) p.send[e] = e < p.n_export ? p.u[p.export_rows[e]] : 0.0;
+}
+
 __global__ void k_decide(const StreamParams p, const double* ranks, int nranks) {
+  if (p.ctl->done) return;
   // rank partials combined in rank order: identical decision on every rank
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   for (int r = 0; r < nranks; ++r) {
@@ -241,7 +258,11 @@ void stream_launch_global(const StreamParams& p, cudaStream_t s) {
 }
 void stream_launch_local(const StreamParams& p, cudaStream_t s) {
   k_local<<<p.nchunks, kStreamRows, 0, s>>>(p);
+  if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
   k_final<<<1, kFinalThreads, 0, s>>>(p);
+}
+void stream_launch_pack(const StreamParams& p, cudaStream_t s) {
+  if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
 }
 void stream_launch_decide(const StreamParams& p, const double* ranks, int nranks, cudaStream_t s) {
   k_decide<<<1, 1, 0, s>>>(p, ranks, nranks);

@@ -45,6 +45,9 @@ struct StreamParams {
   double* trace;         // [max_iter][6] or null
   StreamCtl* ctl;
   double* partials_out;  // partitioned: this rank's 7 combined partials (null: decide here)
+  const int32_t* export_rows;  // partitioned: rows whose u other ranks read
+  double* send;          // [max_export] packed exports
+  int32_t n_export, max_export;
   double rho, eps;
   int32_t max_iter;
   int32_t nchunks;
@@ -63,6 +66,7 @@ void stream_launch_iteration(const StreamParams& p, cudaStream_t s);
 /// all ranks' partials (8 doubles per rank, rank order).
 void stream_launch_global(const StreamParams& p, cudaStream_t s);
 void stream_launch_local(const StreamParams& p, cudaStream_t s);
+void stream_launch_pack(const StreamParams& p, cudaStream_t s);
 void stream_launch_decide(const StreamParams& p, const double* ranks, int nranks, cudaStream_t s);
 
 }  // namespace dopf::cuda

@@ -8,12 +8,26 @@
 namespace dopf::cuda {
 
 StreamLayout build_stream_layout(const dopf_model_view& m) {
+  return build_stream_layout_part(m, 1, 0, nullptr);
+}
+
+StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int part,
+                                      const int32_t* part_of_s) {
   if (!m.has_pre) throw std::invalid_argument("model view lacks precomputed operators");
+  if (nparts < 1 || part < 0 || part >= nparts || (nparts > 1 && !part_of_s))
+    throw std::invalid_argument("bad partition");
+  auto part_of = [&](int s) { return nparts == 1 ? 0 : part_of_s[s]; };
+  for (int s = 0; s < m.S; ++s)
+    if (part_of(s) < 0 || part_of(s) >= nparts) throw std::invalid_argument("subsystem part out of range");
   StreamLayout L;
   L.S = m.S;
   L.n = m.n;
   L.N_z = m.N_z;
-  const std::vector<int> order = locality_order(m);
+  L.nparts = nparts;
+  L.part = part;
+  std::vector<int> order;
+  for (int s : locality_order(m))
+    if (part_of(s) == part) order.push_back(s);
   auto ns_of = [&](int s) { return m.z_offsets[s + 1] - m.z_offsets[s]; };
   for (int s = 0; s < m.S; ++s)
     if (ns_of(s) > kStreamRows) throw std::invalid_argument("subsystem wider than a streaming chunk");
@@ -55,12 +69,26 @@ StreamLayout build_stream_layout(const dopf_model_view& m) {
   L.v.resize(row);
   L.z0.resize(row);
   L.ref_of_dev.resize(row);
+  std::vector<int> s_of_ref(m.N_z);
+  for (int s = 0; s < m.S; ++s)
+    for (int k2 = m.z_offsets[s]; k2 < m.z_offsets[s + 1]; ++k2) s_of_ref[k2] = s;
+
+  // columns updated here: every column a local row references, ascending
+  std::vector<int32_t> loc_of_col(m.n, -1);
+  for (int ref = 0; ref < m.N_z; ++ref)
+    if (dev_of_ref[ref] >= 0) loc_of_col[m.l2g[ref]] = 1;
+  for (int c = 0; c < m.n; ++c)
+    if (loc_of_col[c] > 0) {
+      loc_of_col[c] = static_cast<int32_t>(L.gcol.size());
+      L.gcol.push_back(c);
+    }
   for (int ref = 0; ref < m.N_z; ++ref) {
     const int32_t d = dev_of_ref[ref];
+    if (d < 0) continue;
     L.ref_of_dev[d] = ref;
     L.v[d] = m.v[ref];
     L.z0[d] = m.z0[ref];
-    L.rmeta[d] = StreamRow{prow[d].n, prow[d].base, m.l2g[ref], 0};
+    L.rmeta[d] = StreamRow{prow[d].n, prow[d].base, loc_of_col[m.l2g[ref]], 0};
   }
   // sliced ELL per chunk-local warp (rows of a warp never span chunks)
   auto pack = [](const std::vector<Src>& rows, const std::vector<StreamChunk>& chunks, bool arow_mode,
@@ -93,20 +121,60 @@ StreamLayout build_stream_layout(const dopf_model_view& m) {
       }
       L.ameta[c * kStreamRows + a] = am;
     }
-  // columns: all of them, CSR copies in ascending s -> device rows
-  L.cols = m.n;
-  L.col_ptr.assign(m.csr_ptr, m.csr_ptr + m.n + 1);
-  L.copies.resize(m.N_z);
-  for (int q = 0; q < m.N_z; ++q) L.copies[q] = dev_of_ref[m.csr_copy[q]];
-  L.gcol.resize(m.n);
-  for (int c = 0; c < m.n; ++c) L.gcol[c] = c;
-  L.c.assign(m.c, m.c + m.n);
-  L.inv.assign(m.inv_copy, m.inv_copy + m.n);
-  L.lo.assign(m.x_lo, m.x_lo + m.n);
-  L.hi.assign(m.x_hi, m.x_hi + m.n);
-  L.x0.assign(m.x0, m.x0 + m.n);
-  L.owner.assign(m.n, 1);
-  L.bytes_per_iteration = algorithmic_bytes(m);
+
+  // exports of every part (identical on all parts): copies of columns held by
+  // more than one part, ascending reference index per part
+  std::vector<std::vector<int32_t>> exports(nparts);
+  std::vector<int32_t> slot_of_ref(m.N_z, -1);
+  if (nparts > 1) {
+    std::vector<char> multi(m.n, 0);
+    for (int c = 0; c < m.n; ++c) {
+      const int p0 = part_of(s_of_ref[m.csr_copy[m.csr_ptr[c]]]);
+      for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q)
+        if (part_of(s_of_ref[m.csr_copy[q]]) != p0) multi[c] = 1;
+    }
+    for (int ref = 0; ref < m.N_z; ++ref)
+      if (multi[m.l2g[ref]]) exports[part_of(s_of_ref[ref])].push_back(ref);
+    for (const auto& e : exports) L.max_export = std::max<int32_t>(L.max_export, static_cast<int32_t>(e.size()));
+    for (int q = 0; q < nparts; ++q)
+      for (std::size_t e = 0; e < exports[q].size(); ++e)
+        slot_of_ref[exports[q][e]] = q * L.max_export + static_cast<int32_t>(e);
+    for (int32_t ref : exports[part]) L.export_rows.push_back(dev_of_ref[ref]);
+    L.remote_slots = nparts * L.max_export;
+  }
+
+  // columns: CSR over copies in ascending s; local copies -> device rows,
+  // copies of other parts -> remote slots
+  L.cols = static_cast<int32_t>(L.gcol.size());
+  L.col_ptr.assign(1, 0);
+  double msum = 0, n2 = 0, mn = 0;
+  for (const StreamChunk& ch : L.chunks) msum += ch.arows;
+  for (int32_t gc : L.gcol) {
+    for (int q = m.csr_ptr[gc]; q < m.csr_ptr[gc + 1]; ++q) {
+      const int ref = m.csr_copy[q];
+      if (part_of(s_of_ref[ref]) == part) {
+        L.copies.push_back(dev_of_ref[ref]);
+      } else {
+        if (slot_of_ref[ref] < 0) throw std::logic_error("remote copy without an export slot");
+        L.copies.push_back(-(slot_of_ref[ref] + 1));
+      }
+    }
+    L.col_ptr.push_back(static_cast<int32_t>(L.copies.size()));
+    L.c.push_back(m.c[gc]);
+    L.inv.push_back(m.inv_copy[gc]);
+    L.lo.push_back(m.x_lo[gc]);
+    L.hi.push_back(m.x_hi[gc]);
+    L.x0.push_back(m.x0[gc]);
+    L.owner.push_back(part_of(s_of_ref[m.csr_copy[m.csr_ptr[gc]]]) == part ? 1 : 0);
+  }
+  for (int s : order) {
+    const double n = ns_of(s);
+    n2 += n * n;
+    mn += m.m_s[s] * n;
+  }
+  // algorithmic bytes of this part (DESIGN.md section 4 restricted to it)
+  L.bytes_per_iteration = 8.0 * (n2 + mn + msum) + 56.0 * L.rows + 48.0 * L.cols +
+                          4.0 * (2.0 * L.rows + L.cols + 1) + 16.0 * static_cast<double>(order.size());
   return L;
 }
 

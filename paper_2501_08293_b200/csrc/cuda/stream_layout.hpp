@@ -57,10 +57,21 @@ struct StreamLayout {
   std::vector<double> c, inv, lo, hi, x0;
   std::vector<uint8_t> owner;          // 1: this rank writes x and adds c x to the objective
   int32_t remote_slots = 0;            // partitioned: size of the gathered remote u array
-  double bytes_per_iteration = 0;      // algorithmic (whole model)
+  double bytes_per_iteration = 0;      // algorithmic bytes of this rank's share
+  // partitioned exchange: this rank's exported rows (u packed into slot
+  // part * max_export + e of every rank's remote array, in this order)
+  int32_t nparts = 1, part = 0, max_export = 0;
+  std::vector<int32_t> export_rows;
 };
 
 /// Whole-model streaming layout (one rank).
 StreamLayout build_stream_layout(const dopf_model_view& m);
+
+/// Partitioned layout: part `part` of `nparts`, subsystem s on part
+/// part_of_s[s]. Columns referenced by this part's rows are updated here;
+/// copies held by other parts are read from the gathered remote array. Every
+/// part derives the same export lists from the whole model, so slots agree.
+StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int part,
+                                      const int32_t* part_of_s);
 
 }  // namespace dopf::cuda

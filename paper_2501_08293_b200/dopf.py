@@ -88,7 +88,7 @@ class Feeder:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and N is not None:  # N is None at interpreter shutdown
             N.host().dopf_feeder_free(h)
             self._h = None
 
@@ -177,7 +177,7 @@ class LinearSystem:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and N is not None:
             N.host().dopf_lp_free(h)
             self._h = None
 
@@ -287,7 +287,7 @@ class DecomposedModel:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and N is not None:
             N.host().dopf_model_free(h)
             self._h = None
 
