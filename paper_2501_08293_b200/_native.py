@@ -136,6 +136,7 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_kernel_launches", i64, vp)
     _sig(lib, "dopf_cuda_kernels_executed", i64, vp)
     _sig(lib, "dopf_cuda_set_path", C.c_int, vp, i32)
+    _sig(lib, "dopf_cuda_timeline", C.c_int, vp, P(u64), i64)
     _sig(lib, "dopf_cuda_bytes_per_iteration", f64, vp)
     _sig(lib, "dopf_cuda_last_kernel_seconds", f64, vp)
     _sig(lib, "dopf_cuda_set_profiling", C.c_int, vp, i32)

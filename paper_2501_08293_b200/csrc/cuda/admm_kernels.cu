@@ -63,9 +63,11 @@ namespace dopf::cuda {
 namespace {
 
 constexpr int kWarps = kThreads / 32;
+constexpr int kHoist = kThreads > 512 ? 4 : 8;  // operator loads in flight per row (register budget)
 constexpr int kCW = kThreads - 32;  // compute threads (warps 1..)
 constexpr int kSlots = kSlotRing;  // partial-slot ring (see header)
-constexpr int kDec = 4;             // decision ring (shared memory)
+constexpr int kDec = 8;             // decision ring (shared memory), > kLag
+static_assert(kDec > kLag, "decision ring too small");
 constexpr int kDecG = 8;            // decision ring (global, written by the leader CTA)
 constexpr int kLine = 16;           // u64 words per 128-byte line: flags are one per line
 enum : int { kBarCompute = 1, kBarExchanged = 3, kBarPartials = 4 };
@@ -129,6 +131,11 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
                : "=l"(tag), "=l"(bits) : "l"(rec) : "memory");
   v = __longlong_as_double(static_cast<long long>(bits));
   return tag;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
@@ -201,8 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   off += bd.rows;
   double* vs = smem + off;
   off += bd.rows;
-  double* xring = smem + off;  // [4][cols]: x^s in slot s % 4
-  off += 4 * static_cast<std::size_t>(bd.cols);
+  double* xring = smem + off;  // [kXRing][cols]: x^s in slot s % kXRing
+  off += kXRing * static_cast<std::size_t>(bd.cols);
   double* c_rho = smem + off;
   off += bd.cols;
   double* c_inv = smem + off;
@@ -219,6 +226,8 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   off += kDec * 4;
   long long* ph = reinterpret_cast<long long*>(smem + off);  // [8] phase clock
   off += 8;
+  double* emax = smem + off;  // [kLag + 1][kWarps] per-warp infeasibility of the last iterations
+  off += (kLag + 1) * kWarps;
   double* a_rhs = smem + off;  // equality-row rhs b_r
   off += bd.arows;
   AMeta* a_meta = reinterpret_cast<AMeta*>(smem + off);  // 16 B each
@@ -245,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
     c_hi[c] = p.chi[bd.col_off + c];
   }
   if (tid < kDec * 4) dec[tid] = 0.0;
+  if (tid < (kLag + 1) * kWarps) emax[tid] = 0.0;
   if (tid < 8) ph[tid] = 0;
 
   const int G = id.blocks;
@@ -260,8 +270,8 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   __syncthreads();
 
   int stop_at = 0;  // set by the branch that detects the stop; broadcast below
-  double m_fold[4] = {0.0, 0.0, 0.0, 0.0};  // compute threads: infeasibility ring at exit
-  int thread_last = 0;                      // compute threads: last iteration executed
+  double m_old = 0.0;   // compute warps (lane 0): warp infeasibility max over iterations <= t - kLag - 1
+  int thread_last = 0;  // compute threads: last iteration executed
   if (warp == 0) {
     // ======================= service warp =======================
     const bool leader_cta = bd.inst_block == 0;  // writes the trace and the scalar results
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       const long long c0 = tick ? clock64() : 0;
       named_sync(kBarPartials, kThreads);  // warp partials of t in red[t & 1]
       const long long c1 = tick ? clock_after_barrier(ph) : 0;
-      const bool cw_stop = (t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter;
+      const bool cw_stop = (t > kLag && dec[((t - kLag) % kDec) * 4] != 0.0) || t == p.max_iter;
       named_arrive(kBarExchanged, kThreads);
       // residuals / stop test of t-1 (read by the compute warps at t+1) --
       // BEFORE counting slot(t): a block's count for t then also certifies it
@@ -356,12 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       }
       if (cw_stop) break;
     }
-    if (t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) {
-      stop_at = t - 2;
+    if (t > kLag && dec[((t - kLag) % kDec) * 4] != 0.0) {
+      stop_at = t - kLag;
     } else {
-      // reached max_iter: decide between t-1 and t
+      // reached max_iter: the first stop among the undecided iterations, else t
       combine(t);
-      stop_at = (t >= 2 && dec[((t - 1) % kDec) * 4] != 0.0) ? t - 1 : t;
+      stop_at = t;
+      for (int q = t; q > t - kLag && q >= 1; --q)
+        if (dec[(q % kDec) * 4] != 0.0) stop_at = q;
     }
     if (lane == 0) {
       red[0] = stop_at;
@@ -464,10 +476,13 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       const unsigned long long want = static_cast<unsigned long long>(it);
       const int cnt = col_count(cpkb);
       const int32_t* q = cps + col_start(cpkb);
-      double a[4];
-      unsigned long long tg[4];
+      // every copy's load is in flight before the first wait (<= 8 copies per
+      // column in the feeders here; more are read after the first eight)
+      constexpr int H = kThreads > 512 ? 4 : 8;
+      double a[H];
+      unsigned long long tg[H];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < H; ++e) {
         a[e] = 0.0;
         tg[e] = want;
         if (e < cnt) {
@@ -480,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       }
       double acc = 0.0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < H; ++e) {
         if (e < cnt) {
           unsigned spins = 0;
           while (tg[e] != want) {
@@ -490,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           acc = acc + a[e];
         }
       }
-      for (int e = 4; e < cnt; ++e) {
+      for (int e = H; e < cnt; ++e) {
         const int32_t ref = q[e];
         double v;
         if (ref >= 0) {
@@ -509,14 +524,13 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
     obj = obj + global_boundary(0, xring + bd.cols);
     named_sync(kBarCompute, kCW);
     long long c0 = tick ? clock64() : 0, c1 = 0;
-    double m_old = 0.0, m2 = 0.0, m1 = 0.0, m0 = 0.0;  // infeasibility: <= t-3, t-2, t-1, t
     int t = 1;
     for (;; ++t) {
-      const double* xt = xring + static_cast<std::size_t>(t % 4) * bd.cols;  // x^t
-      double* xnext = xring + static_cast<std::size_t>((t + 1) % 4) * bd.cols;
+      const double* xt = xring + static_cast<std::size_t>(t % kXRing) * bd.cols;  // x^t
+      double* xnext = xring + static_cast<std::size_t>((t + 1) % kXRing) * bd.cols;
       unsigned long long* u_out = p.ux + static_cast<int64_t>(t & 1) * 2 * p.rows_total;
-      double* z_res = p.z_out + static_cast<int64_t>(t % 3) * p.rows_total;
-      double* l_res = p.lam_out + static_cast<int64_t>(t % 3) * p.rows_total;
+      double* z_res = p.z_out + static_cast<int64_t>(t % kZRing) * p.rows_total;
+      double* l_res = p.lam_out + static_cast<int64_t>(t % kZRing) * p.rows_total;
 
       // (L1) consensus target
 #pragma unroll
@@ -542,10 +556,10 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           const double* pr = Pop + pofs[k];
           const double* tb = tu + row_base(rpk[k]);
           double acc = 0.0;
-          for (int j0 = 0; j0 < n; j0 += 8) {
-            double pv[8], tv[8];
+          for (int j0 = 0; j0 < n; j0 += kHoist) {
+            double pv[kHoist], tv[kHoist];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < kHoist; ++e) {
               pv[e] = 0.0;
               tv[e] = 0.0;
               if (j0 + e < n) {
@@ -554,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
               }
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < kHoist; ++e)
               if (j0 + e < n) acc = acc + pv[e] * tv[e];
           }
           zs[r] = acc + vs[r];
@@ -594,6 +608,11 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
         }
       }
       named_sync(kBarCompute, kCW);  // every u(t) in shared memory
+      unsigned long long* tl = nullptr;
+      if (p.timeline && ctid == 0 && t >= kTimelineT0 && t < kTimelineT0 + kTimelineIters) {
+        tl = p.timeline + (static_cast<int64_t>(blockIdx.x) * kTimelineIters + (t - kTimelineT0)) * 3;
+        tl[0] = globaltimer();  // u(t) published (every warp's stores issued)
+      }
       if (tick) {
         c1 = clock_after_barrier(ph);
         ph[kPhDual] += c1 - c0;
@@ -617,10 +636,10 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           const double* ar = Aop + am.aofs;
           const double* zb = zs + am.base;
           double acc = 0.0;
-          for (int j0 = 0; j0 < am.n; j0 += 8) {
-            double av[8], zv[8];
+          for (int j0 = 0; j0 < am.n; j0 += kHoist) {
+            double av[kHoist], zv[kHoist];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < kHoist; ++e) {
               av[e] = 0.0;
               zv[e] = 0.0;
               if (j0 + e < am.n) {
@@ -629,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
               }
             }
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < kHoist; ++e)
               if (j0 + e < am.n) acc = acc + av[e] * zv[e];
           }
           e_t = sel_max(e_t, fabs(acc - a_rhs[a]));
@@ -643,10 +662,16 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
           l_res[bd.row0 + r] = lam[k];
         }
       }
-      m_old = sel_max(m_old, m2);
-      m2 = m1;
-      m1 = m0;
-      m0 = e_t;
+      {
+        // warp max of this iteration into the ring; lane 0 folds the value
+        // leaving the ring (iteration t - kLag - 1) into its running max
+        const double we = warp_max(e_t);
+        if (lane == 0) {
+          double* slot = emax + (t % (kLag + 1)) * kWarps + warp;
+          m_old = sel_max(m_old, *slot);
+          *slot = we;
+        }
+      }
       {
         const double mine = sum8(v8, lane);
         if ((lane & 3) == 0) red[(t & 1) * kWarps * kPartials + warp * kPartials + sum8_index(lane)] = mine;
@@ -659,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
       }
       // (G, boundary) x^{t+1} of the columns shared with neighbours (waits for
       // their u(t) records); x^{t+1} is speculative until the stop test
+      if (tl) tl[1] = globaltimer();  // boundary update starts
       obj = obj_next + global_boundary(t, xnext);
       if (tick) {
         c1 = clock_after_barrier(ph);
@@ -666,17 +692,17 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
         c0 = c1;
       }
       named_sync(kBarExchanged, kThreads);  // decision of t-2 in dec[]; x^{t+1} complete
+      if (tl) {
+        (void)clock_after_barrier(ph);
+        tl[2] = globaltimer();  // every boundary column of the block done
+      }
       if (tick) {
         c1 = clock_after_barrier(ph);
         ph[kPhWait] += c1 - c0;
         c0 = c1;
       }
-      if ((t >= 3 && dec[((t - 2) % kDec) * 4] != 0.0) || t == p.max_iter) break;
+      if ((t > kLag && dec[((t - kLag) % kDec) * 4] != 0.0) || t == p.max_iter) break;
     }
-    m_fold[0] = m_old;
-    m_fold[1] = m2;
-    m_fold[2] = m1;
-    m_fold[3] = m0;
     thread_last = t;
   }
   __syncthreads();
@@ -684,21 +710,20 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParam
   if (clock_on && tid < 8) p.prof[blockIdx.x * 8 + tid] += ph[tid];
   if (warp != 0) {
     // max_local_infeasibility over iterations 1..stop_at: the loop ended at
-    // t = last with stop_at in {last-2, last-1, last}
+    // t = last, stop_at >= last - kLag; the ring holds iterations last-kLag..last
     const int last = thread_last;
-    double mx = sel_max(m_fold[0], m_fold[1]);  // m_old, m2 (iteration last-2)
-    if (last - 1 <= stop_at) mx = sel_max(mx, m_fold[2]);
-    if (last <= stop_at) mx = sel_max(mx, m_fold[3]);
-    mx = warp_max(mx);
+    double mx = m_old;
+    for (int q = last - kLag; q <= stop_at; ++q)
+      if (q >= 1) mx = sel_max(mx, emax[(q % (kLag + 1)) * kWarps + warp]);
     if (lane == 0)
       atomicMax(reinterpret_cast<unsigned long long*>(p.maxinf + bd.instance),
                 static_cast<unsigned long long>(__double_as_longlong(mx)));  // mx >= 0: bit order = value order
   }
   if (warp != 0) {
     // owners write x^stop_at (still in the ring); (z, lambda)^stop_at are in
-    // result buffer stop_at % 3, which the host reads
+    // result buffer stop_at % kZRing, which the host reads
     const int ctid = tid - 32;
-    const double* xfinal = xring + static_cast<std::size_t>(stop_at % 4) * bd.cols;
+    const double* xfinal = xring + static_cast<std::size_t>(stop_at % kXRing) * bd.cols;
     for (int c = ctid; c < bd.cols; c += kCW) {
       const ColMeta cmc = p.cmeta[bd.col_off + c];
       if (cmc.owner) p.x_out[id.x_off + cmc.gcol] = xfinal[c];

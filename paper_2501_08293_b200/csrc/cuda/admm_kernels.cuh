@@ -10,7 +10,14 @@
 namespace dopf::cuda {
 
 constexpr int kCtlWords = 64;
-constexpr int kSlotRing = 4;   // residual-slot ring depth (admm_kernels.cu)  // per instance: counter (line 0), decision seq (line 1), ring (lines 2-3)
+constexpr int kTimelineT0 = 100, kTimelineIters = 64;  // iterations stamped by the timeline
+constexpr int kSlotRing = 4;   // residual-slot ring depth (admm_kernels.cu)
+// Decision lag: the compute warps act on the stop test of t - kLag at
+// iteration t, so the grid-wide residual reduction never gates an iteration;
+// x is kept kLag + 2 deep (shared memory) and z / lambda kLag + 1 deep.
+constexpr int kLag = 4;
+constexpr int kXRing = kLag + 2;
+constexpr int kZRing = kLag + 1;  // per instance: counter (line 0), decision seq (line 1), ring (lines 2-3)
 
 enum class SyncMode : int32_t { block = 0, cluster = 1, grid = 2 };
 
@@ -39,7 +46,8 @@ struct KernelParams {
   unsigned long long* flags;  // [instances][blocks_per_instance][16] "u(t) published", one per 128-B line
   unsigned long long* ctl;    // [instances][kCtlWords]: slot counter, decision seq, decision ring
   double* trace;        // [instances][trace_stride][6] (may be null)
-  long long* prof;      // [8] phase cycle counters of CTA 0 (null: off)
+  long long* prof;      // [blocks][8] phase cycle counters (null: off)
+  unsigned long long* timeline;  // [blocks][kTimelineIters][3] globaltimer stamps (null: off)
   int32_t* iters;       // [instances]
   int32_t* status;      // [instances] 0 converged, 1 iteration limit
   double* maxinf;       // [instances]

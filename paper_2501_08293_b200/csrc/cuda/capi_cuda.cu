@@ -92,6 +92,8 @@ struct dopf_cuda_ctx {
     double *send = nullptr, *ranks = nullptr;
   } sd;
   bool partitioned = false;
+  unsigned long long* d_timeline = nullptr;
+  std::size_t timeline_len = 0;
   StreamParams part_params{};
   bool part_trace = false;
   cudaStream_t own_stream = nullptr;  // the context's stream (set_stream may point elsewhere)
@@ -216,8 +218,8 @@ void upload_layout(dopf_cuda_ctx* c) {
   const std::size_t I = L.inst.size();
   const std::size_t R = static_cast<std::size_t>(L.rows_total);
   c->d_u = c->scratch<double>(k++, 4 * R);    // tagged records {t, u}, two buffers
-  c->d_z = c->scratch<double>(k++, 3 * R);    // [t % 3][row]
-  c->d_lam = c->scratch<double>(k++, 3 * R);
+  c->d_z = c->scratch<double>(k++, kZRing * R);    // [t % kZRing][row]
+  c->d_lam = c->scratch<double>(k++, kZRing * R);
   c->d_x = c->scratch<double>(k++, L.x_total);
   c->d_part = c->scratch<double>(k++, I * kSlotRing * L.blocks_per_instance * kPartials);
   c->d_flags = c->scratch<unsigned long long>(k++, I * L.blocks_per_instance * 16);
@@ -330,6 +332,13 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     ck(cudaMemset(c->d_prof, 0, c->prof_cap * sizeof(long long)), "memset");
   }
   p.prof = c->profiling ? c->d_prof : nullptr;
+  if (c->profiling) {
+    const std::size_t need = static_cast<std::size_t>(c->num_blocks) * kTimelineIters * 3;
+    c->d_timeline = c->scratch<unsigned long long>(63, need);
+    ck(cudaMemsetAsync(c->d_timeline, 0, need * 8, c->stream), "memset");
+    c->timeline_len = need;
+  }
+  p.timeline = c->profiling ? c->d_timeline : nullptr;
   p.iters = c->d_iters;
   p.status = c->d_status;
   p.maxinf = c->d_maxinf;
@@ -364,18 +373,18 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   bool any_vec = false;
   for (int i = 0; i < count; ++i)
     any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
-  // results: a single instance needs only ring buffer iters % 3; a batch
-  // copies all three (instances stop at different iterations)
+  // results: a single instance needs only ring buffer iters % kZRing; a
+  // batch copies all of them (instances stop at different iterations)
   const std::size_t R = static_cast<std::size_t>(L.rows_total);
   const bool one = I == 1;
-  const std::size_t nbuf = one ? 1 : 3;
+  const std::size_t nbuf = one ? 1 : kZRing;
   double *zdev = nullptr, *ldev = nullptr, *xall = nullptr;
   if (copy_vectors && any_vec) {
     double* st = static_cast<double*>(c->stage((2 * nbuf * R + L.x_total) * sizeof(double)));
     zdev = st;
     ldev = st + nbuf * R;
     xall = st + 2 * nbuf * R;
-    const std::size_t from = one ? (iters[0] % 3) * R : 0;
+    const std::size_t from = one ? (iters[0] % kZRing) * R : 0;
     ck(cudaMemcpyAsync(zdev, c->d_z + from, nbuf * R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaMemcpyAsync(ldev, c->d_lam + from, nbuf * R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaMemcpyAsync(xall, c->d_x, L.x_total * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
@@ -392,7 +401,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     r.time_global = r.time_local = r.time_dual = 0.0;
     if (copy_vectors && any_vec) {
       if (r.x) std::memcpy(r.x, xall + id.x_off, sizeof(double) * id.n);
-      const std::size_t base = one ? 0 : (iters[i] % 3) * R;
+      const std::size_t base = one ? 0 : (iters[i] % kZRing) * R;
       for (int32_t d = id.row0; d < id.row0 + id.rows; ++d) {
         const int32_t ref = L.ref_of_dev[d];
         if (r.z) r.z[ref] = zdev[base + d];
@@ -828,6 +837,14 @@ int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask
       ck(cudaMemcpy(r->trace, c->d_trace, static_cast<std::size_t>(h.t) * 6 * sizeof(double),
                     cudaMemcpyDeviceToHost),
          "trace d2h");
+  });
+}
+
+int dopf_cuda_timeline(const dopf_cuda_ctx* c, uint64_t* out, int64_t cap) {
+  if (!c || !out || !c->d_timeline) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(const_cast<dopf_cuda_ctx*>(c), [&] {
+    const std::size_t n = std::min<std::size_t>(static_cast<std::size_t>(cap), c->timeline_len);
+    ck(cudaMemcpy(out, c->d_timeline, n * 8, cudaMemcpyDeviceToHost), "d2h");
   });
 }
 

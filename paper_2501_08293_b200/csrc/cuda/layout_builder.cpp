@@ -1,5 +1,7 @@
 #include "layout_builder.hpp"
 
+#include "admm_kernels.cuh"
+
 #include <algorithm>
 #include <cstring>
 #include <thread>
@@ -83,8 +85,9 @@ std::size_t block_smem_bytes(const BlockDesc& b, bool ops_in_smem) {
   std::size_t doubles = 0;
   if (ops_in_smem) doubles += static_cast<std::size_t>(b.p_len) + b.a_len;
   doubles += 3ull * b.rows;                     // target, z, v
-  doubles += 9ull * b.cols;                     // x (four buffers), c/rho, inv, lo, hi, c
-  doubles += 2 * (kThreads / 32ull) * kPartials + 16 + 8;  // warp partials x2, decision ring, phase clock
+  doubles += (kXRing + 5ull) * b.cols;          // x ring, c/rho, inv, lo, hi, c
+  doubles += 2 * (kThreads / 32ull) * kPartials + 8 * 4 + 8;  // warp partials x2, decision ring, phase clock
+  doubles += (kLag + 1ull) * (kThreads / 32);   // per-warp infeasibility ring
   doubles += 3ull * b.arows;                    // equality rows: rhs + AMeta (16 B)
   return 8 * doubles + 4ull * b.copy_len + 64;
 }

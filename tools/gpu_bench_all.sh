@@ -10,3 +10,5 @@ timeout 900 python bench.py --config batch123 --steps 3 --warmup 3 > gpurun_out/
 tail -1 gpurun_out/${TAG}_bench_batch123.log | cut -c1-300
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_ref_ieee8500.log 2>&1
 tail -1 gpurun_out/${TAG}_ref_ieee8500.log | cut -c1-200
+timeout 1500 python bench.py --config tiled --tiles 64 --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_tiled.log 2>&1
+tail -1 gpurun_out/${TAG}_bench_tiled.log | cut -c1-300

@@ -44,3 +44,25 @@ for q, name in enumerate(PHASES):
 busy = a[:, [0, 1, 2, 3, 5]].sum(axis=1)
 print(f"  compute (no exch-wait): min {busy.min():.0f} median {np.median(busy):.0f} "
       f"max {busy.max():.0f} (CTA {int(busy.argmax())})")
+
+# cross-CTA timeline (globaltimer, ns) for iterations 100..163
+T = 64
+buf = (N.u64 * (G * T * 3))()
+if lib.dopf_cuda_timeline(s._h, buf, G * T * 3) == 0:
+    tl = np.array(buf[:], dtype=np.float64).reshape(G, T, 3)
+    ok = tl[:, :, 0] > 0
+    if ok.any():
+        t0 = tl[:, :, 0][ok].min()
+        pub = tl[:, :, 0] - t0
+        per = np.diff(pub, axis=1)
+        print(f"timeline: iteration period median {np.median(per):.0f} ns; "
+              f"publish skew across CTAs per iteration: median {np.median(pub.max(0) - pub.min(0)):.0f} ns, "
+              f"max {np.max(pub.max(0) - pub.min(0)):.0f} ns")
+        wait = tl[:, :, 2] - tl[:, :, 1]
+        gap = tl[:, :, 1] - tl[:, :, 0]
+        print(f"  publish -> boundary start: median {np.median(gap):.0f} ns; boundary update: median "
+              f"{np.median(wait):.0f} ns, p90 {np.percentile(wait, 90):.0f}, max {wait.max():.0f}")
+        late = np.argsort(-np.median(pub - pub.min(0), axis=1))[:5]
+        print("  latest publishers (CTA: median lag ns):",
+              ", ".join(f"{g}: {np.median(pub[g] - pub.min(0)):.0f}" for g in late))
+        print("  globaltimer distinct deltas (resolution probe):", np.unique(np.diff(np.sort(tl[0, :, 0])))[:5])
