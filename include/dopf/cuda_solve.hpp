@@ -12,9 +12,9 @@
 //   std::runtime_error      CUDA / device failures (message from dopf_cuda_last_error)
 // iteration_limit is a result status, not an error.
 //
-// The host precompute (admm.cpp:31-88) runs here in C++ on
-// settings.workers threads; the iteration loop runs on the GPU through the
-// C ABI of include/dopf_cuda.h. Linking libdopf_cuda.so in place of the
+// The precompute (admm.cpp:31-88) runs as one batched GPU kernel (bitwise
+// equal to the host restatement); the iteration loop runs on the GPU through
+// the C ABI of include/dopf_cuda.h. Linking libdopf_cuda.so in place of the
 // reference's admm.cpp is the whole integration.
 #pragma once
 
@@ -40,7 +40,9 @@ class Solver {
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
 
-  /// Precomputes (host, `workers` threads) and uploads the device layout.
+  /// Precomputes the operators -- on the GPU (batched kernel, bitwise equal
+  /// to the host restatement), or on the host with -workers threads when
+  /// workers < 0 -- and uploads the device layout.
   void upload(const DecomposedModel& model, int workers = 1);
   /// Runs the loop on the device; record_iterates fills `snapshots` by
   /// re-running the deterministic device loop to every t (test use).

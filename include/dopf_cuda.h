@@ -60,6 +60,15 @@ int dopf_cuda_solve_batch(dopf_cuda_ctx* ctx, const dopf_settings* settings,
                           dopf_result_view* results, int32_t count);
 
 int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
+/* One-time operators on the GPU (reference admm.cpp:31-88, batched over all
+ * subsystems): P (row-major n_s x n_s at p_offsets) and v (N_z) of the model
+ * view's A, b -- bitwise identical to the host precompute (same sequential
+ * Gram / Cholesky / substitution order, no FMA). Code 2 (singular) names the
+ * first failing subsystem in *first_singular. Feed the result to
+ * dopf_model_set_operators (dopf_host.h). */
+int dopf_cuda_precompute(dopf_cuda_ctx* ctx, const dopf_model_view* model, double* P, double* v,
+                         int32_t* first_singular);
+
 /* Solver path for the next uploads: 0 auto (default: shared-memory-resident
  * persistent kernel when the operators fit the CTAs' shared memory, else the
  * HBM-streaming CUDA graph), 1 resident, 2 streaming. */

@@ -83,6 +83,10 @@ int dopf_model_from_arrays(int32_t S, int32_t n, const int32_t* z_offsets, const
                            const double* c, const double* x_lo, const double* x_hi,
                            const int32_t* is_w, dopf_model** out);
 int dopf_model_precompute(dopf_model* m, int32_t workers);
+/* Adopt operators computed elsewhere (dopf_cuda_precompute): P (row-major
+ * n_s x n_s per subsystem, p_offsets order) and v (N_z); copy counts and the
+ * CSR scatter are built here exactly as dopf_model_precompute does. */
+int dopf_model_set_operators(dopf_model* m, const double* P, const double* v);
 int dopf_model_view_get(const dopf_model* m, dopf_model_view* out);
 int dopf_model_component_id(const dopf_model* m, int32_t s, char* buf, size_t cap);
 int dopf_model_rows_before_reduction(const dopf_model* m, int32_t* out /* S */);

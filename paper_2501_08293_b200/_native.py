@@ -104,6 +104,7 @@ def host() -> C.CDLL:
     _sig(lib, "dopf_model_from_arrays", C.c_int, i32, i32, P(i32), P(i32), P(i32), P(f64),
          P(f64), P(f64), P(f64), P(f64), P(i32), P(vp))
     _sig(lib, "dopf_model_precompute", C.c_int, vp, i32)
+    _sig(lib, "dopf_model_set_operators", C.c_int, vp, P(f64), P(f64))
     _sig(lib, "dopf_model_view_get", C.c_int, vp, P(ModelView_t))
     _sig(lib, "dopf_model_component_id", C.c_int, vp, i32, C.c_char_p, sz)
     _sig(lib, "dopf_model_rows_before_reduction", C.c_int, vp, P(i32))
@@ -136,6 +137,7 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_kernel_launches", i64, vp)
     _sig(lib, "dopf_cuda_kernels_executed", i64, vp)
     _sig(lib, "dopf_cuda_set_path", C.c_int, vp, i32)
+    _sig(lib, "dopf_cuda_precompute", C.c_int, vp, P(ModelView_t), P(f64), P(f64), P(i32))
     _sig(lib, "dopf_cuda_timeline", C.c_int, vp, P(u64), i64)
     _sig(lib, "dopf_cuda_bytes_per_iteration", f64, vp)
     _sig(lib, "dopf_cuda_last_kernel_seconds", f64, vp)

@@ -25,6 +25,7 @@ ORACLE_BUILD = os.path.join(ORACLE_DIR, "_build")
 HOST_SO = os.path.join(LIB, "libdopf_host.so")
 CUDA_SO = os.path.join(LIB, "libdopf_cuda.so")
 DROPIN_TEST = os.path.join(LIB, "dopf_dropin_test")
+CLI = os.path.join(LIB, "dopf")
 ORACLE_SO = os.path.join(ORACLE_BUILD, "libdopf_oracle.so")
 
 # The system g++ links libstdc++ dynamically; a CXX wrapper that links it
@@ -105,7 +106,19 @@ def build_cuda(verbose: bool = False) -> str:
         _run([NVCC, "-shared", "-o", CUDA_SO, *objs, "-L", LIB, "-ldopf_host",
               "-Xlinker", "-rpath,$ORIGIN", "-lcudart"])
     build_dropin_test()
+    build_cli()
     return CUDA_SO
+
+
+def build_cli() -> str:
+    """`dopf` CLI (solve / validate / inspect), the drop-in of proj/tools/main.cpp."""
+    src = os.path.join(PKG, "csrc", "cli", "main.cpp")
+    hdrs = _headers(os.path.join(ROOT, "include"), os.path.join(ROOT, "include", "dopf"),
+                    os.path.join(PKG, "csrc", "host"))
+    if _newer(CLI, [src, CUDA_SO, HOST_SO] + hdrs):
+        _run([CXX, *CXXFLAGS, src, "-o", CLI, "-L", LIB, "-ldopf_cuda", "-ldopf_host",
+              "-Wl,-rpath,$ORIGIN", "-lpthread"])
+    return CLI
 
 
 def build_dropin_test() -> str:

@@ -13,11 +13,16 @@
 #include "../../../include/dopf_cuda.h"
 #include "admm_kernels.cuh"
 #include "layout_builder.hpp"
+#include "precompute_kernels.cuh"
 #include "stream_kernels.cuh"
 
 using namespace dopf::cuda;
 
 namespace {
+
+struct SingularFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 struct CudaFailure : std::runtime_error {
   cudaError_t code;
@@ -180,6 +185,8 @@ int guarded(dopf_cuda_ctx* ctx, F&& body) {
   } catch (const CudaFailure& e) {
     return fail(ctx, e.code == cudaErrorMemoryAllocation ? DOPF_ERR_OUT_OF_MEMORY : DOPF_ERR_CUDA,
                 e.what());
+  } catch (const SingularFailure& e) {
+    return fail(ctx, DOPF_ERR_SINGULAR, e.what());
   } catch (const std::invalid_argument& e) {
     return fail(ctx, DOPF_ERR_INVALID_ARGUMENT, e.what());
   } catch (const std::bad_alloc&) {
@@ -705,6 +712,65 @@ int dopf_cuda_solve_device(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result
   return guarded(c, [&] {
     if (c->streaming) run_stream(c, s, r, false);
     else run(c, s, r, 1, false);
+  });
+}
+
+int dopf_cuda_precompute(dopf_cuda_ctx* c, const dopf_model_view* m, double* P, double* v,
+                         int32_t* first_singular) {
+  if (!c || !m || !P || !v) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    const int S = m->S;
+    if (first_singular) *first_singular = -1;
+    if (S == 0) return;
+    std::vector<int64_t> so(S);
+    int64_t scratch = 0;
+    for (int s = 0; s < S; ++s) {
+      const int64_t n = m->z_offsets[s + 1] - m->z_offsets[s], mm = m->m_s[s];
+      so[s] = scratch;
+      scratch += 2 * mm * mm + mm * n + mm;
+    }
+    auto dev = [&](const void* h, std::size_t bytes) {
+      void* d = nullptr;
+      ck(cudaMalloc(&d, std::max<std::size_t>(bytes, 16)), "cudaMalloc");
+      if (h && bytes) ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream), "h2d");
+      return d;
+    };
+    std::vector<void*> owned;
+    auto keep = [&](void* d) { owned.push_back(d); return d; };
+    try {
+      PrecomputeParams p{};
+      p.S = S;
+      p.z_offsets = static_cast<int32_t*>(keep(dev(m->z_offsets, (S + 1) * sizeof(int32_t))));
+      p.m_s = static_cast<int32_t*>(keep(dev(m->m_s, S * sizeof(int32_t))));
+      p.a_offsets = static_cast<int64_t*>(keep(dev(m->a_offsets, (S + 1) * sizeof(int64_t))));
+      p.A = static_cast<double*>(keep(dev(m->A, m->a_offsets[S] * sizeof(double))));
+      p.b_offsets = static_cast<int32_t*>(keep(dev(m->b_offsets, (S + 1) * sizeof(int32_t))));
+      p.b = static_cast<double*>(keep(dev(m->b, m->b_offsets[S] * sizeof(double))));
+      p.p_offsets = static_cast<int64_t*>(keep(dev(m->p_offsets, (S + 1) * sizeof(int64_t))));
+      p.scratch_offsets = static_cast<int64_t*>(keep(dev(so.data(), S * sizeof(int64_t))));
+      p.scratch = static_cast<double*>(keep(dev(nullptr, scratch * sizeof(double))));
+      p.P = static_cast<double*>(keep(dev(nullptr, m->p_offsets[S] * sizeof(double))));
+      p.v = static_cast<double*>(keep(dev(nullptr, m->N_z * sizeof(double))));
+      p.singular = static_cast<int32_t*>(keep(dev(nullptr, S * sizeof(int32_t))));
+      ck(launch_precompute(p, c->stream), "precompute launch");
+      std::vector<int32_t> sing(S);
+      ck(cudaMemcpyAsync(P, p.P, m->p_offsets[S] * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      ck(cudaMemcpyAsync(v, p.v, m->N_z * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      ck(cudaMemcpyAsync(sing.data(), p.singular, S * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      ck(cudaStreamSynchronize(c->stream), "precompute");
+      ++c->kernels;
+      for (void* d : owned) cudaFree(d);
+      owned.clear();
+      for (int s = 0; s < S; ++s)
+        if (sing[s]) {
+          if (first_singular) *first_singular = s;
+          throw SingularFailure("numerically singular subsystem #" + std::to_string(s));
+        }
+    } catch (...) {
+      for (void* d : owned) cudaFree(d);
+      throw;
+    }
   });
 }
 

@@ -93,8 +93,21 @@ Solver::~Solver() {
 
 void Solver::upload(const DecomposedModel& model, int workers) {
   const auto t0 = std::chrono::steady_clock::now();
-  WorkerPool pool(workers < 1 ? 1 : workers);
-  impl_->pre = precompute(model, &pool);
+  if (workers < 0) {  // host precompute (restatement shared with the CPU oracle)
+    WorkerPool pool(-workers);
+    impl_->pre = precompute(model, &pool);
+  } else {
+    // one-time operators on the GPU: the batched kernel, bitwise equal to the
+    // host precompute (precompute_kernels.cu)
+    impl_->flat.build(model, nullptr);
+    const dopf_model_view bare = impl_->flat.view(model, nullptr);
+    std::vector<double> P(static_cast<std::size_t>(impl_->flat.p_offsets.back())), v(model.total_local_vars());
+    int32_t first = -1;
+    const int rc = dopf_cuda_precompute(impl_->ctx, &bare, P.data(), v.data(), &first);
+    if (rc == DOPF_ERR_SINGULAR && first >= 0) throw SingularSubsystemError(model.subsystems[first].component_id);
+    impl_->check(rc);
+    impl_->pre = precompute_from(model, P.data(), v.data());
+  }
   impl_->precompute_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   impl_->flat.build(model, &impl_->pre);
   const dopf_model_view view = impl_->flat.view(model, &impl_->pre);

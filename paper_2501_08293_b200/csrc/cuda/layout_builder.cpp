@@ -175,6 +175,29 @@ InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions&
     auto& ord = order[g];
     ord = parts[g];
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return ns_of(m, a) > ns_of(m, b); });
+    // Balance the per-thread row work across warps: thread slot k holds rows
+    // [k cw, (k+1) cw). Widest-first order would give the first warps the
+    // widest row of every slot; reversing the subsystem order inside odd
+    // slots pairs wide rows of one slot with narrow rows of the next.
+    {
+      const int cwb = opt.threads - 32;
+      std::vector<int> out;
+      std::vector<int> seg;
+      int rows_done = 0, k = 0;
+      for (int s : ord) {
+        seg.push_back(s);
+        rows_done += ns_of(m, s);
+        if (rows_done >= (k + 1) * cwb) {
+          if (k & 1) std::reverse(seg.begin(), seg.end());
+          out.insert(out.end(), seg.begin(), seg.end());
+          seg.clear();
+          ++k;
+        }
+      }
+      if (k & 1) std::reverse(seg.begin(), seg.end());
+      out.insert(out.end(), seg.begin(), seg.end());
+      ord.swap(out);
+    }
     block_row0[g] = next_row;
     for (int s : ord)
       for (int i = 0; i < ns_of(m, s); ++i) dev_of_ref[m.z_offsets[s] + i] = next_row++;

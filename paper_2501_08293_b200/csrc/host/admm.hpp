@@ -52,6 +52,10 @@ class SingularSubsystemError : public std::runtime_error {
 /// the CSR scatter (reference admm.cpp:31-88).
 Precomputed precompute(const DecomposedModel& model, WorkerPool* pool = nullptr);
 
+/// The same Precomputed from operators computed elsewhere (the batched GPU
+/// precompute): flat P (row-major n_s x n_s, subsystem order) and v (N_z).
+Precomputed precompute_from(const DecomposedModel& model, const double* P, const double* v);
+
 /// Initial iterate rule (reference admm.cpp:92-116): 1.0 for squared-voltage
 /// columns, the bound midpoint when both bounds are finite, else 0.
 double initial_value(const DecomposedModel& model, int global_col);

@@ -103,21 +103,11 @@ bool project_one(const Subsystem& sub, PrecomputedSub& ps) {
 
 }  // namespace
 
-Precomputed precompute(const DecomposedModel& model, WorkerPool* pool) {
-  const int S = model.subsystem_count();
-  Precomputed pre;
-  pre.subs.resize(S);
-  std::vector<char> singular(S, 0);
-  auto one = [&](int s) {
-    if (!project_one(model.subsystems[s], pre.subs[s])) singular[s] = 1;
-  };
-  if (pool && pool->worker_count() > 1)
-    pool->run(S, one);
-  else
-    for (int s = 0; s < S; ++s) one(s);
-  for (int s = 0; s < S; ++s)
-    if (singular[s]) throw SingularSubsystemError(model.subsystems[s].component_id);
+namespace {
 
+// inverse copy counts and the CSR scatter, ascending s (admm.cpp:75-86)
+void build_scatter(const DecomposedModel& model, Precomputed& pre) {
+  const int S = model.subsystem_count();
   const int n = model.global_cols;
   pre.inv_copy_counts.resize(n);
   for (int i = 0; i < n; ++i) {
@@ -136,6 +126,42 @@ Precomputed precompute(const DecomposedModel& model, WorkerPool* pool) {
     for (int j = 0; j < sub.col_count(); ++j)
       pre.copy_index[fill[sub.local_to_global[j]]++] = model.z_offsets[s] + j;
   }
+}
+
+}  // namespace
+
+Precomputed precompute(const DecomposedModel& model, WorkerPool* pool) {
+  const int S = model.subsystem_count();
+  Precomputed pre;
+  pre.subs.resize(S);
+  std::vector<char> singular(S, 0);
+  auto one = [&](int s) {
+    if (!project_one(model.subsystems[s], pre.subs[s])) singular[s] = 1;
+  };
+  if (pool && pool->worker_count() > 1)
+    pool->run(S, one);
+  else
+    for (int s = 0; s < S; ++s) one(s);
+  for (int s = 0; s < S; ++s)
+    if (singular[s]) throw SingularSubsystemError(model.subsystems[s].component_id);
+  build_scatter(model, pre);
+  return pre;
+}
+
+Precomputed precompute_from(const DecomposedModel& model, const double* P, const double* v) {
+  const int S = model.subsystem_count();
+  Precomputed pre;
+  pre.subs.resize(S);
+  std::size_t at = 0;
+  for (int s = 0; s < S; ++s) {
+    const int n = model.subsystems[s].col_count();
+    PrecomputedSub& ps = pre.subs[s];
+    ps.kernel_projector = Dense(n, n);
+    std::copy(P + at, P + at + static_cast<std::size_t>(n) * n, ps.kernel_projector.a.begin());
+    at += static_cast<std::size_t>(n) * n;
+    ps.min_norm_solution.assign(v + model.z_offsets[s], v + model.z_offsets[s] + n);
+  }
+  build_scatter(model, pre);
   return pre;
 }
 

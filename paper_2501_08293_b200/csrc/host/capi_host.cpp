@@ -304,6 +304,15 @@ int dopf_model_precompute(dopf_model* m, int32_t workers) {
   });
 }
 
+int dopf_model_set_operators(dopf_model* m, const double* P, const double* v) {
+  if (!m || !P || !v) return fail(DOPF_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    m->pre = dopf::precompute_from(m->model, P, v);
+    m->has_pre = true;
+    m->flat_ready = false;
+  });
+}
+
 int dopf_model_view_get(const dopf_model* cm, dopf_model_view* out) {
   if (!cm || !out) return fail(DOPF_ERR_INVALID_ARGUMENT, "null argument");
   auto* m = const_cast<dopf_model*>(cm);

@@ -308,6 +308,22 @@ class DecomposedModel:
         self._view = None
         return self
 
+    def precompute_gpu(self, solver: "CudaSolver") -> "DecomposedModel":
+        """One-time operators on the GPU (batched kernel, bitwise equal to precompute())."""
+        v = self.view()
+        S = v.S
+        zo = np.ctypeslib.as_array(v.z_offsets, shape=(S + 1,)) if S else np.zeros(1, dtype=np.int32)
+        ns = np.diff(zo).astype(np.int64)
+        P = np.zeros(int((ns * ns).sum()))
+        vv = np.zeros(int(v.N_z))
+        first = N.i32(-1)
+        solver._err(solver._lib.dopf_cuda_precompute(solver._h, C.byref(v), P.ctypes.data_as(C.POINTER(C.c_double)),
+                                                     vv.ctypes.data_as(C.POINTER(C.c_double)), C.byref(first)))
+        _check(N.host().dopf_model_set_operators(self._h, P.ctypes.data_as(C.POINTER(C.c_double)),
+                                                 vv.ctypes.data_as(C.POINTER(C.c_double))))
+        self._view = None
+        return self
+
     def reduce(self, tol: float = 1e-9, workers: int = 1) -> None:
         _check(N.host().dopf_model_reduce(self._h, tol, workers))
         self._view = None

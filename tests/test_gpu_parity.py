@@ -243,3 +243,28 @@ def test_tiled_feeder_auto_streams_bitwise():
     gpu = s.solve(settings)
     ref = O.solve(model, dopf.Settings(max_iter=300, workers=8))
     assert_same(gpu, ref, bitwise=True)
+
+
+# ------------------------------------------------------------ GPU precompute (row f2)
+
+
+@pytest.mark.parametrize("source", FIXTURES + ["ieee123", "ieee8500"])
+def test_gpu_precompute_bitwise_equals_host(solver, source):
+    if source in FIXTURES:
+        _, _, host = dopf.load_model(fixture_path(source))
+        _, _, gpu = dopf.load_model(fixture_path(source))
+    else:
+        f = dopf.synthetic_feeder(source, 123 if source == "ieee123" else 8500)
+        _, _, host = dopf.load_model(f, workers=4)
+        _, _, gpu = dopf.load_model(f, workers=4)
+    host.precompute(4)
+    gpu.precompute_gpu(solver)
+    for name in ("P", "v", "inv_copy", "csr_ptr", "csr_copy"):
+        assert np.array_equal(host.arr(name), gpu.arr(name)), name
+
+
+def test_gpu_precompute_flags_singular_subsystem(solver):
+    m = dopf.single_sub_model([[1.0, 0, 0], [1.0, 0, 0]], [1.0, 1.0], np.zeros(3), [-np.inf] * 3,
+                              [np.inf] * 3)
+    with pytest.raises(dopf.SingularSubsystemError):
+        m.precompute_gpu(solver)
