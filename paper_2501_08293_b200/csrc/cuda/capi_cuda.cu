@@ -57,7 +57,7 @@ struct dopf_cuda_ctx {
     void* p = nullptr;
     std::size_t cap = 0;  // bytes
   };
-  std::vector<Buf> bufs = std::vector<Buf>(64);
+  std::vector<Buf> bufs = std::vector<Buf>(96);
   BlockDesc* d_blocks = nullptr;
   InstDesc* d_inst = nullptr;
   double *d_P = nullptr, *d_A = nullptr, *d_v = nullptr, *d_z0 = nullptr;
@@ -91,7 +91,8 @@ struct dopf_cuda_ctx {
     double *cost = nullptr, *inv = nullptr, *lo = nullptr, *hi = nullptr;
     uint8_t* owner = nullptr;
     double *x = nullptr, *z = nullptr, *lam = nullptr, *u = nullptr, *u_remote = nullptr;
-    double *part = nullptr, *objp = nullptr, *partials = nullptr;
+    double *part = nullptr, *objp = nullptr, *partials = nullptr, *part2 = nullptr;
+    unsigned* final_count = nullptr;
     StreamCtl* ctl = nullptr;
     int32_t* export_rows = nullptr;
     double *send = nullptr, *ranks = nullptr;
@@ -341,7 +342,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.prof = c->profiling ? c->d_prof : nullptr;
   if (c->profiling) {
     const std::size_t need = static_cast<std::size_t>(c->num_blocks) * kTimelineIters * 3;
-    c->d_timeline = c->scratch<unsigned long long>(63, need);
+    c->d_timeline = c->scratch<unsigned long long>(95, need);
     ck(cudaMemsetAsync(c->d_timeline, 0, need * 8, c->stream), "memset");
     c->timeline_len = need;
   }
@@ -508,6 +509,8 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.objp = c->scratch<double>(k++, (L.cols + kStreamRows - 1) / kStreamRows);
   d.partials = c->scratch<double>(k++, 8);
   d.ctl = c->scratch<StreamCtl>(k++, 1);
+  d.part2 = c->scratch<double>(k++, 128 * 8);
+  d.final_count = c->scratch<unsigned>(k++, 1);
   d.export_rows = c->put(k++, L.export_rows);
   d.send = c->scratch<double>(k++, std::max(1, L.max_export));
   d.ranks = c->scratch<double>(k++, static_cast<std::size_t>(L.nparts) * 8);
@@ -542,6 +545,8 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   p.u_remote = d.u_remote;
   p.part = d.part;
   p.objp = d.objp;
+  p.part2 = d.part2;
+  p.final_count = d.final_count;
   p.trace = trace;
   p.ctl = d.ctl;
   p.partials_out = nullptr;
@@ -566,6 +571,7 @@ void stream_reset(dopf_cuda_ctx* c) {
   ck(cudaMemcpyAsync(d.u, d.z0, L.rows * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "u0");
   ck(cudaMemsetAsync(d.lam, 0, L.rows * sizeof(double), c->stream), "lambda0");
   ck(cudaMemsetAsync(d.ctl, 0, sizeof(StreamCtl), c->stream), "ctl");
+  ck(cudaMemsetAsync(d.final_count, 0, sizeof(unsigned), c->stream), "counter");
 }
 
 void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, bool copy_vectors) {

@@ -20,6 +20,8 @@
 // reductions are trees (stop test and trace only).
 #include "stream_kernels.cuh"
 
+#include <cstdlib>
+
 namespace dopf::cuda {
 
 namespace {
@@ -104,7 +106,8 @@ __global__ void __launch_bounds__(kStreamRows) k_global(const StreamParams p) {
   if (threadIdx.x == 0) p.objp[blockIdx.x] = o[0];
 }
 
-__global__ void __launch_bounds__(kStreamRows, 3) k_local(const StreamParams p) {
+template <int kMinBlocks, bool kPrefetch>
+__global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamParams p) {
   __shared__ double tgt[kStreamRows];
   __shared__ double zsh[kStreamRows];
   __shared__ double sh[6 * (kStreamRows / 32)];
@@ -115,21 +118,45 @@ __global__ void __launch_bounds__(kStreamRows, 3) k_local(const StreamParams p) 
   const bool on = r < ch.rows;
   const int d = ch.row0 + r;
   StreamRow rm{0, 0, 0, 0};
-  double bx = 0.0, lamv = 0.0;
+  double bx = 0.0, lamv = 0.0, vd = 0.0, zprev = 0.0;
+  const double* pr = p.P + p.pslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
+  double pv[8];  // first chunk of this row of P: in flight across the target barrier
+  double av[8];  // ... and of this thread's equality row of A
+  StreamARow am{0, 0};
+  double abv = 0.0;
+  const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
+  if (kPrefetch && r < ch.arows) {
+    am = p.ameta[blockIdx.x * kStreamRows + r];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) av[e] = e < am.n ? __ldcs(ar + 32 * e) : 0.0;
+    abv = p.ab[ch.arow0 + r];
+  }
   if (on) {
     rm = p.rmeta[d];
+    if (kPrefetch) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) pv[e] = e < rm.n ? __ldcs(pr + 32 * e) : 0.0;
+    }
     bx = p.x[rm.xcol];
     lamv = p.lam[d];
+    if (kPrefetch) {
+      vd = p.v[d];
+      zprev = p.z[d];
+    }
     tgt[r] = bx + lamv / rho;  // admm.cpp:136
   }
   __syncthreads();
   double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (on) {
-    const double* pr = p.P + p.pslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
     const double* tb = tgt + rm.base;
     double acc = 0.0;
-    for (int j0 = 0; j0 < rm.n; j0 += 8) {
-      double pv[8], tv[8];
+    if (kPrefetch) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (e < rm.n) acc = acc + pv[e] * tb[e];
+    }
+    for (int j0 = kPrefetch ? 8 : 0; j0 < rm.n; j0 += 8) {
+      double tv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         pv[e] = 0.0;
@@ -143,8 +170,11 @@ __global__ void __launch_bounds__(kStreamRows, 3) k_local(const StreamParams p) 
       for (int e = 0; e < 8; ++e)
         if (j0 + e < rm.n) acc = acc + pv[e] * tv[e];
     }
-    const double z = acc + p.v[d];
-    const double zprev = p.z[d];
+    if (!kPrefetch) {
+      vd = p.v[d];
+      zprev = p.z[d];
+    }
+    const double z = acc + vd;
     const double dd = bx - z;
     const double ln = lamv + rho * dd;  // admm.cpp:142
     p.z[d] = z;
@@ -160,19 +190,22 @@ __global__ void __launch_bounds__(kStreamRows, 3) k_local(const StreamParams p) 
   }
   __syncthreads();
   if (r < ch.arows) {
-    const StreamARow am = p.ameta[blockIdx.x * kStreamRows + r];
-    const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
+    if (!kPrefetch) {
+      am = p.ameta[blockIdx.x * kStreamRows + r];
+      abv = p.ab[ch.arow0 + r];
+    }
     const double* zb = zsh + am.base;
     double acc = 0.0;
     for (int j0 = 0; j0 < am.n; j0 += 8) {
-      double av[8];
+      if (!kPrefetch || j0 > 0) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? __ldcs(ar + 32 * (j0 + e)) : 0.0;
+        for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? __ldcs(ar + 32 * (j0 + e)) : 0.0;
+      }
 #pragma unroll
       for (int e = 0; e < 8; ++e)
         if (j0 + e < am.n) acc = acc + av[e] * zb[j0 + e];
     }
-    v[5] = fabs(acc - p.ab[ch.arow0 + r]);
+    v[5] = fabs(acc - abv);
   }
   block_reduce<6, kStreamRows>(v, sh, 5);
   if (threadIdx.x == 0) {
@@ -182,47 +215,56 @@ __global__ void __launch_bounds__(kStreamRows, 3) k_local(const StreamParams p) 
   }
 }
 
-constexpr int kFinalThreads = 1024;
+constexpr int kFinalThreads = 256;
+constexpr int kFinalBlocks = 128;
 
+// Two-level fixed-order reduction of the chunk partials and objective
+// partials: CTA g folds a contiguous range into level-2 slot g; the last CTA
+// to finish (device-scope counter) folds the 128 slots in order and decides.
 __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
   __shared__ double sh[7 * (kFinalThreads / 32)];
+  __shared__ bool last;
   if (p.ctl->done) return;
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gap, step, bx2, z2, lam2, maxinf, objective
-  // loads of 4 strided partials in flight per step, summed in the same fixed order
-  constexpr int U = 4;
-  for (int k0 = threadIdx.x; k0 < p.nchunks; k0 += U * kFinalThreads) {
-    double q[U][6];
+  const int g = blockIdx.x;
+  const int c0 = static_cast<int>(static_cast<int64_t>(p.nchunks) * g / kFinalBlocks);
+  const int c1 = static_cast<int>(static_cast<int64_t>(p.nchunks) * (g + 1) / kFinalBlocks);
+  for (int k = c0 + threadIdx.x; k < c1; k += kFinalThreads) {
+    const double* q = p.part + static_cast<int64_t>(k) * 8;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * kFinalThreads;
-#pragma unroll
-      for (int i = 0; i < 6; ++i) q[u][i] = k < p.nchunks ? __ldcg(p.part + static_cast<int64_t>(k) * 8 + i) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int i = 0; i < 5; ++i) v[i] = v[i] + q[u][i];
-      v[5] = sel_max(v[5], q[u][5]);
-    }
+    for (int i = 0; i < 5; ++i) v[i] = v[i] + __ldcg(q + i);
+    v[5] = sel_max(v[5], __ldcg(q + 5));
   }
-  for (int k0 = threadIdx.x; k0 < p.col_blocks; k0 += U * kFinalThreads) {
-    double q[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + u * kFinalThreads;
-      q[u] = k < p.col_blocks ? __ldcg(p.objp + k) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[6] = v[6] + q[u];
-  }
+  const int o0 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * g / kFinalBlocks);
+  const int o1 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * (g + 1) / kFinalBlocks);
+  for (int k = o0 + threadIdx.x; k < o1; k += kFinalThreads) v[6] = v[6] + __ldcg(p.objp + k);
   block_reduce<7, kFinalThreads>(v, sh, 5);
   if (threadIdx.x == 0) {
+    double* slot = p.part2 + g * 8;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) slot[q] = v[q];
+    __threadfence();
+    const unsigned done_blocks = atomicAdd(p.final_count, 1u);
+    last = done_blocks == kFinalBlocks - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double w[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (threadIdx.x < kFinalBlocks) {
+    const double* q = p.part2 + threadIdx.x * 8;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) w[i] = __ldcg(q + i);
+  }
+  block_reduce<7, kFinalThreads>(w, sh, 5);
+  if (threadIdx.x == 0) {
+    *p.final_count = 0;  // ready for the next iteration (kernel boundary orders it)
     if (p.partials_out) {  // partitioned: the host combines ranks, then calls k_decide
 #pragma unroll
-      for (int q = 0; q < 7; ++q) p.partials_out[q] = v[q];
+      for (int q = 0; q < 7; ++q) p.partials_out[q] = w[q];
       return;
     }
-    finalize_iteration(p, v);
+    finalize_iteration(p, w);
   }
 }
 
@@ -247,19 +289,30 @@ __global__ void k_decide(const StreamParams p, const double* ranks, int nranks) 
 
 }  // namespace
 
+using LocalKernel = void (*)(const StreamParams);
+
+LocalKernel local_kernel() {
+  // DOPF_KLOCAL: 0 = 3 CTAs/SM without the P prefetch, 1 = 2 CTAs/SM with it
+  static const LocalKernel k = [] {
+    const char* e = std::getenv("DOPF_KLOCAL");
+    return (e && e[0] == '1') ? &k_local<2, true> : &k_local<3, false>;
+  }();
+  return k;
+}
+
 void stream_launch_iteration(const StreamParams& p, cudaStream_t s) {
   k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
-  k_local<<<p.nchunks, kStreamRows, 0, s>>>(p);
-  k_final<<<1, kFinalThreads, 0, s>>>(p);
+  local_kernel()<<<p.nchunks, kStreamRows, 0, s>>>(p);
+  k_final<<<kFinalBlocks, kFinalThreads, 0, s>>>(p);
 }
 
 void stream_launch_global(const StreamParams& p, cudaStream_t s) {
   k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
 }
 void stream_launch_local(const StreamParams& p, cudaStream_t s) {
-  k_local<<<p.nchunks, kStreamRows, 0, s>>>(p);
+  local_kernel()<<<p.nchunks, kStreamRows, 0, s>>>(p);
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
-  k_final<<<1, kFinalThreads, 0, s>>>(p);
+  k_final<<<kFinalBlocks, kFinalThreads, 0, s>>>(p);
 }
 void stream_launch_pack(const StreamParams& p, cudaStream_t s) {
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
@@ -294,11 +347,11 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   kg.blockDim = dim3(kStreamRows);
   kg.kernelParams = args;
   kl = kg;
-  kl.func = reinterpret_cast<void*>(k_local);
+  kl.func = reinterpret_cast<void*>(local_kernel());
   kl.gridDim = dim3(p.nchunks);
   kf = kg;
   kf.func = reinterpret_cast<void*>(k_final);
-  kf.gridDim = dim3(1);
+  kf.gridDim = dim3(kFinalBlocks);
   kf.blockDim = dim3(kFinalThreads);
   cudaGraphNode_t ng, nl, nf;
   if ((e = cudaGraphAddKernelNode(&ng, body, nullptr, 0, &kg)) != cudaSuccess) return e;

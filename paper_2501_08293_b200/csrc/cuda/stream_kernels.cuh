@@ -42,6 +42,8 @@ struct StreamParams {
   const double* u_remote;  // partitioned: gathered copies of other ranks
   double* part;          // [nchunks][8]
   double* objp;          // [col_blocks]
+  double* part2;         // [128][8] level-2 partials (k_final)
+  unsigned* final_count; // k_final's last-block counter (zero between iterations)
   double* trace;         // [max_iter][6] or null
   StreamCtl* ctl;
   double* partials_out;  // partitioned: this rank's 7 combined partials (null: decide here)

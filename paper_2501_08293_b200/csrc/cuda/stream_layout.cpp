@@ -1,6 +1,8 @@
 #include "stream_layout.hpp"
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
 #include <stdexcept>
 
 #include "layout_builder.hpp"
@@ -38,15 +40,30 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
   std::vector<Src> prow, arow;
   int32_t row = 0;
   std::size_t k = 0;
+  std::vector<int> members;
   while (k < order.size()) {
     StreamChunk ch{};
     ch.row0 = row;
     ch.arow0 = static_cast<int32_t>(arow.size());
+    // the chunk's subsystems: the next run of the locality walk that fits
     int rows = 0, arows = 0;
+    members.clear();
     while (k < order.size()) {
       const int s = order[k];
       const int n = ns_of(s), ms = m.m_s[s];
       if (rows + n > kStreamRows || arows + ms > kStreamRows) break;
+      members.push_back(s);
+      rows += n;
+      arows += ms;
+      ++k;
+    }
+    // widest first inside the chunk: the 32 rows of a warp slice then have
+    // (nearly) equal n_s, so the sliced-ELL padding -- which still costs
+    // DRAM sectors -- stays small
+    std::stable_sort(members.begin(), members.end(), [&](int a, int b) { return ns_of(a) > ns_of(b); });
+    rows = 0;
+    for (int s : members) {
+      const int n = ns_of(s), ms = m.m_s[s];
       for (int i = 0; i < n; ++i) {
         dev_of_ref[m.z_offsets[s] + i] = row + rows + i;
         prow.push_back(Src{m.p_offsets[s] + static_cast<int64_t>(i) * n, n, rows});
@@ -56,8 +73,6 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
         L.ab.push_back(m.b[m.b_offsets[s] + r]);
       }
       rows += n;
-      arows += ms;
-      ++k;
     }
     ch.rows = rows;
     ch.arows = arows;
@@ -73,15 +88,20 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
   for (int s = 0; s < m.S; ++s)
     for (int k2 = m.z_offsets[s]; k2 < m.z_offsets[s + 1]; ++k2) s_of_ref[k2] = s;
 
-  // columns updated here: every column a local row references, ascending
+  // columns updated here: every column a local row references, ordered by
+  // their first local copy's device row (ties by column) -- the global update
+  // then walks u and the local update gathers x in near-sequential order
   std::vector<int32_t> loc_of_col(m.n, -1);
-  for (int ref = 0; ref < m.N_z; ++ref)
-    if (dev_of_ref[ref] >= 0) loc_of_col[m.l2g[ref]] = 1;
-  for (int c = 0; c < m.n; ++c)
-    if (loc_of_col[c] > 0) {
-      loc_of_col[c] = static_cast<int32_t>(L.gcol.size());
-      L.gcol.push_back(c);
-    }
+  {
+    std::vector<int32_t> first_row(m.n, INT32_MAX);
+    for (int ref = 0; ref < m.N_z; ++ref)
+      if (dev_of_ref[ref] >= 0) first_row[m.l2g[ref]] = std::min(first_row[m.l2g[ref]], dev_of_ref[ref]);
+    for (int c = 0; c < m.n; ++c)
+      if (first_row[c] != INT32_MAX) L.gcol.push_back(c);
+    std::stable_sort(L.gcol.begin(), L.gcol.end(),
+                     [&](int32_t a, int32_t b) { return first_row[a] < first_row[b]; });
+    for (std::size_t q = 0; q < L.gcol.size(); ++q) loc_of_col[L.gcol[q]] = static_cast<int32_t>(q);
+  }
   for (int ref = 0; ref < m.N_z; ++ref) {
     const int32_t d = dev_of_ref[ref];
     if (d < 0) continue;
