@@ -178,7 +178,7 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 template <int K, bool kSmemOps>
-__global__ void __launch_bounds__(kThreads, 1) admm_persistent(const KernelParams p) {
+__global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(const KernelParams p) {
   extern __shared__ __align__(16) double smem[];
   const BlockDesc bd = p.blocks[blockIdx.x];
   const InstDesc id = p.inst[bd.instance];

@@ -40,6 +40,7 @@ struct dopf_cuda_ctx {
   int device = 0;
   int sm_count = 0;
   int smem_optin = 0;
+  int smem_per_sm = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
@@ -239,6 +240,14 @@ void upload_layout(dopf_cuda_ctx* c) {
   ck(cudaStreamSynchronize(c->stream), "upload sync");
 }
 
+// CTAs of the resident kernel per SM (register budget: kThreads x 128 regs
+// each); DOPF_CTAS_PER_SM overrides for experiments
+int ctas_per_sm() {
+  const char* e = std::getenv("DOPF_CTAS_PER_SM");
+  if (e && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
+  return kThreads <= 256 ? 2 : 1;
+}
+
 void choose_sync(dopf_cuda_ctx* c) {
   const int G = c->L.blocks_per_instance;
   c->num_blocks = static_cast<int>(c->L.blocks.size());
@@ -251,7 +260,7 @@ void choose_sync(dopf_cuda_ctx* c) {
   } else {
     if (c->L.inst.size() != 1)
       throw std::invalid_argument("batched instances must fit a cluster of <= 8 CTAs");
-    if (G > c->sm_count) throw std::invalid_argument("instance needs more CTAs than SMs");
+    if (G > c->sm_count * ctas_per_sm()) throw std::invalid_argument("instance needs more CTAs than fit the GPU");
     c->mode = SyncMode::grid;
     c->cluster = 1;
   }
@@ -259,8 +268,10 @@ void choose_sync(dopf_cuda_ctx* c) {
 
 LayoutOptions options_for(const dopf_cuda_ctx* c) {
   LayoutOptions o;
-  o.smem_limit = static_cast<std::size_t>(c->smem_optin);
-  o.max_blocks = c->sm_count;
+  const int cps = ctas_per_sm();
+  o.smem_limit = cps == 1 ? static_cast<std::size_t>(c->smem_optin)
+                          : static_cast<std::size_t>(c->smem_per_sm) / cps - 1024;  // 1 KB reserved per CTA
+  o.max_blocks = c->sm_count * cps;
   return o;
 }
 
@@ -447,6 +458,7 @@ int dopf_cuda_create(int device, dopf_cuda_ctx** out) {
     c->device = device;
     ck(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
     c->smem_optin = max_dynamic_smem(device);
+    ck(cudaDeviceGetAttribute(&c->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device), "attr");
     ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "stream");
     c->stream = c->own_stream;
     ck(cudaEventCreate(&c->ev0), "event");
