@@ -13,6 +13,7 @@
 #include "../../../include/dopf_cuda.h"
 #include "admm_kernels.cuh"
 #include "layout_builder.hpp"
+#include "layout_gather.cuh"
 #include "precompute_kernels.cuh"
 #include "stream_kernels.cuh"
 
@@ -58,7 +59,7 @@ struct dopf_cuda_ctx {
     void* p = nullptr;
     std::size_t cap = 0;  // bytes
   };
-  std::vector<Buf> bufs = std::vector<Buf>(96);
+  std::vector<Buf> bufs = std::vector<Buf>(128);
   BlockDesc* d_blocks = nullptr;
   InstDesc* d_inst = nullptr;
   double *d_P = nullptr, *d_A = nullptr, *d_v = nullptr, *d_z0 = nullptr;
@@ -108,6 +109,15 @@ struct dopf_cuda_ctx {
   double graph_key[3] = {0, 0, 0};  // rho, eps, max_iter the graph was built for
   const double* graph_trace = nullptr;
   int64_t kernels = 0;       // kernels launched (graph iterations x 3 + persistent launches)
+  // re-upload fast path: the plan whose index maps / structure sit on the device
+  const InstancePlan* dev_plan = nullptr;
+  int64_t* d_psrc = nullptr;
+  int64_t* d_asrc = nullptr;
+  int64_t* d_absrc = nullptr;
+  int32_t* d_refdev = nullptr;
+  int32_t* d_gcol = nullptr;
+  double *d_rawP = nullptr, *d_rawA = nullptr, *d_rawb = nullptr, *d_rawv = nullptr, *d_rawz0 = nullptr,
+         *d_rawc = nullptr, *d_rawinv = nullptr, *d_rawlo = nullptr, *d_rawhi = nullptr;
   // pinned staging for results copied back to the host
   void* h_stage = nullptr;
   std::size_t h_stage_cap = 0;
@@ -353,7 +363,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.prof = c->profiling ? c->d_prof : nullptr;
   if (c->profiling) {
     const std::size_t need = static_cast<std::size_t>(c->num_blocks) * kTimelineIters * 3;
-    c->d_timeline = c->scratch<unsigned long long>(95, need);
+    c->d_timeline = c->scratch<unsigned long long>(127, need);
     ck(cudaMemsetAsync(c->d_timeline, 0, need * 8, c->stream), "memset");
     c->timeline_len = need;
   }
@@ -666,6 +676,78 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   r->time_upload = std::chrono::duration<double>(t_dn0 - t_up0).count() - c->last_kernel_s;
 }
 
+// index maps of the plan (instance 0 layout) -> device, once per plan
+void upload_plan_maps(dopf_cuda_ctx* c, const dopf_model_view& m) {
+  const InstancePlan& P = *c->plan;
+  int k = 64;  // slots 64.. (resident 0..31, streaming 32..62)
+  c->d_psrc = c->put(k++, P.p_src);
+  c->d_asrc = c->put(k++, P.a_src);
+  c->d_absrc = c->put(k++, P.ab_src);
+  c->d_refdev = c->put(k++, P.ref_of_dev);
+  std::vector<int32_t> gcol(P.cmeta.size());
+  for (std::size_t q = 0; q < gcol.size(); ++q) gcol[q] = P.cmeta[q].gcol;
+  c->d_gcol = c->put(k++, gcol);
+  c->d_rawP = c->scratch<double>(k++, static_cast<std::size_t>(m.p_offsets[m.S]));
+  c->d_rawA = c->scratch<double>(k++, static_cast<std::size_t>(m.a_offsets[m.S]));
+  c->d_rawb = c->scratch<double>(k++, static_cast<std::size_t>(m.b_offsets[m.S]));
+  c->d_rawv = c->scratch<double>(k++, m.N_z);
+  c->d_rawz0 = c->scratch<double>(k++, m.N_z);
+  c->d_rawc = c->scratch<double>(k++, m.n);
+  c->d_rawinv = c->scratch<double>(k++, m.n);
+  c->d_rawlo = c->scratch<double>(k++, m.n);
+  c->d_rawhi = c->scratch<double>(k++, m.n);
+  ck(cudaStreamSynchronize(c->stream), "plan maps");
+  c->dev_plan = c->plan.get();
+}
+
+void upload_values(dopf_cuda_ctx* c, const dopf_model_view& m) {
+  auto h2d = [&](double* d, const double* h, std::size_t n) {
+    if (n) ck(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "upload");
+  };
+  h2d(c->d_rawP, m.P, static_cast<std::size_t>(m.p_offsets[m.S]));
+  h2d(c->d_rawA, m.A, static_cast<std::size_t>(m.a_offsets[m.S]));
+  h2d(c->d_rawb, m.b, static_cast<std::size_t>(m.b_offsets[m.S]));
+  h2d(c->d_rawv, m.v, m.N_z);
+  h2d(c->d_rawz0, m.z0, m.N_z);
+  h2d(c->d_rawc, m.c, m.n);
+  h2d(c->d_rawinv, m.inv_copy, m.n);
+  h2d(c->d_rawlo, m.x_lo, m.n);
+  h2d(c->d_rawhi, m.x_hi, m.n);
+  const InstancePlan& P = *c->plan;
+  GatherParams g{};
+  g.np = static_cast<int64_t>(P.p_src.size());
+  g.na = static_cast<int64_t>(P.a_src.size());
+  g.rows = static_cast<int64_t>(P.ref_of_dev.size());
+  g.cols = static_cast<int64_t>(P.cmeta.size());
+  g.nab = static_cast<int64_t>(P.ab_src.size());
+  g.p_src = c->d_psrc;
+  g.a_src = c->d_asrc;
+  g.ref_of_dev = c->d_refdev;
+  g.gcol = c->d_gcol;
+  g.ab_src = c->d_absrc;
+  g.rawP = c->d_rawP;
+  g.rawA = c->d_rawA;
+  g.rawb = c->d_rawb;
+  g.rawv = c->d_rawv;
+  g.rawz0 = c->d_rawz0;
+  g.rawc = c->d_rawc;
+  g.rawinv = c->d_rawinv;
+  g.rawlo = c->d_rawlo;
+  g.rawhi = c->d_rawhi;
+  g.P = c->d_P;
+  g.A = c->d_A;
+  g.ab = c->d_ab;
+  g.v = c->d_v;
+  g.z0 = c->d_z0;
+  g.cc = c->d_cc;
+  g.cinv = c->d_cinv;
+  g.clo = c->d_clo;
+  g.chi = c->d_chi;
+  ck(launch_gather(g, c->sm_count, c->stream), "gather");
+  ++c->kernels;
+  ck(cudaStreamSynchronize(c->stream), "upload sync");
+}
+
 }  // namespace
 
 int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
@@ -673,7 +755,6 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->uploaded = false;
-    c->L.reset();
     const LayoutOptions opt = options_for(c);
     if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
     c->streaming = c->path_request == 2 || (c->path_request == 0 && needs_streaming(*m, opt));
@@ -681,15 +762,26 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
     c->inst_n = {m->n};
     c->partitioned = false;
     if (c->streaming) {
+      c->dev_plan = nullptr;
+      c->L.reset();
       upload_stream(c, *m);
       c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
       c->uploaded = true;
       return;
     }
-    if (!c->plan || !c->plan->same_structure(*m, opt))
-      c->plan = std::make_shared<InstancePlan>(plan_instance(*m, choose_blocks(*m, opt), opt));
+    const bool same = c->plan && c->plan->same_structure(*m, opt);
+    if (same && c->dev_plan == c->plan.get() && c->L.inst.size() == 1) {
+      // fast path: structure and index maps already on the device; copy the
+      // raw value arrays and scatter them on the GPU (no host repacking)
+      upload_values(c, *m);
+      c->uploaded = true;
+      return;
+    }
+    if (!same) c->plan = std::make_shared<InstancePlan>(plan_instance(*m, choose_blocks(*m, opt), opt));
+    c->L.reset();
     append_instance(c->L, *c->plan, *m);
     finish_upload(c);
+    upload_plan_maps(c, *m);
   });
 }
 
@@ -698,6 +790,7 @@ int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t 
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->uploaded = false;
+    c->dev_plan = nullptr;
     c->streaming = false;
     c->partitioned = false;
     LayoutOptions opt = options_for(c);
@@ -805,6 +898,7 @@ int dopf_cuda_upload_part(dopf_cuda_ctx* c, const dopf_model_view* m, int32_t np
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
     c->uploaded = false;
+    c->dev_plan = nullptr;
     c->L.reset();
     c->streaming = true;
     c->partitioned = true;

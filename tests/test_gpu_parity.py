@@ -268,3 +268,16 @@ def test_gpu_precompute_flags_singular_subsystem(solver):
                               [np.inf] * 3)
     with pytest.raises(dopf.SingularSubsystemError):
         m.precompute_gpu(solver)
+
+
+def test_reupload_same_structure_fast_path_bitwise(solver):
+    """Scenarios share the structure: the second and later uploads copy raw
+    values and scatter them on the GPU (cached plan) -- still bitwise."""
+    from paper_2501_08293_b200 import scenarios
+    models = scenarios.build_scenarios("ieee123", 123, range(3))
+    settings = dopf.Settings()
+    for m in models + models[:1]:
+        solver.upload(m)
+        gpu = solver.solve(settings)
+        ref = O.solve(m, dopf.Settings(workers=8))
+        assert_same(gpu, ref, bitwise=True)
