@@ -403,19 +403,37 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   for (int i = 0; i < count; ++i)
     any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
   // results: a single instance needs only ring buffer iters % kZRing; a
-  // batch copies all of them (instances stop at different iterations)
+  // batch gathers every instance's slot on the device first (instances stop
+  // at different iterations), so one compact copy comes back
   const std::size_t R = static_cast<std::size_t>(L.rows_total);
   const bool one = I == 1;
-  const std::size_t nbuf = one ? 1 : kZRing;
   double *zdev = nullptr, *ldev = nullptr, *xall = nullptr;
   if (copy_vectors && any_vec) {
-    double* st = static_cast<double*>(c->stage((2 * nbuf * R + L.x_total) * sizeof(double)));
+    double* st = static_cast<double*>(c->stage((2 * R + L.x_total) * sizeof(double)));
     zdev = st;
-    ldev = st + nbuf * R;
-    xall = st + 2 * nbuf * R;
-    const std::size_t from = one ? (iters[0] % kZRing) * R : 0;
-    ck(cudaMemcpyAsync(zdev, c->d_z + from, nbuf * R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
-    ck(cudaMemcpyAsync(ldev, c->d_lam + from, nbuf * R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ldev = st + R;
+    xall = st + 2 * R;
+    const double *zsrc = c->d_z + (one ? (iters[0] % kZRing) * R : 0);
+    const double *lsrc = c->d_lam + (one ? (iters[0] % kZRing) * R : 0);
+    if (!one) {
+      std::vector<int32_t> row0(I), rows(I);
+      for (std::size_t i = 0; i < I; ++i) {
+        row0[i] = L.inst[i].row0;
+        rows[i] = L.inst[i].rows;
+      }
+      int32_t* d_meta = c->scratch<int32_t>(120, 2 * I);
+      double* d_out = c->scratch<double>(121, 2 * R);
+      ck(cudaMemcpyAsync(d_meta, row0.data(), I * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream), "h2d");
+      ck(cudaMemcpyAsync(d_meta + I, rows.data(), I * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream), "h2d");
+      ck(launch_final_iterates(c->d_z, c->d_lam, L.rows_total, d_meta, d_meta + I, c->d_iters,
+                               static_cast<int>(I), kZRing, d_out, d_out + R, c->stream),
+         "final iterates");
+      ++c->kernels;
+      zsrc = d_out;
+      lsrc = d_out + R;
+    }
+    ck(cudaMemcpyAsync(zdev, zsrc, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(ldev, lsrc, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaMemcpyAsync(xall, c->d_x, L.x_total * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaStreamSynchronize(c->stream), "d2h");
   }
@@ -430,7 +448,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     r.time_global = r.time_local = r.time_dual = 0.0;
     if (copy_vectors && any_vec) {
       if (r.x) std::memcpy(r.x, xall + id.x_off, sizeof(double) * id.n);
-      const std::size_t base = one ? 0 : (iters[i] % kZRing) * R;
+      const std::size_t base = 0;
       for (int32_t d = id.row0; d < id.row0 + id.rows; ++d) {
         const int32_t ref = L.ref_of_dev[d];
         if (r.z) r.z[ref] = zdev[base + d];

@@ -32,7 +32,28 @@ __global__ void k_gather(const GatherParams g) {
   for (int64_t k = i; k < g.nab; k += stride) g.ab[k] = g.rawb[g.ab_src[k]];
 }
 
+// final iterate of every instance out of the z / lambda rings (one CTA per
+// instance): instance i stopped at iters[i], its (z, lambda) in ring slot
+// iters[i] % ring
+__global__ void k_final_iterates(const double* zring, const double* lring, int64_t rows_total,
+                                 const int32_t* row0, const int32_t* rows, const int32_t* iters,
+                                 int ring, double* zout, double* lout) {
+  const int i = blockIdx.x;
+  const int64_t base = static_cast<int64_t>(iters[i] % ring) * rows_total;
+  for (int d = row0[i] + threadIdx.x; d < row0[i] + rows[i]; d += blockDim.x) {
+    zout[d] = zring[base + d];
+    lout[d] = lring[base + d];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_final_iterates(const double* zring, const double* lring, int64_t rows_total,
+                                  const int32_t* row0, const int32_t* rows, const int32_t* iters,
+                                  int instances, int ring, double* zout, double* lout, cudaStream_t s) {
+  k_final_iterates<<<instances, 256, 0, s>>>(zring, lring, rows_total, row0, rows, iters, ring, zout, lout);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gather(const GatherParams& g, int sm_count, cudaStream_t s) {
   k_gather<<<sm_count * 4, 512, 0, s>>>(g);

@@ -20,4 +20,10 @@ struct GatherParams {
 
 cudaError_t launch_gather(const GatherParams& g, int sm_count, cudaStream_t s);
 
+/// Batch results: each instance's final (z, lambda) out of the rings into
+/// compact [rows_total] arrays.
+cudaError_t launch_final_iterates(const double* zring, const double* lring, int64_t rows_total,
+                                  const int32_t* row0, const int32_t* rows, const int32_t* iters,
+                                  int instances, int ring, double* zout, double* lout, cudaStream_t s);
+
 }  // namespace dopf::cuda
