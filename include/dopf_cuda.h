@@ -25,6 +25,7 @@
 #ifndef DOPF_CUDA_H
 #define DOPF_CUDA_H
 
+#include "dopf_host.h"
 #include "dopf_types.h"
 
 #ifdef __cplusplus
@@ -68,6 +69,22 @@ int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
  * dopf_model_set_operators (dopf_host.h). */
 int dopf_cuda_precompute(dopf_cuda_ctx* ctx, const dopf_model_view* model, double* P, double* v,
                          int32_t* first_singular);
+
+/* Post-solve certification on the GPU (reference oracle.cpp:10-43,
+ * check_feasibility): ||A x - b||_inf over the centralized LP, bound
+ * violation, worst row / column (first maximum, -1 if none) and c'x. */
+typedef struct dopf_certificate {
+  double max_equality_violation;
+  double max_bound_violation;
+  double objective;
+  int32_t worst_row, worst_col;
+} dopf_certificate;
+int dopf_cuda_certify(dopf_cuda_ctx* ctx, const dopf_lp_view* lp, const double* x,
+                      dopf_certificate* out);
+/* Copy-average reconstruction (oracle.cpp:275-292): per column the mean of its
+ * copies (ascending s), clamped to the bounds; x where a column has no copy. */
+int dopf_cuda_reconstruct(dopf_cuda_ctx* ctx, const dopf_model_view* model, const double* x,
+                          const double* z, double* out);
 
 /* Solver path for the next uploads: 0 auto (default: shared-memory-resident
  * persistent kernel when the operators fit the CTAs' shared memory, else the

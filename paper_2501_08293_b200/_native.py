@@ -59,6 +59,11 @@ class PartInfo_t(C.Structure):
                 ("bytes_per_iteration", f64)]
 
 
+class Certificate_t(C.Structure):
+    _fields_ = [("max_equality_violation", f64), ("max_bound_violation", f64), ("objective", f64),
+                ("worst_row", i32), ("worst_col", i32)]
+
+
 class BatchInfo_t(C.Structure):
     _fields_ = [("instances", i32), ("blocks", i32), ("threads", i32), ("smem_bytes", i32),
                 ("resident", i32), ("sync_mode", i32)]
@@ -138,6 +143,8 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_kernels_executed", i64, vp)
     _sig(lib, "dopf_cuda_set_path", C.c_int, vp, i32)
     _sig(lib, "dopf_cuda_precompute", C.c_int, vp, P(ModelView_t), P(f64), P(f64), P(i32))
+    _sig(lib, "dopf_cuda_certify", C.c_int, vp, P(LpView_t), P(f64), P(Certificate_t))
+    _sig(lib, "dopf_cuda_reconstruct", C.c_int, vp, P(ModelView_t), P(f64), P(f64), P(f64))
     _sig(lib, "dopf_cuda_timeline", C.c_int, vp, P(u64), i64)
     _sig(lib, "dopf_cuda_bytes_per_iteration", f64, vp)
     _sig(lib, "dopf_cuda_last_kernel_seconds", f64, vp)

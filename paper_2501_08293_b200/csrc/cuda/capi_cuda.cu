@@ -13,6 +13,7 @@
 #include "../../../include/dopf_cuda.h"
 #include "admm_kernels.cuh"
 #include "layout_builder.hpp"
+#include "certify_kernels.cuh"
 #include "layout_gather.cuh"
 #include "precompute_kernels.cuh"
 #include "stream_kernels.cuh"
@@ -900,6 +901,91 @@ int dopf_cuda_precompute(dopf_cuda_ctx* c, const dopf_model_view* m, double* P, 
       for (void* d : owned) cudaFree(d);
       throw;
     }
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+T* dev_copy(dopf_cuda_ctx* c, std::vector<void*>& owned, const T* h, std::size_t n) {
+  void* d = nullptr;
+  ck(cudaMalloc(&d, std::max<std::size_t>(n * sizeof(T), 16)), "cudaMalloc");
+  owned.push_back(d);
+  if (h && n) ck(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream), "h2d");
+  return static_cast<T*>(d);
+}
+
+struct Owned {
+  std::vector<void*> p;
+  ~Owned() {
+    for (void* d : p) cudaFree(d);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int dopf_cuda_certify(dopf_cuda_ctx* c, const dopf_lp_view* lp, const double* x, dopf_certificate* out) {
+  if (!c || !lp || !x || !out) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    Owned o;
+    CertifyParams p{};
+    p.rows = lp->rows;
+    p.cols = lp->cols;
+    p.row_blocks = std::max(1, (lp->rows + 255) / 256);
+    p.col_blocks = std::max(1, (lp->cols + 255) / 256);
+    p.row_ptr = dev_copy(c, o.p, lp->row_ptr, static_cast<std::size_t>(lp->rows) + 1);
+    p.col_idx = dev_copy(c, o.p, lp->col_idx, static_cast<std::size_t>(lp->nnz));
+    p.values = dev_copy(c, o.p, lp->values, static_cast<std::size_t>(lp->nnz));
+    p.b = dev_copy(c, o.p, lp->b, static_cast<std::size_t>(lp->rows));
+    p.lo = dev_copy(c, o.p, lp->x_lo, static_cast<std::size_t>(lp->cols));
+    p.hi = dev_copy(c, o.p, lp->x_hi, static_cast<std::size_t>(lp->cols));
+    p.x = dev_copy(c, o.p, x, static_cast<std::size_t>(lp->cols));
+    p.blk_v = dev_copy<double>(c, o.p, nullptr, p.row_blocks + p.col_blocks);
+    p.blk_i = dev_copy<int32_t>(c, o.p, nullptr, p.row_blocks + p.col_blocks);
+    p.out = dev_copy<double>(c, o.p, nullptr, 2);
+    p.out_idx = dev_copy<int32_t>(c, o.p, nullptr, 2);
+    ck(launch_certify(p, c->stream), "certify");
+    c->kernels += 3;
+    double v[2];
+    int32_t idx[2];
+    ck(cudaMemcpyAsync(v, p.out, sizeof v, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(idx, p.out_idx, sizeof idx, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "certify");
+    out->max_equality_violation = v[0];
+    out->max_bound_violation = v[1];
+    out->worst_row = idx[0];
+    out->worst_col = idx[1];
+    double obj = 0.0;  // c'x in column order (the host check's sequence)
+    for (int j = 0; j < lp->cols; ++j) obj += lp->c[j] * x[j];
+    out->objective = obj;
+  });
+}
+
+int dopf_cuda_reconstruct(dopf_cuda_ctx* c, const dopf_model_view* m, const double* x, const double* z,
+                          double* out) {
+  if (!c || !m || !x || !z || !out || !m->has_pre) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    Owned o;
+    ReconstructParams p{};
+    p.n = m->n;
+    p.csr_ptr = dev_copy(c, o.p, m->csr_ptr, static_cast<std::size_t>(m->n) + 1);
+    p.csr_copy = dev_copy(c, o.p, m->csr_copy, static_cast<std::size_t>(m->N_z));
+    p.z = dev_copy(c, o.p, z, static_cast<std::size_t>(m->N_z));
+    p.x = dev_copy(c, o.p, x, static_cast<std::size_t>(m->n));
+    p.lo = dev_copy(c, o.p, m->x_lo, static_cast<std::size_t>(m->n));
+    p.hi = dev_copy(c, o.p, m->x_hi, static_cast<std::size_t>(m->n));
+    double* d_out = dev_copy<double>(c, o.p, nullptr, static_cast<std::size_t>(m->n));
+    p.out = d_out;
+    ck(launch_reconstruct(p, c->stream), "reconstruct");
+    ++c->kernels;
+    ck(cudaMemcpyAsync(out, d_out, m->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "reconstruct");
   });
 }
 

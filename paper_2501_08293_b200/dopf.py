@@ -603,6 +603,35 @@ def solve(model: DecomposedModel, settings: Settings = Settings(), device: int =
     return res
 
 
+def check_feasibility(ls: LinearSystem, x: np.ndarray, solver: Optional["CudaSolver"] = None) -> dict:
+    """GPU certification of a solution (reference check_feasibility, oracle.cpp:10-43)."""
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    if xs.shape != (ls.cols,):
+        raise ValueError(f"check_feasibility: x has {xs.size} entries, model has {ls.cols} columns")
+    s = solver or CudaSolver(0)
+    out = N.Certificate_t()
+    s._err(s._lib.dopf_cuda_certify(s._h, C.byref(ls.view), xs.ctypes.data_as(C.POINTER(C.c_double)),
+                                    C.byref(out)))
+    return {"max_equality_violation": out.max_equality_violation,
+            "max_bound_violation": out.max_bound_violation, "worst_row": out.worst_row,
+            "worst_col": out.worst_col, "objective": out.objective}
+
+
+def reconstruct_centralized(model: DecomposedModel, x: np.ndarray, z: np.ndarray,
+                            solver: Optional["CudaSolver"] = None) -> np.ndarray:
+    """GPU copy-average reconstruction (reference oracle.cpp:275-292)."""
+    if not model.has_precompute:
+        model.precompute()
+    xs = np.ascontiguousarray(x, dtype=np.float64)
+    zs = np.ascontiguousarray(z, dtype=np.float64)
+    out = np.zeros(model.global_cols)
+    s = solver or CudaSolver(0)
+    p = C.POINTER(C.c_double)
+    s._err(s._lib.dopf_cuda_reconstruct(s._h, C.byref(model.view()), xs.ctypes.data_as(p),
+                                        zs.ctypes.data_as(p), out.ctypes.data_as(p)))
+    return out
+
+
 def write_trace_csv(trace: np.ndarray) -> str:
     t = np.ascontiguousarray(trace, dtype=np.float64).reshape(-1, 6)
     rc, text = N.text_call(N.host().dopf_write_trace_csv,

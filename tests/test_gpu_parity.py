@@ -281,3 +281,25 @@ def test_reupload_same_structure_fast_path_bitwise(solver):
         gpu = solver.solve(settings)
         ref = O.solve(m, dopf.Settings(workers=8))
         assert_same(gpu, ref, bitwise=True)
+
+
+# ------------------------------------------------------------ certification (row f4)
+
+
+@pytest.mark.parametrize("source", ["two_bus", "four_bus_delta", "ieee8500"])
+def test_gpu_certify_and_reconstruct_match_host_checks(solver, source):
+    if source.startswith("ieee"):
+        f = dopf.synthetic_feeder(source, 8500)
+        _, ls, model = dopf.load_model(f, workers=8)
+        model.precompute(8)
+    else:
+        _, ls, model = dopf.load_model(fixture_path(source))
+        model.precompute()
+    solver.upload(model)
+    res = solver.solve(dopf.Settings(eps_rel=1e-4))
+    rebuilt = dopf.reconstruct_centralized(model, res.x, res.z, solver)
+    assert np.array_equal(rebuilt, O.reconstruct_centralized(model, res.x, res.z))
+    for x in (rebuilt, res.x, np.zeros(ls.cols)):
+        gpu, host = dopf.check_feasibility(ls, x, solver), O.check_feasibility(ls, x)
+        for k in ("max_equality_violation", "max_bound_violation", "worst_row", "worst_col", "objective"):
+            assert gpu[k] == host[k], (k, gpu[k], host[k])
