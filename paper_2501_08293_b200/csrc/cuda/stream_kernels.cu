@@ -86,16 +86,29 @@ __device__ __forceinline__ void finalize_iteration(const StreamParams& p, const 
   }
 }
 
-__global__ void __launch_bounds__(kStreamRows) k_global(const StreamParams p) {
+__global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p) {
   __shared__ double sh[8];
   if (p.ctl->done) return;  // partitioned loops may run past the stop (lazy host check)
   const int c = blockIdx.x * kStreamRows + threadIdx.x;
   double o[1] = {0.0};
   if (c < p.cols) {
+    // the column's first four copies: index loads, then value loads, all in
+    // flight before the ascending-s sum
+    const int q0 = p.col_ptr[c], q1 = p.col_ptr[c + 1];
+    int32_t ref[4];
+    double uv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ref[e] = q0 + e < q1 ? p.copies[q0 + e] : 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      uv[e] = q0 + e < q1 ? (ref[e] >= 0 ? p.u[ref[e]] : p.u_remote[-ref[e] - 1]) : 0.0;
     double acc = 0.0;
-    for (int q = p.col_ptr[c]; q < p.col_ptr[c + 1]; ++q) {
-      const int32_t ref = p.copies[q];
-      acc = acc + (ref >= 0 ? p.u[ref] : p.u_remote[-ref - 1]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (q0 + e < q1) acc = acc + uv[e];
+    for (int q = q0 + 4; q < q1; ++q) {
+      const int32_t rq = p.copies[q];
+      acc = acc + (rq >= 0 ? p.u[rq] : p.u_remote[-rq - 1]);
     }
     const double unclamped = (acc - p.cost[c] / p.rho) * p.inv[c];
     const double xv = sel_min(sel_max(unclamped, p.lo[c]), p.hi[c]);
