@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p)
   if (threadIdx.x == 0) p.objp[blockIdx.x] = o[0];
 }
 
-template <int kMinBlocks, bool kPrefetch>
+template <int kMinBlocks>
 __global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamParams p) {
   __shared__ double tgt[kStreamRows];
   __shared__ double zsh[kStreamRows];
@@ -131,45 +131,21 @@ __global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamP
   const bool on = r < ch.rows;
   const int d = ch.row0 + r;
   StreamRow rm{0, 0, 0, 0};
-  double bx = 0.0, lamv = 0.0, vd = 0.0, zprev = 0.0;
-  const double* pr = p.P + p.pslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
-  double pv[8];  // first chunk of this row of P: in flight across the target barrier
-  double av[8];  // ... and of this thread's equality row of A
-  StreamARow am{0, 0};
-  double abv = 0.0;
-  const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
-  if (kPrefetch && r < ch.arows) {
-    am = p.ameta[blockIdx.x * kStreamRows + r];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) av[e] = e < am.n ? __ldcs(ar + 32 * e) : 0.0;
-    abv = p.ab[ch.arow0 + r];
-  }
+  double bx = 0.0, lamv = 0.0;
   if (on) {
     rm = p.rmeta[d];
-    if (kPrefetch) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) pv[e] = e < rm.n ? __ldcs(pr + 32 * e) : 0.0;
-    }
     bx = p.x[rm.xcol];
     lamv = p.lam[d];
-    if (kPrefetch) {
-      vd = p.v[d];
-      zprev = p.z[d];
-    }
     tgt[r] = bx + lamv / rho;  // admm.cpp:136
   }
   __syncthreads();
   double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (on) {
+    const double* pr = p.P + p.pslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
     const double* tb = tgt + rm.base;
     double acc = 0.0;
-    if (kPrefetch) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (e < rm.n) acc = acc + pv[e] * tb[e];
-    }
-    for (int j0 = kPrefetch ? 8 : 0; j0 < rm.n; j0 += 8) {
-      double tv[8];
+    for (int j0 = 0; j0 < rm.n; j0 += 8) {
+      double pv[8], tv[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         pv[e] = 0.0;
@@ -183,11 +159,8 @@ __global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamP
       for (int e = 0; e < 8; ++e)
         if (j0 + e < rm.n) acc = acc + pv[e] * tv[e];
     }
-    if (!kPrefetch) {
-      vd = p.v[d];
-      zprev = p.z[d];
-    }
-    const double z = acc + vd;
+    const double z = acc + p.v[d];
+    const double zprev = p.z[d];
     const double dd = bx - z;
     const double ln = lamv + rho * dd;  // admm.cpp:142
     p.z[d] = z;
@@ -203,22 +176,19 @@ __global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamP
   }
   __syncthreads();
   if (r < ch.arows) {
-    if (!kPrefetch) {
-      am = p.ameta[blockIdx.x * kStreamRows + r];
-      abv = p.ab[ch.arow0 + r];
-    }
+    const StreamARow am = p.ameta[blockIdx.x * kStreamRows + r];
+    const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
     const double* zb = zsh + am.base;
     double acc = 0.0;
     for (int j0 = 0; j0 < am.n; j0 += 8) {
-      if (!kPrefetch || j0 > 0) {
+      double av[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? __ldcs(ar + 32 * (j0 + e)) : 0.0;
-      }
+      for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? __ldcs(ar + 32 * (j0 + e)) : 0.0;
 #pragma unroll
       for (int e = 0; e < 8; ++e)
         if (j0 + e < am.n) acc = acc + av[e] * zb[j0 + e];
     }
-    v[5] = fabs(acc - abv);
+    v[5] = fabs(acc - p.ab[ch.arow0 + r]);
   }
   block_reduce<6, kStreamRows>(v, sh, 5);
   if (threadIdx.x == 0) {
@@ -305,10 +275,10 @@ __global__ void k_decide(const StreamParams p, const double* ranks, int nranks) 
 using LocalKernel = void (*)(const StreamParams);
 
 LocalKernel local_kernel() {
-  // DOPF_KLOCAL: 0 = 3 CTAs/SM without the P prefetch, 1 = 2 CTAs/SM with it
+  // CTAs per SM for k_local: 4 (32 registers) measured fastest; DOPF_KLOCAL=3 for experiments
   static const LocalKernel k = [] {
     const char* e = std::getenv("DOPF_KLOCAL");
-    return (e && e[0] == '1') ? &k_local<2, true> : &k_local<3, false>;
+    return (e && e[0] == '3') ? &k_local<3> : &k_local<4>;
   }();
   return k;
 }
