@@ -112,6 +112,7 @@ struct dopf_cuda_ctx {
   int64_t kernels = 0;       // kernels launched (graph iterations x 3 + persistent launches)
   // re-upload fast path: the plan whose index maps / structure sit on the device
   const InstancePlan* dev_plan = nullptr;
+  bool stream_maps = false;  // the streaming layout's maps are on the device
   int64_t* d_psrc = nullptr;
   int64_t* d_asrc = nullptr;
   int64_t* d_absrc = nullptr;
@@ -767,6 +768,76 @@ void upload_values(dopf_cuda_ctx* c, const dopf_model_view& m) {
   ck(cudaStreamSynchronize(c->stream), "upload sync");
 }
 
+void upload_stream_maps(dopf_cuda_ctx* c, const dopf_model_view& m) {
+  const StreamLayout& L = c->SL;
+  int k = 96;  // slots 96.. (resident 0..31, streaming 32..62, resident maps 64..78)
+  c->d_psrc = c->put(k++, L.p_src);
+  c->d_asrc = c->put(k++, L.a_src);
+  c->d_absrc = c->put(k++, L.ab_src);
+  c->d_refdev = c->put(k++, L.ref_of_dev);
+  c->d_gcol = c->put(k++, L.gcol);
+  c->d_rawP = c->scratch<double>(k++, static_cast<std::size_t>(m.p_offsets[m.S]));
+  c->d_rawA = c->scratch<double>(k++, static_cast<std::size_t>(m.a_offsets[m.S]));
+  c->d_rawb = c->scratch<double>(k++, static_cast<std::size_t>(m.b_offsets[m.S]));
+  c->d_rawv = c->scratch<double>(k++, m.N_z);
+  c->d_rawz0 = c->scratch<double>(k++, m.N_z);
+  c->d_rawc = c->scratch<double>(k++, m.n);
+  c->d_rawinv = c->scratch<double>(k++, m.n);
+  c->d_rawlo = c->scratch<double>(k++, m.n);
+  c->d_rawhi = c->scratch<double>(k++, m.n);
+  ck(cudaStreamSynchronize(c->stream), "stream maps");
+  c->stream_maps = true;
+}
+
+void upload_stream_values(dopf_cuda_ctx* c, const dopf_model_view& m) {
+  auto h2d = [&](double* d, const double* h, std::size_t n) {
+    if (n) ck(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "upload");
+  };
+  h2d(c->d_rawP, m.P, static_cast<std::size_t>(m.p_offsets[m.S]));
+  h2d(c->d_rawA, m.A, static_cast<std::size_t>(m.a_offsets[m.S]));
+  h2d(c->d_rawb, m.b, static_cast<std::size_t>(m.b_offsets[m.S]));
+  h2d(c->d_rawv, m.v, m.N_z);
+  h2d(c->d_rawz0, m.z0, m.N_z);
+  h2d(c->d_rawc, m.c, m.n);
+  h2d(c->d_rawinv, m.inv_copy, m.n);
+  h2d(c->d_rawlo, m.x_lo, m.n);
+  h2d(c->d_rawhi, m.x_hi, m.n);
+  const StreamLayout& L = c->SL;
+  auto& d = c->sd;
+  GatherParams g{};
+  g.np = static_cast<int64_t>(L.p_src.size());
+  g.na = static_cast<int64_t>(L.a_src.size());
+  g.rows = L.rows;
+  g.cols = L.cols;
+  g.nab = static_cast<int64_t>(L.ab_src.size());
+  g.p_src = c->d_psrc;
+  g.a_src = c->d_asrc;
+  g.ref_of_dev = c->d_refdev;
+  g.gcol = c->d_gcol;
+  g.ab_src = c->d_absrc;
+  g.rawP = c->d_rawP;
+  g.rawA = c->d_rawA;
+  g.rawb = c->d_rawb;
+  g.rawv = c->d_rawv;
+  g.rawz0 = c->d_rawz0;
+  g.rawc = c->d_rawc;
+  g.rawinv = c->d_rawinv;
+  g.rawlo = c->d_rawlo;
+  g.rawhi = c->d_rawhi;
+  g.P = d.P;
+  g.A = d.A;
+  g.ab = d.ab;
+  g.v = d.v;
+  g.z0 = d.z0;
+  g.cc = d.cost;
+  g.cinv = d.inv;
+  g.clo = d.lo;
+  g.chi = d.hi;
+  ck(launch_gather(g, c->sm_count, c->stream), "gather");
+  ++c->kernels;
+  ck(cudaStreamSynchronize(c->stream), "upload sync");
+}
+
 }  // namespace
 
 int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
@@ -779,15 +850,24 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
     c->streaming = c->path_request == 2 || (c->path_request == 0 && needs_streaming(*m, opt));
     c->inst_nz = {m->N_z};
     c->inst_n = {m->n};
+    const bool was_partitioned = c->partitioned;
     c->partitioned = false;
+    if (was_partitioned) c->stream_maps = false;
     if (c->streaming) {
       c->dev_plan = nullptr;
       c->L.reset();
-      upload_stream(c, *m);
+      if (c->stream_maps && !c->partitioned && c->SL.same_structure(*m)) {
+        upload_stream_values(c, *m);  // raw values + device gather (structure unchanged)
+      } else {
+        c->stream_maps = false;
+        upload_stream(c, *m);
+        upload_stream_maps(c, *m);
+      }
       c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
       c->uploaded = true;
       return;
     }
+    c->stream_maps = false;  // the map pointers are about to hold the resident plan's
     const bool same = c->plan && c->plan->same_structure(*m, opt);
     if (same && c->dev_plan == c->plan.get() && c->L.inst.size() == 1) {
       // fast path: structure and index maps already on the device; copy the
@@ -810,6 +890,7 @@ int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t 
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->uploaded = false;
     c->dev_plan = nullptr;
+    c->stream_maps = false;
     c->streaming = false;
     c->partitioned = false;
     LayoutOptions opt = options_for(c);
@@ -1003,6 +1084,7 @@ int dopf_cuda_upload_part(dopf_cuda_ctx* c, const dopf_model_view* m, int32_t np
     if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
     c->uploaded = false;
     c->dev_plan = nullptr;
+    c->stream_maps = false;
     c->L.reset();
     c->streaming = true;
     c->partitioned = true;

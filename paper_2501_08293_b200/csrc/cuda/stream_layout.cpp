@@ -1,6 +1,7 @@
 #include "stream_layout.hpp"
 
 #include <algorithm>
+#include <cstring>
 #include <climits>
 #include <cstdint>
 #include <stdexcept>
@@ -8,6 +9,16 @@
 #include "layout_builder.hpp"
 
 namespace dopf::cuda {
+
+bool StreamLayout::same_structure(const dopf_model_view& m) const {
+  auto eq = [](const std::vector<int32_t>& v, const int32_t* p, std::size_t n) {
+    return v.size() == n && (n == 0 || std::memcmp(v.data(), p, n * sizeof(int32_t)) == 0);
+  };
+  return nparts == 1 && m.has_pre && S == m.S && n == m.n && N_z == m.N_z &&
+         eq(sig_z_offsets, m.z_offsets, m.S + 1) && eq(sig_m_s, m.m_s, m.S) &&
+         eq(sig_l2g, m.l2g, m.N_z) && eq(sig_csr_ptr, m.csr_ptr, m.n + 1) &&
+         eq(sig_csr_copy, m.csr_copy, m.N_z);
+}
 
 StreamLayout build_stream_layout(const dopf_model_view& m) {
   return build_stream_layout_part(m, 1, 0, nullptr);
@@ -71,6 +82,7 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
       for (int r = 0; r < ms; ++r) {
         arow.push_back(Src{m.a_offsets[s] + static_cast<int64_t>(r) * n, n, rows});
         L.ab.push_back(m.b[m.b_offsets[s] + r]);
+        L.ab_src.push_back(m.b_offsets[s] + r);
       }
       rows += n;
     }
@@ -112,7 +124,8 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
   }
   // sliced ELL per chunk-local warp (rows of a warp never span chunks)
   auto pack = [](const std::vector<Src>& rows, const std::vector<StreamChunk>& chunks, bool arow_mode,
-                 std::vector<double>& out, std::vector<int64_t>& slices, const double* src) {
+                 std::vector<double>& out, std::vector<int64_t>& slices, const double* src,
+                 std::vector<int64_t>& srcidx) {
     for (const StreamChunk& ch : chunks) {
       const int first = arow_mode ? ch.arow0 : ch.row0;
       const int count = arow_mode ? ch.arows : ch.rows;
@@ -125,12 +138,13 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
           for (int l = 0; l < 32; ++l) {
             const bool ok = l < lanes && j < rows[first + w0 + l].n;
             out.push_back(ok ? src[rows[first + w0 + l].at + j] : 0.0);
+            srcidx.push_back(ok ? rows[first + w0 + l].at + j : -1);
           }
       }
     }
   };
-  pack(prow, L.chunks, false, L.P, L.pslice, m.P);
-  pack(arow, L.chunks, true, L.A, L.aslice, m.A);
+  pack(prow, L.chunks, false, L.P, L.pslice, m.P, L.p_src);
+  pack(arow, L.chunks, true, L.A, L.aslice, m.A, L.a_src);
   L.ameta.resize(static_cast<std::size_t>(L.chunks.size()) * kStreamRows);
   for (std::size_t c = 0; c < L.chunks.size(); ++c)
     for (int a = 0; a < kStreamRows; ++a) {
@@ -193,6 +207,13 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     mn += m.m_s[s] * n;
   }
   // algorithmic bytes of this part (DESIGN.md section 4 restricted to it)
+  if (nparts == 1) {  // signature for the re-upload fast path
+    L.sig_z_offsets.assign(m.z_offsets, m.z_offsets + m.S + 1);
+    L.sig_m_s.assign(m.m_s, m.m_s + m.S);
+    L.sig_l2g.assign(m.l2g, m.l2g + m.N_z);
+    L.sig_csr_ptr.assign(m.csr_ptr, m.csr_ptr + m.n + 1);
+    L.sig_csr_copy.assign(m.csr_copy, m.csr_copy + m.N_z);
+  }
   L.bytes_per_iteration = 8.0 * (n2 + mn + msum) + 56.0 * L.rows + 48.0 * L.cols +
                           4.0 * (2.0 * L.rows + L.cols + 1) + 16.0 * static_cast<double>(order.size());
   return L;

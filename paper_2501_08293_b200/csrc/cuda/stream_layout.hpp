@@ -62,6 +62,11 @@ struct StreamLayout {
   // part * max_export + e of every rank's remote array, in this order)
   int32_t nparts = 1, part = 0, max_export = 0;
   std::vector<int32_t> export_rows;
+  // re-upload fast path: where every packed value comes from in the model
+  // view (P / A / b indices, -1 = zero padding) and the structure signature
+  std::vector<int64_t> p_src, a_src, ab_src;
+  std::vector<int32_t> sig_z_offsets, sig_m_s, sig_l2g, sig_csr_ptr, sig_csr_copy;
+  bool same_structure(const dopf_model_view& m) const;
 };
 
 /// Whole-model streaming layout (one rank).

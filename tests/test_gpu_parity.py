@@ -283,6 +283,21 @@ def test_reupload_same_structure_fast_path_bitwise(solver):
         assert_same(gpu, ref, bitwise=True)
 
 
+def test_stream_reupload_same_structure_fast_path_bitwise():
+    """Streaming path: a same-structure re-upload skips the host layout build
+    (raw values + device gather over the cached maps) -- still bitwise."""
+    from paper_2501_08293_b200 import scenarios
+    models = scenarios.build_scenarios("ieee123", 123, range(3))
+    s = dopf.CudaSolver(0)
+    s.set_path("stream")
+    settings = dopf.Settings()
+    for m in models + models[:1]:
+        s.upload(m)
+        gpu = s.solve(settings)
+        ref = O.solve(m, dopf.Settings(workers=8))
+        assert_same(gpu, ref, bitwise=True)
+
+
 # ------------------------------------------------------------ certification (row f4)
 
 
