@@ -548,7 +548,7 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.u = c->scratch<double>(k++, L.rows);
   d.u_remote = c->scratch<double>(k++, std::max(1, L.remote_slots));
   d.part = c->scratch<double>(k++, static_cast<std::size_t>(L.chunks.size()) * 8);
-  d.objp = c->scratch<double>(k++, (L.cols + kStreamRows - 1) / kStreamRows);
+  d.objp = c->scratch<double>(k++, std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows));
   d.partials = c->scratch<double>(k++, 8);
   d.ctl = c->scratch<StreamCtl>(k++, 1);
   d.part2 = c->scratch<double>(k++, 128 * 8);
@@ -601,7 +601,8 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   p.max_iter = s->max_iter;
   p.nchunks = static_cast<int32_t>(L.chunks.size());
   p.cols = L.cols;
-  p.col_blocks = (L.cols + kStreamRows - 1) / kStreamRows;
+  p.bcols = L.bcols;
+  p.col_blocks = std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows);
   return p;
 }
 

@@ -4,10 +4,12 @@
 // condition the finalize kernel clears at the stop test -- no host round trip
 // per iteration:
 //
-//  k_global   (thread per column)  admm.cpp:118-129: acc = sum over the
-//             column's copies (CSR, ascending s) of u = z - lambda/rho;
+//  k_global   (thread per boundary column)  admm.cpp:118-129: acc = sum over
+//             the column's copies (CSR, ascending s) of u = z - lambda/rho;
 //             x = clamp((acc - c/rho) * inv_count, lo, hi); c'x partials.
 //  k_local    (CTA per chunk of whole subsystems, thread per row)
+//             the same global update for the chunk's interior columns (all
+//             copies in the chunk) from the z, lambda it loads anyway, then
 //             admm.cpp:131-143, 203-205, 150-163: target in shared memory,
 //             z = P target + v with P streamed from HBM (sliced ELL: 256
 //             contiguous bytes per warp load), dual update, u, ||A z - b||_inf,
@@ -27,6 +29,14 @@ namespace dopf::cuda {
 namespace {
 
 __device__ __forceinline__ double sel_max(double a, double b) { return (a < b) ? b : a; }
+
+// one bulk (TMA-engine) prefetch of [ptr, ptr + bytes) into L2; bytes % 16 == 0
+__device__ __forceinline__ void bulk_prefetch_l2(const void* ptr, uint32_t bytes) {
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void* ptr) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+}
 __device__ __forceinline__ double sel_min(double a, double b) { return (b < a) ? b : a; }
 
 // fixed-shape block reduction of `V` values (sum; index `imax` uses max)
@@ -91,7 +101,7 @@ __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p)
   if (p.ctl->done) return;  // partitioned loops may run past the stop (lazy host check)
   const int c = blockIdx.x * kStreamRows + threadIdx.x;
   double o[1] = {0.0};
-  if (c < p.cols) {
+  if (c < p.bcols) {
     // the column's first four copies: index loads, then value loads, all in
     // flight before the ascending-s sum
     const int q0 = p.col_ptr[c], q1 = p.col_ptr[c + 1];
@@ -122,20 +132,68 @@ __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p)
 template <int kMinBlocks>
 __global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamParams p) {
   __shared__ double tgt[kStreamRows];
-  __shared__ double zsh[kStreamRows];
+  __shared__ double ush[kStreamRows];  // u = z - lambda/rho of the chunk's rows, then z
+  __shared__ double xsh[kStreamRows];  // x of the chunk's interior columns
+  __shared__ double zsh[kStreamRows];  // z^{t-1} (kept out of registers across the GEMV)
+  __shared__ int32_t csh[kStreamRows + 1];  // interior CSR: chunk-local copy rows, column offsets
+  __shared__ int32_t psh[kStreamRows + 1];
+  __shared__ double osh[kStreamRows / 32];  // per-warp c'x of the interior columns
   __shared__ double sh[6 * (kStreamRows / 32)];
   if (p.ctl->done) return;
-  const StreamChunk ch = p.chunks[blockIdx.x];
+  // chunk fields are re-read where used (uniform, L1-resident) rather than
+  // held in registers across the whole kernel
+  const StreamChunk* ch = p.chunks + blockIdx.x;
   const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
   const double rho = p.rho;
-  const bool on = r < ch.rows;
-  const int d = ch.row0 + r;
+  const bool on = r < ch->rows;
+  const int d = ch->row0 + r;
+  // the chunk's operator slabs start moving HBM -> L2 now, overlapping the
+  // dependent row loads and the interior-column update below
+  if (r == 0) {
+    bulk_prefetch_l2(p.P + ch->p0, static_cast<uint32_t>(8 * (ch->p1 - ch->p0)));
+    bulk_prefetch_l2(p.A + ch->a0, static_cast<uint32_t>(8 * (ch->a1 - ch->a0)));
+  }
+  if (r < ch->icols) {
+    const int c = ch->icol0 + r;
+    prefetch_l1(p.cost + c);
+    prefetch_l1(p.inv + c);
+    prefetch_l1(p.lo + c);
+    prefetch_l1(p.hi + c);
+    prefetch_l1(p.owner + c);
+  }
+  // interior columns (admm.cpp:118-129): their CSR slice is staged in shared
+  // memory by the same load round as the rows (copies <= rows)
+  if (r < ch->icopies) csh[r] = p.copies[ch->icopy0 + r] - ch->row0;
+  if (r <= ch->icols) psh[r] = p.col_ptr[ch->icol0 + r] - ch->icopy0;
   StreamRow rm{0, 0, 0, 0};
   double bx = 0.0, lamv = 0.0;
   if (on) {
     rm = p.rmeta[d];
-    bx = p.x[rm.xcol];
     lamv = p.lam[d];
+    const double zprev = p.z[d];
+    if (rm.xcol < p.bcols) bx = p.x[rm.xcol];  // boundary column: k_global wrote x^t
+    ush[r] = zprev - lamv / rho;               // the u the previous iteration stored
+    zsh[r] = zprev;
+  }
+  __syncthreads();
+  double o = 0.0;
+  if (r < ch->icols) {
+    const int c = ch->icol0 + r;
+    const int q1 = psh[r + 1];
+    double acc = 0.0;
+    for (int q = psh[r]; q < q1; ++q) acc = acc + ush[csh[q]];  // ascending s
+    const double unclamped = (acc - p.cost[c] / rho) * p.inv[c];
+    const double xv = sel_min(sel_max(unclamped, p.lo[c]), p.hi[c]);
+    xsh[r] = xv;
+    p.x[c] = xv;
+    if (p.owner[c]) o = p.cost[c] * xv;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) o = o + __shfl_xor_sync(0xffffffffu, o, off);
+  if (lane == 0) osh[warp] = o;
+  __syncthreads();
+  if (on) {
+    if (rm.xcol >= p.bcols) bx = xsh[rm.xcol - ch->icol0];
     tgt[r] = bx + lamv / rho;  // admm.cpp:136
   }
   __syncthreads();
@@ -160,25 +218,24 @@ __global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamP
         if (j0 + e < rm.n) acc = acc + pv[e] * tv[e];
     }
     const double z = acc + p.v[d];
-    const double zprev = p.z[d];
     const double dd = bx - z;
     const double ln = lamv + rho * dd;  // admm.cpp:142
     p.z[d] = z;
     p.lam[d] = ln;
-    p.u[d] = z - ln / rho;  // the next global update's z - lambda/rho
-    zsh[r] = z;
+    if (rm.xcol < p.bcols) p.u[d] = z - ln / rho;  // read by the next boundary update / exports
     v[0] = dd * dd;
-    const double dz = z - zprev;
+    const double dz = z - zsh[r];
     v[1] = dz * dz;
     v[2] = bx * bx;
     v[3] = z * z;
     v[4] = ln * ln;
+    ush[r] = z;  // every read of u happened before the previous barrier
   }
   __syncthreads();
-  if (r < ch.arows) {
+  if (r < ch->arows) {
     const StreamARow am = p.ameta[blockIdx.x * kStreamRows + r];
     const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
-    const double* zb = zsh + am.base;
+    const double* zb = ush + am.base;
     double acc = 0.0;
     for (int j0 = 0; j0 < am.n; j0 += 8) {
       double av[8];
@@ -188,13 +245,17 @@ __global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamP
       for (int e = 0; e < 8; ++e)
         if (j0 + e < am.n) acc = acc + av[e] * zb[j0 + e];
     }
-    v[5] = fabs(acc - p.ab[ch.arow0 + r]);
+    v[5] = fabs(acc - p.ab[ch->arow0 + r]);
   }
   block_reduce<6, kStreamRows>(v, sh, 5);
   if (threadIdx.x == 0) {
     double* out = p.part + static_cast<int64_t>(blockIdx.x) * 8;
 #pragma unroll
     for (int q = 0; q < 6; ++q) out[q] = v[q];
+    double obj = 0.0;
+#pragma unroll
+    for (int w = 0; w < kStreamRows / 32; ++w) obj = obj + osh[w];
+    out[6] = obj;
   }
 }
 
@@ -217,6 +278,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
 #pragma unroll
     for (int i = 0; i < 5; ++i) v[i] = v[i] + __ldcg(q + i);
     v[5] = sel_max(v[5], __ldcg(q + 5));
+    v[6] = v[6] + __ldcg(q + 6);  // interior columns' c'x
   }
   const int o0 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * g / kFinalBlocks);
   const int o1 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * (g + 1) / kFinalBlocks);

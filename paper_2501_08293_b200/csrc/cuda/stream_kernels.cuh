@@ -38,10 +38,10 @@ struct StreamParams {
   double* x;             // [cols]
   double* z;             // [rows] (in place: z^{t-1} -> z^t)
   double* lam;           // [rows]
-  double* u;             // [rows] z - lambda/rho
+  double* u;             // [rows] z - lambda/rho (rows of boundary columns)
   const double* u_remote;  // partitioned: gathered copies of other ranks
   double* part;          // [nchunks][8]
-  double* objp;          // [col_blocks]
+  double* objp;          // [col_blocks] boundary columns' c'x
   double* part2;         // [128][8] level-2 partials (k_final)
   unsigned* final_count; // k_final's last-block counter (zero between iterations)
   double* trace;         // [max_iter][6] or null
@@ -54,10 +54,10 @@ struct StreamParams {
   int32_t max_iter;
   int32_t nchunks;
   int32_t cols;
-  int32_t col_blocks;
+  int32_t bcols;         // boundary columns [0, bcols) (k_global); the rest are per-chunk interior
+  int32_t col_blocks;    // k_global CTAs (>= 1)
   cudaGraphConditionalHandle cond;
   int32_t use_cond;
-  int32_t pad;
 };
 
 /// The whole solve as one graph: a while-node over {k_global, k_local, k_final}.

@@ -103,16 +103,42 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
   // columns updated here: every column a local row references, ordered by
   // their first local copy's device row (ties by column) -- the global update
   // then walks u and the local update gathers x in near-sequential order
+  // Boundary columns (copies in several chunks, or on other parts) come
+  // first; interior columns follow grouped by their chunk.
   std::vector<int32_t> loc_of_col(m.n, -1);
   {
-    std::vector<int32_t> first_row(m.n, INT32_MAX);
-    for (int ref = 0; ref < m.N_z; ++ref)
-      if (dev_of_ref[ref] >= 0) first_row[m.l2g[ref]] = std::min(first_row[m.l2g[ref]], dev_of_ref[ref]);
-    for (int c = 0; c < m.n; ++c)
-      if (first_row[c] != INT32_MAX) L.gcol.push_back(c);
-    std::stable_sort(L.gcol.begin(), L.gcol.end(),
-                     [&](int32_t a, int32_t b) { return first_row[a] < first_row[b]; });
-    for (std::size_t q = 0; q < L.gcol.size(); ++q) loc_of_col[L.gcol[q]] = static_cast<int32_t>(q);
+    std::vector<int32_t> chunk_of_row(row);
+    for (std::size_t q = 0; q < L.chunks.size(); ++q)
+      for (int r = 0; r < L.chunks[q].rows; ++r) chunk_of_row[L.chunks[q].row0 + r] = static_cast<int32_t>(q);
+    std::vector<int32_t> first_row(m.n, INT32_MAX), chunk_of_col(m.n, -1);
+    std::vector<char> boundary(m.n, 0);
+    for (int ref = 0; ref < m.N_z; ++ref) {
+      const int32_t d = dev_of_ref[ref], gc = m.l2g[ref];
+      if (d < 0) continue;
+      first_row[gc] = std::min(first_row[gc], d);
+      if (chunk_of_col[gc] < 0) chunk_of_col[gc] = chunk_of_row[d];
+      else if (chunk_of_col[gc] != chunk_of_row[d]) boundary[gc] = 1;
+    }
+    for (int c = 0; c < m.n; ++c) {
+      if (first_row[c] == INT32_MAX) continue;
+      for (int q = m.csr_ptr[c]; q < m.csr_ptr[c + 1]; ++q)
+        if (dev_of_ref[m.csr_copy[q]] < 0) boundary[c] = 1;  // a copy on another part
+      L.gcol.push_back(c);
+    }
+    std::stable_sort(L.gcol.begin(), L.gcol.end(), [&](int32_t a, int32_t b) {
+      return boundary[a] != boundary[b] ? boundary[a] > boundary[b] : first_row[a] < first_row[b];
+    });
+    for (std::size_t q = 0; q < L.gcol.size(); ++q) {
+      const int32_t gc = L.gcol[q];
+      loc_of_col[gc] = static_cast<int32_t>(q);
+      if (boundary[gc]) {
+        L.bcols = static_cast<int32_t>(q) + 1;
+        continue;
+      }
+      StreamChunk& ch = L.chunks[chunk_of_col[gc]];
+      if (ch.icols == 0) ch.icol0 = static_cast<int32_t>(q);
+      ++ch.icols;
+    }
   }
   for (int ref = 0; ref < m.N_z; ++ref) {
     const int32_t d = dev_of_ref[ref];
@@ -145,6 +171,13 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
   };
   pack(prow, L.chunks, false, L.P, L.pslice, m.P, L.p_src);
   pack(arow, L.chunks, true, L.A, L.aslice, m.A, L.a_src);
+  for (std::size_t c = 0; c < L.chunks.size(); ++c) {
+    const std::size_t w = c * (kStreamRows / 32), wn = (c + 1) * (kStreamRows / 32);
+    L.chunks[c].p0 = L.pslice[w];
+    L.chunks[c].p1 = wn < L.pslice.size() ? L.pslice[wn] : static_cast<int64_t>(L.P.size());
+    L.chunks[c].a0 = L.aslice[w];
+    L.chunks[c].a1 = wn < L.aslice.size() ? L.aslice[wn] : static_cast<int64_t>(L.A.size());
+  }
   L.ameta.resize(static_cast<std::size_t>(L.chunks.size()) * kStreamRows);
   for (std::size_t c = 0; c < L.chunks.size(); ++c)
     for (int a = 0; a < kStreamRows; ++a) {
@@ -200,6 +233,11 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     L.hi.push_back(m.x_hi[gc]);
     L.x0.push_back(m.x0[gc]);
     L.owner.push_back(part_of(s_of_ref[m.csr_copy[m.csr_ptr[gc]]]) == part ? 1 : 0);
+  }
+  for (StreamChunk& ch : L.chunks) {
+    ch.icopy0 = ch.icols ? L.col_ptr[ch.icol0] : 0;
+    ch.icopies = ch.icols ? L.col_ptr[ch.icol0 + ch.icols] - ch.icopy0 : 0;
+    if (ch.icopies > ch.rows) throw std::logic_error("interior copies exceed the chunk's rows");
   }
   for (int s : order) {
     const double n = ns_of(s);

@@ -39,12 +39,19 @@ struct StreamChunk {
   int32_t rows;
   int32_t arow0;  // first equality row
   int32_t arows;
+  int32_t icol0;  // first interior column (all copies in this chunk): updated by k_local
+  int32_t icols;
+  int32_t icopy0; // their copies: [icopy0, icopy0 + icopies) of `copies` (<= rows)
+  int32_t icopies;
+  int64_t p0, p1; // the chunk's P slab [p0, p1) and A slab [a0, a1) (doubles): bulk-prefetched to L2
+  int64_t a0, a1;
 };
 
 struct StreamLayout {
   int32_t S = 0, n = 0, N_z = 0;       // whole model
   int32_t rows = 0;                    // device rows (this rank)
   int32_t cols = 0;                    // columns this rank updates
+  int32_t bcols = 0;                   // boundary columns [0, bcols): copies in >1 chunk or remote
   std::vector<StreamChunk> chunks;
   std::vector<StreamRow> rmeta;        // per device row
   std::vector<int64_t> pslice;         // per warp-slice of rows: offset into P
