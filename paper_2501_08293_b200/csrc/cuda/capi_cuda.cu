@@ -3,6 +3,7 @@
 
 #include <chrono>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -86,10 +87,12 @@ struct dopf_cuda_ctx {
   StreamLayout SL;
   struct StreamDev {
     StreamChunk* chunks = nullptr;
-    StreamRow* rmeta = nullptr;
-    int64_t *pslice = nullptr, *aslice = nullptr;
-    StreamARow* ameta = nullptr;
-    double *P = nullptr, *A = nullptr, *ab = nullptr, *v = nullptr, *z0 = nullptr;
+    int32_t* staged_ids = nullptr;
+    int32_t* big_ids = nullptr;
+    int32_t *imp_ptr = nullptr, *imp_slot = nullptr;
+    double* ximp = nullptr;
+    unsigned char* blob = nullptr;  // chunk images
+    double* z0 = nullptr;
     int32_t *col_ptr = nullptr, *copies = nullptr;
     double *cost = nullptr, *inv = nullptr, *lo = nullptr, *hi = nullptr;
     uint8_t* owner = nullptr;
@@ -112,12 +115,15 @@ struct dopf_cuda_ctx {
   int64_t kernels = 0;       // kernels launched (graph iterations x 3 + persistent launches)
   // re-upload fast path: the plan whose index maps / structure sit on the device
   const InstancePlan* dev_plan = nullptr;
+  int staged_grid = 1;       // persistent CTAs of the staged streaming kernel
   bool stream_maps = false;  // the streaming layout's maps are on the device
   int64_t* d_psrc = nullptr;
   int64_t* d_asrc = nullptr;
   int64_t* d_absrc = nullptr;
   int32_t* d_refdev = nullptr;
   int32_t* d_gcol = nullptr;
+  int32_t* d_blobsrc = nullptr;  // streaming re-upload: chunk-image value map
+  double* d_raw = nullptr;       // streaming re-upload: raw value concatenation
   double *d_rawP = nullptr, *d_rawA = nullptr, *d_rawb = nullptr, *d_rawv = nullptr, *d_rawz0 = nullptr,
          *d_rawc = nullptr, *d_rawinv = nullptr, *d_rawlo = nullptr, *d_rawhi = nullptr;
   // pinned staging for results copied back to the host
@@ -149,7 +155,8 @@ struct dopf_cuda_ctx {
 
   void* ensure(int slot, std::size_t bytes) {
     Buf& b = bufs.at(slot);
-    bytes = std::max<std::size_t>(bytes, 16);
+    // 64 bytes of slack: bulk copies round slice ends up to 16 bytes
+    bytes = std::max<std::size_t>(bytes, 16) + 64;
     if (b.cap < bytes) {
       if (b.p) cudaFree(b.p);
       b.p = nullptr;
@@ -526,14 +533,7 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   auto& d = c->sd;
   int k = 32;  // slots 32.. (the resident path uses 0..31)
   d.chunks = c->put(k++, L.chunks);
-  d.rmeta = c->put(k++, L.rmeta);
-  d.pslice = c->put(k++, L.pslice);
-  d.aslice = c->put(k++, L.aslice);
-  d.ameta = c->put(k++, L.ameta);
-  d.P = c->put(k++, L.P);
-  d.A = c->put(k++, L.A);
-  d.ab = c->put(k++, L.ab);
-  d.v = c->put(k++, L.v);
+  d.blob = reinterpret_cast<unsigned char*>(c->put(k++, L.blob));
   d.z0 = c->put(k++, L.z0);
   d.col_ptr = c->put(k++, L.col_ptr);
   d.copies = c->put(k++, L.copies);
@@ -547,7 +547,10 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.lam = c->scratch<double>(k++, L.rows);
   d.u = c->scratch<double>(k++, L.rows);
   d.u_remote = c->scratch<double>(k++, std::max(1, L.remote_slots));
-  d.part = c->scratch<double>(k++, static_cast<std::size_t>(L.chunks.size()) * 8);
+  // persistent staged CTAs: two per SM, one SM left to the direct-load chunks if any
+  c->staged_grid = std::max(1, std::min<int>(kStagedCtasPerSm * (c->sm_count - (L.big_ids.empty() ? 0 : 1)),
+                                             static_cast<int>(L.staged_ids.size())));
+  d.part = c->scratch<double>(k++, static_cast<std::size_t>(c->staged_grid + L.big_ids.size()) * 8);
   d.objp = c->scratch<double>(k++, std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows));
   d.partials = c->scratch<double>(k++, 8);
   d.ctl = c->scratch<StreamCtl>(k++, 1);
@@ -556,6 +559,18 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.export_rows = c->put(k++, L.export_rows);
   d.send = c->scratch<double>(k++, std::max(1, L.max_export));
   d.ranks = c->scratch<double>(k++, static_cast<std::size_t>(L.nparts) * 8);
+  d.staged_ids = c->put(k++, L.staged_ids);
+  d.big_ids = c->put(k++, L.big_ids);
+  d.imp_ptr = c->put(k++, L.imp_ptr);
+  d.imp_slot = c->put(k++, L.imp_slot);
+  d.ximp = c->scratch<double>(k++, L.bimp.size());
+  ck(stream_prepare(), "staged kernel attributes");
+  if (const char* vb = std::getenv("DOPF_VERBOSE"); vb && vb[0] == '1')
+    std::fprintf(stderr,
+                 "stream layout: %zu chunks (%zu staged, %zu direct), %d rows, %d cols (%d boundary), %zu imports, "
+                 "%.1f MB of chunk images\n",
+                 L.chunks.size(), L.staged_ids.size(), L.big_ids.size(), L.rows, L.cols, L.bcols, L.bimp.size(),
+                 8e-6 * static_cast<double>(L.blob.size()));
   ck(cudaStreamSynchronize(c->stream), "upload sync");
   c->drop_graph();
 }
@@ -565,14 +580,18 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   auto& d = c->sd;
   StreamParams p{};
   p.chunks = d.chunks;
-  p.rmeta = d.rmeta;
-  p.pslice = d.pslice;
-  p.aslice = d.aslice;
-  p.ameta = d.ameta;
-  p.P = d.P;
-  p.A = d.A;
-  p.ab = d.ab;
-  p.v = d.v;
+  p.blob = d.blob;
+  p.staged_ids = d.staged_ids;
+  p.big_ids = d.big_ids;
+  p.imp_ptr = d.imp_ptr;
+  p.imp_slot = d.imp_slot;
+  p.ximp = d.ximp;
+  p.n_staged = static_cast<int32_t>(L.staged_ids.size());
+  p.n_big = static_cast<int32_t>(L.big_ids.size());
+  p.staged_grid = c->staged_grid;
+  p.npart = c->staged_grid + p.n_big;
+  p.stages = L.stages;
+  p.stage_bytes = L.stage_bytes;
   p.col_ptr = d.col_ptr;
   p.copies = d.copies;
   p.cost = d.cost;
@@ -771,70 +790,46 @@ void upload_values(dopf_cuda_ctx* c, const dopf_model_view& m) {
 
 void upload_stream_maps(dopf_cuda_ctx* c, const dopf_model_view& m) {
   const StreamLayout& L = c->SL;
-  int k = 96;  // slots 96.. (resident 0..31, streaming 32..62, resident maps 64..78)
-  c->d_psrc = c->put(k++, L.p_src);
-  c->d_asrc = c->put(k++, L.a_src);
-  c->d_absrc = c->put(k++, L.ab_src);
+  (void)m;
+  int k = 96;  // slots 96.. (resident 0..31, streaming 32..70, resident maps 64..78 unused here)
+  c->d_blobsrc = c->put(k++, L.blob_src);
   c->d_refdev = c->put(k++, L.ref_of_dev);
   c->d_gcol = c->put(k++, L.gcol);
-  c->d_rawP = c->scratch<double>(k++, static_cast<std::size_t>(m.p_offsets[m.S]));
-  c->d_rawA = c->scratch<double>(k++, static_cast<std::size_t>(m.a_offsets[m.S]));
-  c->d_rawb = c->scratch<double>(k++, static_cast<std::size_t>(m.b_offsets[m.S]));
-  c->d_rawv = c->scratch<double>(k++, m.N_z);
-  c->d_rawz0 = c->scratch<double>(k++, m.N_z);
-  c->d_rawc = c->scratch<double>(k++, m.n);
-  c->d_rawinv = c->scratch<double>(k++, m.n);
-  c->d_rawlo = c->scratch<double>(k++, m.n);
-  c->d_rawhi = c->scratch<double>(k++, m.n);
+  c->d_raw = c->scratch<double>(k++, static_cast<std::size_t>(L.raw_off[kRawEnd]));
   ck(cudaStreamSynchronize(c->stream), "stream maps");
   c->stream_maps = true;
 }
 
 void upload_stream_values(dopf_cuda_ctx* c, const dopf_model_view& m) {
-  auto h2d = [&](double* d, const double* h, std::size_t n) {
-    if (n) ck(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "upload");
-  };
-  h2d(c->d_rawP, m.P, static_cast<std::size_t>(m.p_offsets[m.S]));
-  h2d(c->d_rawA, m.A, static_cast<std::size_t>(m.a_offsets[m.S]));
-  h2d(c->d_rawb, m.b, static_cast<std::size_t>(m.b_offsets[m.S]));
-  h2d(c->d_rawv, m.v, m.N_z);
-  h2d(c->d_rawz0, m.z0, m.N_z);
-  h2d(c->d_rawc, m.c, m.n);
-  h2d(c->d_rawinv, m.inv_copy, m.n);
-  h2d(c->d_rawlo, m.x_lo, m.n);
-  h2d(c->d_rawhi, m.x_hi, m.n);
   const StreamLayout& L = c->SL;
+  const double* sec[kRawEnd] = {m.P, m.A, m.b, m.v, m.z0, m.c, m.inv_copy, m.x_lo, m.x_hi};
+  for (int i = 0; i < kRawEnd; ++i) {
+    const std::size_t n = static_cast<std::size_t>(L.raw_off[i + 1] - L.raw_off[i]);
+    if (n)
+      ck(cudaMemcpyAsync(c->d_raw + L.raw_off[i], sec[i], n * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+         "upload");
+  }
   auto& d = c->sd;
-  GatherParams g{};
-  g.np = static_cast<int64_t>(L.p_src.size());
-  g.na = static_cast<int64_t>(L.a_src.size());
-  g.rows = L.rows;
-  g.cols = L.cols;
-  g.nab = static_cast<int64_t>(L.ab_src.size());
-  g.p_src = c->d_psrc;
-  g.a_src = c->d_asrc;
+  StreamRegather g{};
+  g.raw = c->d_raw;
+  g.blob_src = c->d_blobsrc;
+  g.blob = reinterpret_cast<double*>(d.blob);
+  g.nblob = static_cast<int64_t>(L.blob.size());
   g.ref_of_dev = c->d_refdev;
-  g.gcol = c->d_gcol;
-  g.ab_src = c->d_absrc;
-  g.rawP = c->d_rawP;
-  g.rawA = c->d_rawA;
-  g.rawb = c->d_rawb;
-  g.rawv = c->d_rawv;
-  g.rawz0 = c->d_rawz0;
-  g.rawc = c->d_rawc;
-  g.rawinv = c->d_rawinv;
-  g.rawlo = c->d_rawlo;
-  g.rawhi = c->d_rawhi;
-  g.P = d.P;
-  g.A = d.A;
-  g.ab = d.ab;
-  g.v = d.v;
   g.z0 = d.z0;
-  g.cc = d.cost;
-  g.cinv = d.inv;
-  g.clo = d.lo;
-  g.chi = d.hi;
-  ck(launch_gather(g, c->sm_count, c->stream), "gather");
+  g.rows = L.rows;
+  g.gcol = c->d_gcol;
+  g.cost = d.cost;
+  g.inv = d.inv;
+  g.lo = d.lo;
+  g.hi = d.hi;
+  g.bcols = L.bcols;
+  g.off_z0 = L.raw_off[kRawZ0];
+  g.off_c = L.raw_off[kRawC];
+  g.off_inv = L.raw_off[kRawInv];
+  g.off_lo = L.raw_off[kRawLo];
+  g.off_hi = L.raw_off[kRawHi];
+  ck(stream_launch_regather(g, c->sm_count, c->stream), "regather");
   ++c->kernels;
   ck(cudaStreamSynchronize(c->stream), "upload sync");
 }
@@ -1245,9 +1240,9 @@ int dopf_cuda_info(const dopf_cuda_ctx* c, dopf_cuda_info_t* out) {
   if (!c || !out) return DOPF_ERR_INVALID_ARGUMENT;
   if (c->streaming) {
     out->instances = 1;
-    out->blocks = static_cast<int32_t>(c->SL.chunks.size());
-    out->threads = kStreamRows;
-    out->smem_bytes = 0;
+    out->blocks = c->staged_grid;  // persistent CTAs of the staged kernel
+    out->threads = kStagedThreads;
+    out->smem_bytes = c->SL.stages * c->SL.stage_bytes;
     out->resident = 0;
     out->sync_mode = 3;  // streaming graph (while-node)
     return DOPF_OK;

@@ -123,140 +123,285 @@ __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p)
     const double unclamped = (acc - p.cost[c] / p.rho) * p.inv[c];
     const double xv = sel_min(sel_max(unclamped, p.lo[c]), p.hi[c]);
     p.x[c] = xv;
+    for (int e = p.imp_ptr[c]; e < p.imp_ptr[c + 1]; ++e) p.ximp[p.imp_slot[e]] = xv;  // chunk imports
     if (p.owner[c]) o[0] = p.cost[c] * xv;
   }
   block_reduce<1, kStreamRows>(o, sh, -1);
   if (threadIdx.x == 0) p.objp[blockIdx.x] = o[0];
 }
 
-template <int kMinBlocks>
-__global__ void __launch_bounds__(kStreamRows, kMinBlocks) k_local(const StreamParams p) {
-  __shared__ double tgt[kStreamRows];
-  __shared__ double ush[kStreamRows];  // u = z - lambda/rho of the chunk's rows, then z
-  __shared__ double xsh[kStreamRows];  // x of the chunk's interior columns
-  __shared__ double zsh[kStreamRows];  // z^{t-1} (kept out of registers across the GEMV)
-  __shared__ int32_t csh[kStreamRows + 1];  // interior CSR: chunk-local copy rows, column offsets
-  __shared__ int32_t psh[kStreamRows + 1];
-  __shared__ double osh[kStreamRows / 32];  // per-warp c'x of the interior columns
-  __shared__ double sh[6 * (kStreamRows / 32)];
-  if (p.ctl->done) return;
-  // chunk fields are re-read where used (uniform, L1-resident) rather than
-  // held in registers across the whole kernel
-  const StreamChunk* ch = p.chunks + blockIdx.x;
+template <typename T>
+__device__ __forceinline__ const T* sec(const unsigned char* img, const ChunkHead& h, int id) {
+  return reinterpret_cast<const T*>(img + h.off[id]);
+}
+
+// One chunk's iteration, shared by the direct-load kernel (image in HBM) and
+// the staged kernel (image in shared memory): thread r = row r, interior
+// column r, equality row r. `img` is the chunk image, zin / lin / xin the
+// chunk's z^{t-1}, lambda^{t-1} and imported boundary x. Four barriers
+// (`sync`) separate: u -> interior x -> target -> GEMV/dual -> A z - b.
+// Accumulates the residual partials into v (gap, step, bx2, z2, lam2, maxinf, c'x).
+template <int kRows, typename Sync, typename Ld>
+__device__ __forceinline__ void chunk_iteration(const StreamParams& p, const StreamChunk& ch,
+                                                const unsigned char* img, const ChunkHead& h,
+                                                const double* zin, const double* lin, const double* xin,
+                                                double* tgt, double* ush, double* xsh, double* zsh,
+                                                double (&v)[7], Sync sync, Ld ld) {
   const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
   const double rho = p.rho;
-  const bool on = r < ch->rows;
-  const int d = ch->row0 + r;
-  // the chunk's operator slabs start moving HBM -> L2 now, overlapping the
-  // dependent row loads and the interior-column update below
-  if (r == 0) {
-    bulk_prefetch_l2(p.P + ch->p0, static_cast<uint32_t>(8 * (ch->p1 - ch->p0)));
-    bulk_prefetch_l2(p.A + ch->a0, static_cast<uint32_t>(8 * (ch->a1 - ch->a0)));
-  }
-  if (r < ch->icols) {
-    const int c = ch->icol0 + r;
-    prefetch_l1(p.cost + c);
-    prefetch_l1(p.inv + c);
-    prefetch_l1(p.lo + c);
-    prefetch_l1(p.hi + c);
-    prefetch_l1(p.owner + c);
-  }
-  // interior columns (admm.cpp:118-129): their CSR slice is staged in shared
-  // memory by the same load round as the rows (copies <= rows)
-  if (r < ch->icopies) csh[r] = p.copies[ch->icopy0 + r] - ch->row0;
-  if (r <= ch->icols) psh[r] = p.col_ptr[ch->icol0 + r] - ch->icopy0;
-  StreamRow rm{0, 0, 0, 0};
-  double bx = 0.0, lamv = 0.0;
+  const bool on = r < h.rows;
+  StreamRow rm{0, 0, -1, -1};
+  double lamv = 0.0, q = 0.0;
   if (on) {
-    rm = p.rmeta[d];
-    lamv = p.lam[d];
-    const double zprev = p.z[d];
-    if (rm.xcol < p.bcols) bx = p.x[rm.xcol];  // boundary column: k_global wrote x^t
-    ush[r] = zprev - lamv / rho;               // the u the previous iteration stored
+    rm = sec<StreamRow>(img, h, kImgRmeta)[r];
+    lamv = lin[r];
+    const double zprev = zin[r];
+    q = lamv / rho;
+    ush[r] = zprev - q;  // the u = z - lambda/rho the previous iteration produced
     zsh[r] = zprev;
   }
-  __syncthreads();
-  double o = 0.0;
-  if (r < ch->icols) {
-    const int c = ch->icol0 + r;
-    const int q1 = psh[r + 1];
+  sync();
+  if (r < h.icols) {  // interior column: admm.cpp:118-129 over the chunk's own copies
+    const int32_t* cp = sec<int32_t>(img, h, kImgCptr);
+    const int32_t* cc = sec<int32_t>(img, h, kImgCopies);
+    const int q1 = cp[r + 1];
     double acc = 0.0;
-    for (int q = psh[r]; q < q1; ++q) acc = acc + ush[csh[q]];  // ascending s
-    const double unclamped = (acc - p.cost[c] / rho) * p.inv[c];
-    const double xv = sel_min(sel_max(unclamped, p.lo[c]), p.hi[c]);
+    for (int e = cp[r]; e < q1; ++e) acc = acc + ush[cc[e]];  // ascending s
+    const double cost = sec<double>(img, h, kImgCost)[r];
+    const double unclamped = (acc - cost / rho) * sec<double>(img, h, kImgInv)[r];
+    const double xv = sel_min(sel_max(unclamped, sec<double>(img, h, kImgLo)[r]), sec<double>(img, h, kImgHi)[r]);
     xsh[r] = xv;
-    p.x[c] = xv;
-    if (p.owner[c]) o = p.cost[c] * xv;
+    p.x[ch.icol0 + r] = xv;
+    if (sec<uint8_t>(img, h, kImgOwner)[r]) v[6] = v[6] + cost * xv;
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) o = o + __shfl_xor_sync(0xffffffffu, o, off);
-  if (lane == 0) osh[warp] = o;
-  __syncthreads();
+  sync();
+  double bx = 0.0;
   if (on) {
-    if (rm.xcol >= p.bcols) bx = xsh[rm.xcol - ch->icol0];
-    tgt[r] = bx + lamv / rho;  // admm.cpp:136
+    bx = rm.xin >= 0 ? xin[rm.xin] : xsh[rm.xloc];
+    tgt[r] = bx + q;  // admm.cpp:136
   }
-  __syncthreads();
-  double v[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  sync();
   if (on) {
-    const double* pr = p.P + p.pslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
+    const double* pr = sec<double>(img, h, kImgP) + sec<int32_t>(img, h, kImgPslice)[warp] + lane;
     const double* tb = tgt + rm.base;
     double acc = 0.0;
-    for (int j0 = 0; j0 < rm.n; j0 += 8) {
-      double pv[8], tv[8];
+    for (int j0 = 0; j0 < rm.n; j0 += 8) {  // 8 operator loads in flight, then the sequential-j sum
+      double pv[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        pv[e] = 0.0;
-        tv[e] = 0.0;
-        if (j0 + e < rm.n) {
-          pv[e] = __ldcs(pr + 32 * (j0 + e));  // streamed once per iteration
-          tv[e] = tb[j0 + e];
-        }
-      }
+      for (int e = 0; e < 8; ++e) pv[e] = j0 + e < rm.n ? ld(pr + 32 * (j0 + e)) : 0.0;
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        if (j0 + e < rm.n) acc = acc + pv[e] * tv[e];
+        if (j0 + e < rm.n) acc = acc + pv[e] * tb[j0 + e];  // admm.cpp:137
     }
-    const double z = acc + p.v[d];
+    const double z = acc + sec<double>(img, h, kImgV)[r];
     const double dd = bx - z;
     const double ln = lamv + rho * dd;  // admm.cpp:142
+    const int d = ch.row0 + r;
     p.z[d] = z;
     p.lam[d] = ln;
-    if (rm.xcol < p.bcols) p.u[d] = z - ln / rho;  // read by the next boundary update / exports
-    v[0] = dd * dd;
+    if (rm.xin >= 0) p.u[d] = z - ln / rho;  // read by the next boundary update / exports
+    v[0] = v[0] + dd * dd;
     const double dz = z - zsh[r];
-    v[1] = dz * dz;
-    v[2] = bx * bx;
-    v[3] = z * z;
-    v[4] = ln * ln;
+    v[1] = v[1] + dz * dz;
+    v[2] = v[2] + bx * bx;
+    v[3] = v[3] + z * z;
+    v[4] = v[4] + ln * ln;
     ush[r] = z;  // every read of u happened before the previous barrier
   }
-  __syncthreads();
-  if (r < ch->arows) {
-    const StreamARow am = p.ameta[blockIdx.x * kStreamRows + r];
-    const double* ar = p.A + p.aslice[blockIdx.x * (kStreamRows / 32) + warp] + lane;
+  sync();
+  if (r < h.arows) {  // ||A_s z_s - b_s||_inf (admm.cpp:203-205)
+    const StreamARow am = sec<StreamARow>(img, h, kImgAmeta)[r];
+    const double* ar = sec<double>(img, h, kImgA) + sec<int32_t>(img, h, kImgAslice)[warp] + lane;
     const double* zb = ush + am.base;
     double acc = 0.0;
     for (int j0 = 0; j0 < am.n; j0 += 8) {
       double av[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? __ldcs(ar + 32 * (j0 + e)) : 0.0;
+      for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? ld(ar + 32 * (j0 + e)) : 0.0;
 #pragma unroll
       for (int e = 0; e < 8; ++e)
         if (j0 + e < am.n) acc = acc + av[e] * zb[j0 + e];
     }
-    v[5] = fabs(acc - p.ab[ch->arow0 + r]);
+    v[5] = sel_max(v[5], fabs(acc - sec<double>(img, h, kImgAb)[r]));
   }
-  block_reduce<6, kStreamRows>(v, sh, 5);
-  if (threadIdx.x == 0) {
-    double* out = p.part + static_cast<int64_t>(blockIdx.x) * 8;
+}
+
+// CTA reduction of the 7 partials (fixed shape), written to part[slot]
+template <int kRows, typename Sync>
+__device__ __forceinline__ void write_partials(const StreamParams& p, double (&v)[7], double* red, int slot,
+                                               Sync sync) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int q = 0; q < 6; ++q) out[q] = v[q];
-    double obj = 0.0;
+  for (int qv = 0; qv < 7; ++qv)
 #pragma unroll
-    for (int w = 0; w < kStreamRows / 32; ++w) obj = obj + osh[w];
-    out[6] = obj;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v[qv], off);
+      v[qv] = qv == 5 ? sel_max(v[qv], o) : v[qv] + o;
+    }
+  constexpr int W = kRows / 32;
+  if (lane == 0)
+#pragma unroll
+    for (int qv = 0; qv < 7; ++qv) red[qv * W + warp] = v[qv];
+  sync();
+  if (warp == 0) {
+#pragma unroll
+    for (int qv = 0; qv < 7; ++qv) {
+      double x = lane < W ? red[qv * W + lane] : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, x, off);
+        x = qv == 5 ? sel_max(x, o) : x + o;
+      }
+      if (lane == 0) p.part[static_cast<int64_t>(slot) * 8 + qv] = x;
+    }
   }
+}
+
+// Direct-load kernel for chunks whose stage would not fit shared memory:
+// one CTA per chunk, image read straight from HBM.
+__global__ void __launch_bounds__(kStreamRows, 1) k_local(const StreamParams p) {
+  __shared__ double tgt[kStreamRows], ush[kStreamRows], xsh[kStreamRows], zsh[kStreamRows];
+  __shared__ double red[7 * (kStreamRows / 32)];
+  __shared__ ChunkHead hsh;
+  if (p.ctl->done) return;
+  const StreamChunk ch = p.chunks[p.big_ids[blockIdx.x]];
+  const unsigned char* img = p.blob + ch.image_off;
+  if (threadIdx.x < sizeof(ChunkHead) / 4)
+    reinterpret_cast<int32_t*>(&hsh)[threadIdx.x] = reinterpret_cast<const int32_t*>(img)[threadIdx.x];
+  __syncthreads();
+  double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  auto sync = [] { __syncthreads(); };
+  auto ld = [](const double* a) { return __ldcs(a); };
+  chunk_iteration<kStreamRows>(p, ch, img, hsh, p.z + ch.row0, p.lam + ch.row0, p.ximp + ch.bimp0, tgt, ush,
+                               xsh, zsh, v, sync, ld);
+  __syncthreads();
+  write_partials<kStreamRows>(p, v, red, p.staged_grid + blockIdx.x, sync);
+}
+
+// ---------------------------------------------------------------- staged kernel
+//
+// Persistent, two CTAs per SM, each 8 compute warps + 1 producer warp. Every
+// chunk the CTA owns (static round robin over staged_ids) is brought into
+// shared memory by ~18 bulk copies (cp.async.bulk, TMA engine) into one of
+// kStages pipeline stages, completing on the stage's "full" mbarrier; the
+// producer warp also gathers the chunk's boundary x values. While the compute
+// warps work on chunk i entirely out of shared memory, the next chunks are in
+// flight. The compute warps release a stage through its "empty" mbarrier.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned long long spins = 0;
+  while (!mbar_try(b, parity))
+    if (++spins > (1ull << 28)) __trap();  // watchdog: never hang the device
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// barrier of the 16 compute warps only (the producer warp never joins)
+__device__ __forceinline__ void compute_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kStagedRows) : "memory");
+}
+
+__global__ void __launch_bounds__(kStagedThreads, kStagedCtasPerSm) k_staged(const StreamParams p) {
+  extern __shared__ __align__(128) unsigned char stages[];  // [p.stages][p.stage_bytes]
+  __shared__ double tgt[kStagedRows], ush[kStagedRows], xsh[kStagedRows], zsh[kStagedRows];
+  __shared__ double red[7 * (kStagedRows / 32)];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  if (p.ctl->done) return;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+
+  if (tid >= kStagedRows) {  // ---------------- producer warp (one elected lane)
+    if ((tid & 31) != 0) return;
+    int k = blockIdx.x;
+    StreamChunk ch{};
+    if (k < p.n_staged) ch = p.chunks[p.staged_ids[k]];
+    for (int i = 0; k < p.n_staged; k += G, ++i) {
+      const int s = i % p.stages;
+      const unsigned use = static_cast<unsigned>(i / p.stages);
+      // next chunk's descriptor: its load overlaps the wait and the issue below
+      StreamChunk next{};
+      if (k + G < p.n_staged) next = p.chunks[p.staged_ids[k + G]];
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
+      StagePlan sp;
+      stage_plan(ch, sp);
+      unsigned char* st = stages + s * p.stage_bytes;
+      mbar_expect_tx(&full[s], sp.total);
+      // four bulk copies: image, z slice, lambda slice, imported boundary x
+      bulk_g2s(st, p.blob + ch.image_off, static_cast<unsigned>(ch.image_bytes), &full[s]);
+      auto slice = [&](const StageSeg& g, const double* base, int64_t first) {
+        if (g.bytes)
+          bulk_g2s(st + g.dst, reinterpret_cast<const unsigned char*>(base + first) - g.shift, g.bytes, &full[s]);
+      };
+      slice(sp.z, p.z, ch.row0);
+      slice(sp.lam, p.lam, ch.row0);
+      slice(sp.ximp, p.ximp, ch.bimp0);
+      mbar_arrive(&full[s]);
+      ch = next;
+    }
+    return;
+  }
+
+  // ---------------- compute warps
+  double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  auto sync = [] { compute_sync(); };
+  auto ld = [](const double* a) { return *a; };
+  int i = 0;
+  for (int k = blockIdx.x; k < p.n_staged; k += G, ++i) {
+    const int s = i % p.stages;
+    mbar_wait(&full[s], static_cast<unsigned>(i / p.stages) & 1u);
+    const unsigned char* st = stages + s * p.stage_bytes;
+    const ChunkHead& h = *reinterpret_cast<const ChunkHead*>(st);
+    StreamChunk ch{};  // the fields the stage plan and the iteration use, from the image head
+    ch.row0 = h.row0;
+    ch.rows = h.rows;
+    ch.icol0 = h.icol0;
+    ch.bimp0 = h.bimp0;
+    ch.nbimp = h.nbimp;
+    ch.image_bytes = h.image_bytes;
+    StagePlan sp;
+    stage_plan(ch, sp);
+    chunk_iteration<kStagedRows>(p, ch, st, h, reinterpret_cast<const double*>(st + sp.z.dst + sp.z.shift),
+                                 reinterpret_cast<const double*>(st + sp.lam.dst + sp.lam.shift),
+                                 reinterpret_cast<const double*>(st + sp.ximp.dst + sp.ximp.shift), tgt, ush,
+                                 xsh, zsh, v, sync, ld);
+    compute_sync();  // the stage and the scratch arrays are free again
+    if (tid == 0) mbar_arrive(&empty[s]);
+  }
+  write_partials<kStagedRows>(p, v, red, blockIdx.x, sync);
 }
 
 constexpr int kFinalThreads = 256;
@@ -271,8 +416,8 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
   if (p.ctl->done) return;
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gap, step, bx2, z2, lam2, maxinf, objective
   const int g = blockIdx.x;
-  const int c0 = static_cast<int>(static_cast<int64_t>(p.nchunks) * g / kFinalBlocks);
-  const int c1 = static_cast<int>(static_cast<int64_t>(p.nchunks) * (g + 1) / kFinalBlocks);
+  const int c0 = static_cast<int>(static_cast<int64_t>(p.npart) * g / kFinalBlocks);
+  const int c1 = static_cast<int>(static_cast<int64_t>(p.npart) * (g + 1) / kFinalBlocks);
   for (int k = c0 + threadIdx.x; k < c1; k += kFinalThreads) {
     const double* q = p.part + static_cast<int64_t>(k) * 8;
 #pragma unroll
@@ -332,22 +477,49 @@ __global__ void k_decide(const StreamParams p, const double* ranks, int nranks) 
   finalize_iteration(p, v);
 }
 
+__global__ void k_regather(const StreamRegather g) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < g.nblob; i += stride) {
+    const int32_t src = g.blob_src[i];
+    if (src >= 0) g.blob[i] = g.raw[src];
+    else if (src == -1) g.blob[i] = 0.0;  // -2: metadata, kept
+  }
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < g.rows; i += stride)
+    g.z0[i] = g.raw[g.off_z0 + g.ref_of_dev[i]];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < g.bcols; i += stride) {
+    const int32_t c = g.gcol[i];
+    g.cost[i] = g.raw[g.off_c + c];
+    g.inv[i] = g.raw[g.off_inv + c];
+    g.lo[i] = g.raw[g.off_lo + c];
+    g.hi[i] = g.raw[g.off_hi + c];
+  }
+}
+
 }  // namespace
+
+cudaError_t stream_launch_regather(const StreamRegather& g, int sm_count, cudaStream_t s) {
+  k_regather<<<8 * sm_count, 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
 
 using LocalKernel = void (*)(const StreamParams);
 
-LocalKernel local_kernel() {
-  // CTAs per SM for k_local: 4 (32 registers) measured fastest; DOPF_KLOCAL=3 for experiments
-  static const LocalKernel k = [] {
-    const char* e = std::getenv("DOPF_KLOCAL");
-    return (e && e[0] == '3') ? &k_local<3> : &k_local<4>;
-  }();
-  return k;
+LocalKernel local_kernel() { return &k_local; }
+
+cudaError_t stream_prepare() {
+  static cudaError_t e = cudaFuncSetAttribute(k_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              100 * 1024);
+  return e;
+}
+
+void launch_local_all(const StreamParams& p, cudaStream_t s) {
+  if (p.n_big > 0) local_kernel()<<<p.n_big, kStreamRows, 0, s>>>(p);
+  if (p.n_staged > 0) k_staged<<<p.staged_grid, kStagedThreads, p.stages * p.stage_bytes, s>>>(p);
 }
 
 void stream_launch_iteration(const StreamParams& p, cudaStream_t s) {
   k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
-  local_kernel()<<<p.nchunks, kStreamRows, 0, s>>>(p);
+  launch_local_all(p, s);
   k_final<<<kFinalBlocks, kFinalThreads, 0, s>>>(p);
 }
 
@@ -355,7 +527,7 @@ void stream_launch_global(const StreamParams& p, cudaStream_t s) {
   k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
 }
 void stream_launch_local(const StreamParams& p, cudaStream_t s) {
-  local_kernel()<<<p.nchunks, kStreamRows, 0, s>>>(p);
+  launch_local_all(p, s);
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
   k_final<<<kFinalBlocks, kFinalThreads, 0, s>>>(p);
 }
@@ -386,22 +558,32 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   p.use_cond = 1;
   p.partials_out = nullptr;
   void* args[] = {&p};
-  cudaKernelNodeParams kg = {}, kl = {}, kf = {};
+  cudaKernelNodeParams kg = {}, kb = {}, ks = {}, kf = {};
   kg.func = reinterpret_cast<void*>(k_global);
   kg.gridDim = dim3(p.col_blocks);
   kg.blockDim = dim3(kStreamRows);
   kg.kernelParams = args;
-  kl = kg;
-  kl.func = reinterpret_cast<void*>(local_kernel());
-  kl.gridDim = dim3(p.nchunks);
+  kb = kg;
+  kb.func = reinterpret_cast<void*>(local_kernel());
+  kb.gridDim = dim3(p.n_big);
+  ks = kg;
+  ks.func = reinterpret_cast<void*>(k_staged);
+  ks.gridDim = dim3(p.staged_grid);
+  ks.blockDim = dim3(kStagedThreads);
+  ks.sharedMemBytes = p.stages * p.stage_bytes;
   kf = kg;
   kf.func = reinterpret_cast<void*>(k_final);
   kf.gridDim = dim3(kFinalBlocks);
   kf.blockDim = dim3(kFinalThreads);
-  cudaGraphNode_t ng, nl, nf;
+  // the direct-load chunks run beside the staged kernel (which leaves one SM
+  // for them), not after it
+  cudaGraphNode_t ng, dep[2], nf;
+  int ndep = 0;
   if ((e = cudaGraphAddKernelNode(&ng, body, nullptr, 0, &kg)) != cudaSuccess) return e;
-  if ((e = cudaGraphAddKernelNode(&nl, body, &ng, 1, &kl)) != cudaSuccess) return e;
-  if ((e = cudaGraphAddKernelNode(&nf, body, &nl, 1, &kf)) != cudaSuccess) return e;
+  if (p.n_big > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &kb)) != cudaSuccess) return e;
+  if (p.n_staged > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &ks)) != cudaSuccess) return e;
+  if (ndep == 0) dep[ndep++] = ng;
+  if ((e = cudaGraphAddKernelNode(&nf, body, dep, ndep, &kf)) != cudaSuccess) return e;
   e = cudaGraphInstantiate(exec, g, 0);
   cudaGraphDestroy(g);
   return e;

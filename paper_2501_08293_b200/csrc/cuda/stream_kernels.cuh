@@ -18,16 +18,18 @@ struct StreamCtl {      // device-side loop state
   double objective;     // c'x of the last iteration
 };
 
+constexpr int kStagedThreads = kStagedRows + 32;  // compute warps + 1 producer warp
+constexpr int kStagedCtasPerSm = 2;
+
 struct StreamParams {
   const StreamChunk* chunks;
-  const StreamRow* rmeta;
-  const int64_t* pslice;
-  const int64_t* aslice;
-  const StreamARow* ameta;
-  const double* P;
-  const double* A;
-  const double* ab;
-  const double* v;
+  const int32_t* staged_ids;  // chunks of the staged (bulk-copy pipelined) kernel
+  const int32_t* big_ids;     // chunks too large for a stage (direct-load kernel)
+  const int32_t* imp_ptr;     // boundary column -> import slots (CSR)
+  const int32_t* imp_slot;
+  double* ximp;               // [imports] boundary x per importing chunk (read by bulk copy)
+  const unsigned char* blob;  // chunk images (ChunkHead + sections)
+  // boundary columns [0, bcols)
   const int32_t* col_ptr;
   const int32_t* copies;
   const double* cost;
@@ -40,7 +42,7 @@ struct StreamParams {
   double* lam;           // [rows]
   double* u;             // [rows] z - lambda/rho (rows of boundary columns)
   const double* u_remote;  // partitioned: gathered copies of other ranks
-  double* part;          // [nchunks][8]
+  double* part;          // [npart][8]
   double* objp;          // [col_blocks] boundary columns' c'x
   double* part2;         // [128][8] level-2 partials (k_final)
   unsigned* final_count; // k_final's last-block counter (zero between iterations)
@@ -53,6 +55,10 @@ struct StreamParams {
   double rho, eps;
   int32_t max_iter;
   int32_t nchunks;
+  int32_t n_staged, n_big;
+  int32_t staged_grid;   // persistent CTAs of the staged kernel (partials [0, staged_grid))
+  int32_t npart;         // partial slots: staged_grid + n_big
+  int32_t stages, stage_bytes;  // staged-kernel pipeline (dynamic smem = stages * stage_bytes)
   int32_t cols;
   int32_t bcols;         // boundary columns [0, bcols) (k_global); the rest are per-chunk interior
   int32_t col_blocks;    // k_global CTAs (>= 1)
@@ -60,7 +66,26 @@ struct StreamParams {
   int32_t use_cond;
 };
 
-/// The whole solve as one graph: a while-node over {k_global, k_local, k_final}.
+/// Same-structure re-upload: model values (raw concatenation, stream_layout.hpp)
+/// scattered into the chunk images, z0 and the boundary-column arrays.
+struct StreamRegather {
+  const double* raw;
+  const int32_t* blob_src;
+  double* blob;
+  int64_t nblob;          // 8-byte words
+  const int32_t* ref_of_dev;
+  double* z0;
+  int32_t rows;
+  const int32_t* gcol;
+  double *cost, *inv, *lo, *hi;
+  int32_t bcols;
+  int64_t off_z0, off_c, off_inv, off_lo, off_hi;
+};
+cudaError_t stream_launch_regather(const StreamRegather& g, int sm_count, cudaStream_t s);
+
+/// One-time kernel attributes (dynamic shared memory of the staged kernel).
+cudaError_t stream_prepare();
+/// The whole solve as one graph: a while-node over {k_global, k_big, k_staged, k_final}.
 cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec);
 /// One iteration, stream-ordered (no graph).
 void stream_launch_iteration(const StreamParams& p, cudaStream_t s);

@@ -1,9 +1,10 @@
 #include "stream_layout.hpp"
 
 #include <algorithm>
-#include <cstring>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 
 #include "layout_builder.hpp"
@@ -20,9 +21,51 @@ bool StreamLayout::same_structure(const dopf_model_view& m) const {
          eq(sig_csr_copy, m.csr_copy, m.N_z);
 }
 
+void raw_offsets(const dopf_model_view& m, int64_t (&off)[10]) {
+  const int64_t len[kRawEnd] = {m.p_offsets[m.S], m.a_offsets[m.S], m.b_offsets[m.S], m.N_z, m.N_z,
+                                m.n, m.n, m.n, m.n};
+  off[0] = 0;
+  for (int i = 0; i < kRawEnd; ++i) off[i + 1] = off[i] + len[i];
+}
+
 StreamLayout build_stream_layout(const dopf_model_view& m) {
   return build_stream_layout_part(m, 1, 0, nullptr);
 }
+
+namespace {
+
+// one chunk image under construction: 8-byte words + where each word's value
+// comes from in the raw concatenation (-1 zero padding, -2 metadata)
+struct ImageWriter {
+  std::vector<double>& words;
+  std::vector<int32_t>& src;
+  std::size_t start;
+
+  void align16() {
+    if ((words.size() - start) & 1) put(0.0, -1);
+  }
+  uint32_t here() const { return static_cast<uint32_t>(8 * (words.size() - start)); }
+  void put(double v, int32_t s) {
+    words.push_back(v);
+    src.push_back(s);
+  }
+  void put_value(const double* raw_sec, int64_t sec_off, int64_t i) {
+    put(raw_sec[i], static_cast<int32_t>(sec_off + i));
+  }
+  template <typename T>
+  void put_meta(const std::vector<T>& v) {  // bit-packed, 16-byte padded
+    const std::size_t bytes = v.size() * sizeof(T), padded = (bytes + 15) & ~static_cast<std::size_t>(15);
+    std::vector<unsigned char> buf(padded, 0);
+    if (bytes) std::memcpy(buf.data(), v.data(), bytes);
+    for (std::size_t o = 0; o < padded; o += 8) {
+      double w;
+      std::memcpy(&w, buf.data() + o, 8);
+      put(w, -2);
+    }
+  }
+};
+
+}  // namespace
 
 StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int part,
                                       const int32_t* part_of_s) {
@@ -33,83 +76,88 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
   for (int s = 0; s < m.S; ++s)
     if (part_of(s) < 0 || part_of(s) >= nparts) throw std::invalid_argument("subsystem part out of range");
   StreamLayout L;
+  // pipeline shape of the staged kernel (DOPF_STAGES / DOPF_STAGE_KB for experiments)
+  if (const char* e = std::getenv("DOPF_STAGES")) L.stages = std::max(2, std::min(kMaxStages, std::atoi(e)));
+  if (const char* e = std::getenv("DOPF_STAGE_KB")) L.stage_bytes = std::max(8, std::atoi(e)) * 1024;
+  if (L.stages * L.stage_bytes > 100 * 1024) throw std::invalid_argument("staged pipeline exceeds 100 KB per CTA");
   L.S = m.S;
   L.n = m.n;
   L.N_z = m.N_z;
   L.nparts = nparts;
   L.part = part;
+  raw_offsets(m, L.raw_off);
+  if (L.raw_off[kRawEnd] >= INT32_MAX) throw std::invalid_argument("model too large for 32-bit value maps");
   std::vector<int> order;
   for (int s : locality_order(m))
     if (part_of(s) == part) order.push_back(s);
   auto ns_of = [&](int s) { return m.z_offsets[s + 1] - m.z_offsets[s]; };
   for (int s = 0; s < m.S; ++s)
-    if (ns_of(s) > kStreamRows) throw std::invalid_argument("subsystem wider than a streaming chunk");
+    if (ns_of(s) > kStreamRows || m.m_s[s] > kStreamRows)
+      throw std::invalid_argument("subsystem wider than a streaming chunk");
 
-  // chunks of whole subsystems, <= kStreamRows rows (and equality rows)
+  // ---- chunks of whole subsystems along the locality walk
   std::vector<int32_t> dev_of_ref(m.N_z, -1);
-  struct Src { int64_t at; int n; int base; };
-  std::vector<Src> prow, arow;
-  int32_t row = 0;
-  std::size_t k = 0;
-  std::vector<int> members;
-  while (k < order.size()) {
-    StreamChunk ch{};
-    ch.row0 = row;
-    ch.arow0 = static_cast<int32_t>(arow.size());
-    // the chunk's subsystems: the next run of the locality walk that fits
-    int rows = 0, arows = 0;
-    members.clear();
+  std::vector<std::vector<int>> members_of;  // per chunk, widest first
+  {
+    int32_t row = 0;
+    std::size_t k = 0;
     while (k < order.size()) {
-      const int s = order[k];
-      const int n = ns_of(s), ms = m.m_s[s];
-      if (rows + n > kStreamRows || arows + ms > kStreamRows) break;
-      members.push_back(s);
-      rows += n;
-      arows += ms;
-      ++k;
-    }
-    // widest first inside the chunk: the 32 rows of a warp slice then have
-    // (nearly) equal n_s, so the sliced-ELL padding -- which still costs
-    // DRAM sectors -- stays small
-    std::stable_sort(members.begin(), members.end(), [&](int a, int b) { return ns_of(a) > ns_of(b); });
-    rows = 0;
-    for (int s : members) {
-      const int n = ns_of(s), ms = m.m_s[s];
-      for (int i = 0; i < n; ++i) {
-        dev_of_ref[m.z_offsets[s] + i] = row + rows + i;
-        prow.push_back(Src{m.p_offsets[s] + static_cast<int64_t>(i) * n, n, rows});
+      StreamChunk ch{};
+      ch.row0 = row;
+      int rows = 0, arows = 0;
+      double est = 1024.0;
+      std::vector<int> members;
+      while (k < order.size()) {
+        const int s = order[k];
+        const int n = ns_of(s), ms = m.m_s[s];
+        // stage estimate (operators with sliced-ELL padding headroom + per-row/column data)
+        const double add =
+            1.25 * 8.0 * (static_cast<double>(n) * n + static_cast<double>(ms) * n) + 100.0 * n + 24.0 * ms;
+        // several subsystems share a chunk only within the staged kernel's
+        // limits; a wider one gets a chunk of its own (direct-load kernel)
+        if (!members.empty() &&
+            (rows + n > kStagedRows || arows + ms > kStagedRows || est + add > 0.9 * L.stage_bytes))
+          break;
+        members.push_back(s);
+        rows += n;
+        arows += ms;
+        est += add;
+        ++k;
       }
-      for (int r = 0; r < ms; ++r) {
-        arow.push_back(Src{m.a_offsets[s] + static_cast<int64_t>(r) * n, n, rows});
-        L.ab.push_back(m.b[m.b_offsets[s] + r]);
-        L.ab_src.push_back(m.b_offsets[s] + r);
-      }
-      rows += n;
+      // widest first inside the chunk: the 32 rows of a warp slice then have
+      // (nearly) equal n_s, so the sliced-ELL padding stays small
+      std::stable_sort(members.begin(), members.end(), [&](int a, int b) { return ns_of(a) > ns_of(b); });
+      int r = 0;
+      for (int s : members)
+        for (int i = 0; i < ns_of(s); ++i) dev_of_ref[m.z_offsets[s] + i] = row + r++;
+      ch.rows = rows;
+      ch.arows = arows;
+      row += rows;
+      L.chunks.push_back(ch);
+      members_of.push_back(std::move(members));
     }
-    ch.rows = rows;
-    ch.arows = arows;
-    row += rows;
-    L.chunks.push_back(ch);
+    L.rows = row;
   }
-  L.rows = row;
-  L.rmeta.resize(row);
-  L.v.resize(row);
-  L.z0.resize(row);
-  L.ref_of_dev.resize(row);
+  const int nchunks = static_cast<int>(L.chunks.size());
+  std::vector<int32_t> chunk_of_row(L.rows);
+  for (int q = 0; q < nchunks; ++q)
+    for (int r = 0; r < L.chunks[q].rows; ++r) chunk_of_row[L.chunks[q].row0 + r] = q;
   std::vector<int> s_of_ref(m.N_z);
   for (int s = 0; s < m.S; ++s)
     for (int k2 = m.z_offsets[s]; k2 < m.z_offsets[s + 1]; ++k2) s_of_ref[k2] = s;
+  L.z0.resize(L.rows);
+  L.ref_of_dev.resize(L.rows);
+  for (int ref = 0; ref < m.N_z; ++ref) {
+    const int32_t d = dev_of_ref[ref];
+    if (d < 0) continue;
+    L.ref_of_dev[d] = ref;
+    L.z0[d] = m.z0[ref];
+  }
 
-  // columns updated here: every column a local row references, ordered by
-  // their first local copy's device row (ties by column) -- the global update
-  // then walks u and the local update gathers x in near-sequential order
-  // Boundary columns (copies in several chunks, or on other parts) come
-  // first; interior columns follow grouped by their chunk.
+  // ---- columns: boundary (copies in several chunks or on other parts) first,
+  // then interior ones grouped by chunk; each group by first local copy
   std::vector<int32_t> loc_of_col(m.n, -1);
   {
-    std::vector<int32_t> chunk_of_row(row);
-    for (std::size_t q = 0; q < L.chunks.size(); ++q)
-      for (int r = 0; r < L.chunks[q].rows; ++r) chunk_of_row[L.chunks[q].row0 + r] = static_cast<int32_t>(q);
     std::vector<int32_t> first_row(m.n, INT32_MAX), chunk_of_col(m.n, -1);
     std::vector<char> boundary(m.n, 0);
     for (int ref = 0; ref < m.N_z; ++ref) {
@@ -140,60 +188,14 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
       ++ch.icols;
     }
   }
-  for (int ref = 0; ref < m.N_z; ++ref) {
-    const int32_t d = dev_of_ref[ref];
-    if (d < 0) continue;
-    L.ref_of_dev[d] = ref;
-    L.v[d] = m.v[ref];
-    L.z0[d] = m.z0[ref];
-    L.rmeta[d] = StreamRow{prow[d].n, prow[d].base, loc_of_col[m.l2g[ref]], 0};
-  }
-  // sliced ELL per chunk-local warp (rows of a warp never span chunks)
-  auto pack = [](const std::vector<Src>& rows, const std::vector<StreamChunk>& chunks, bool arow_mode,
-                 std::vector<double>& out, std::vector<int64_t>& slices, const double* src,
-                 std::vector<int64_t>& srcidx) {
-    for (const StreamChunk& ch : chunks) {
-      const int first = arow_mode ? ch.arow0 : ch.row0;
-      const int count = arow_mode ? ch.arows : ch.rows;
-      for (int w0 = 0; w0 < kStreamRows; w0 += 32) {
-        slices.push_back(static_cast<int64_t>(out.size()));
-        const int lanes = std::max(0, std::min(32, count - w0));
-        int width = 0;
-        for (int l = 0; l < lanes; ++l) width = std::max(width, rows[first + w0 + l].n);
-        for (int j = 0; j < width; ++j)
-          for (int l = 0; l < 32; ++l) {
-            const bool ok = l < lanes && j < rows[first + w0 + l].n;
-            out.push_back(ok ? src[rows[first + w0 + l].at + j] : 0.0);
-            srcidx.push_back(ok ? rows[first + w0 + l].at + j : -1);
-          }
-      }
-    }
-  };
-  pack(prow, L.chunks, false, L.P, L.pslice, m.P, L.p_src);
-  pack(arow, L.chunks, true, L.A, L.aslice, m.A, L.a_src);
-  for (std::size_t c = 0; c < L.chunks.size(); ++c) {
-    const std::size_t w = c * (kStreamRows / 32), wn = (c + 1) * (kStreamRows / 32);
-    L.chunks[c].p0 = L.pslice[w];
-    L.chunks[c].p1 = wn < L.pslice.size() ? L.pslice[wn] : static_cast<int64_t>(L.P.size());
-    L.chunks[c].a0 = L.aslice[w];
-    L.chunks[c].a1 = wn < L.aslice.size() ? L.aslice[wn] : static_cast<int64_t>(L.A.size());
-  }
-  L.ameta.resize(static_cast<std::size_t>(L.chunks.size()) * kStreamRows);
-  for (std::size_t c = 0; c < L.chunks.size(); ++c)
-    for (int a = 0; a < kStreamRows; ++a) {
-      StreamARow am{0, 0};
-      if (a < L.chunks[c].arows) {
-        const Src& s = arow[L.chunks[c].arow0 + a];
-        am = StreamARow{s.n, s.base};
-      }
-      L.ameta[c * kStreamRows + a] = am;
-    }
+  L.cols = static_cast<int32_t>(L.gcol.size());
+  for (int32_t gc : L.gcol) L.owner.push_back(part_of(s_of_ref[m.csr_copy[m.csr_ptr[gc]]]) == part ? 1 : 0);
 
-  // exports of every part (identical on all parts): copies of columns held by
-  // more than one part, ascending reference index per part
-  std::vector<std::vector<int32_t>> exports(nparts);
+  // ---- exports of every part (identical on all parts): copies of columns
+  // held by more than one part, ascending reference index per part
   std::vector<int32_t> slot_of_ref(m.N_z, -1);
   if (nparts > 1) {
+    std::vector<std::vector<int32_t>> exports(nparts);
     std::vector<char> multi(m.n, 0);
     for (int c = 0; c < m.n; ++c) {
       const int p0 = part_of(s_of_ref[m.csr_copy[m.csr_ptr[c]]]);
@@ -210,16 +212,14 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     L.remote_slots = nparts * L.max_export;
   }
 
-  // columns: CSR over copies in ascending s; local copies -> device rows,
-  // copies of other parts -> remote slots
-  L.cols = static_cast<int32_t>(L.gcol.size());
+  // ---- boundary columns: CSR over copies in ascending s (local copies ->
+  // device rows, other parts' copies -> remote slots) and their data
   L.col_ptr.assign(1, 0);
-  double msum = 0, n2 = 0, mn = 0;
-  for (const StreamChunk& ch : L.chunks) msum += ch.arows;
-  for (int32_t gc : L.gcol) {
-    for (int q = m.csr_ptr[gc]; q < m.csr_ptr[gc + 1]; ++q) {
-      const int ref = m.csr_copy[q];
-      if (part_of(s_of_ref[ref]) == part) {
+  for (int32_t q = 0; q < L.bcols; ++q) {
+    const int32_t gc = L.gcol[q];
+    for (int e = m.csr_ptr[gc]; e < m.csr_ptr[gc + 1]; ++e) {
+      const int ref = m.csr_copy[e];
+      if (dev_of_ref[ref] >= 0) {
         L.copies.push_back(dev_of_ref[ref]);
       } else {
         if (slot_of_ref[ref] < 0) throw std::logic_error("remote copy without an export slot");
@@ -231,26 +231,160 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     L.inv.push_back(m.inv_copy[gc]);
     L.lo.push_back(m.x_lo[gc]);
     L.hi.push_back(m.x_hi[gc]);
-    L.x0.push_back(m.x0[gc]);
-    L.owner.push_back(part_of(s_of_ref[m.csr_copy[m.csr_ptr[gc]]]) == part ? 1 : 0);
   }
-  for (StreamChunk& ch : L.chunks) {
-    ch.icopy0 = ch.icols ? L.col_ptr[ch.icol0] : 0;
-    ch.icopies = ch.icols ? L.col_ptr[ch.icol0 + ch.icols] - ch.icopy0 : 0;
-    if (ch.icopies > ch.rows) throw std::logic_error("interior copies exceed the chunk's rows");
+
+  // ---- chunk images
+  const int64_t* ro = L.raw_off;
+  for (int q = 0; q < nchunks; ++q) {
+    StreamChunk& ch = L.chunks[q];
+    const std::vector<int>& members = members_of[q];
+    // rows (thread r) and equality rows, with their operator sources
+    struct Src { int64_t at; int n; int base; };
+    std::vector<Src> prow, arow;
+    std::vector<int64_t> bsrc;
+    {
+      int base = 0;
+      for (int s : members) {
+        const int n = ns_of(s);
+        for (int i = 0; i < n; ++i) prow.push_back(Src{m.p_offsets[s] + static_cast<int64_t>(i) * n, n, base});
+        for (int r = 0; r < m.m_s[s]; ++r) {
+          arow.push_back(Src{m.a_offsets[s] + static_cast<int64_t>(r) * n, n, base});
+          bsrc.push_back(m.b_offsets[s] + r);
+        }
+        base += n;
+      }
+    }
+    // row metadata: interior column index or boundary import slot
+    std::vector<StreamRow> rmeta(ch.rows);
+    ch.bimp0 = static_cast<int32_t>(L.bimp.size());
+    for (int r = 0; r < ch.rows; ++r) {
+      const int32_t ref = L.ref_of_dev[ch.row0 + r];
+      const int32_t col = loc_of_col[m.l2g[ref]];
+      StreamRow rm{prow[r].n, prow[r].base, -1, -1};
+      if (col >= L.bcols) {
+        rm.xloc = col - ch.icol0;
+      } else {
+        for (int e = ch.bimp0; e < static_cast<int>(L.bimp.size()); ++e)
+          if (L.bimp[e] == col) rm.xin = e - ch.bimp0;
+        if (rm.xin < 0) {
+          rm.xin = static_cast<int32_t>(L.bimp.size()) - ch.bimp0;
+          L.bimp.push_back(col);
+        }
+      }
+      rmeta[r] = rm;
+    }
+    ch.nbimp = static_cast<int32_t>(L.bimp.size()) - ch.bimp0;
+    // interior columns: chunk-local CSR over their copies (ascending s)
+    std::vector<int32_t> cptr(1, 0), icopies;
+    std::vector<uint8_t> own;
+    for (int e = 0; e < ch.icols; ++e) {
+      const int32_t gc = L.gcol[ch.icol0 + e];
+      for (int k2 = m.csr_ptr[gc]; k2 < m.csr_ptr[gc + 1]; ++k2)
+        icopies.push_back(dev_of_ref[m.csr_copy[k2]] - ch.row0);
+      cptr.push_back(static_cast<int32_t>(icopies.size()));
+      own.push_back(L.owner[ch.icol0 + e]);
+    }
+    // the image
+    ch.image_off = static_cast<int64_t>(8 * L.blob.size());
+    ImageWriter w{L.blob, L.blob_src, L.blob.size()};
+    ChunkHead head{};
+    head.rows = ch.rows;
+    head.arows = ch.arows;
+    head.icols = ch.icols;
+    head.icopies = static_cast<int32_t>(icopies.size());
+    head.nbimp = ch.nbimp;
+    head.row0 = ch.row0;
+    head.icol0 = ch.icol0;
+    head.bimp0 = ch.bimp0;
+    const std::size_t head_at = L.blob.size();
+    for (std::size_t i = 0; i < sizeof(ChunkHead) / 8; ++i) w.put(0.0, -2);  // ChunkHead (filled below)
+    head.off[kImgRmeta] = w.here();
+    w.put_meta(rmeta);
+    head.off[kImgV] = w.here();
+    for (int r = 0; r < ch.rows; ++r) w.put_value(m.v, ro[kRawV], L.ref_of_dev[ch.row0 + r]);
+    w.align16();
+    // sliced ELL of P and A per warp of 32 rows
+    auto pack = [&](const std::vector<Src>& rows, const double* raw, int64_t sec, std::vector<int32_t>& slices) {
+      const std::size_t sec_start = L.blob.size();
+      for (int w0 = 0; w0 < static_cast<int>(rows.size()); w0 += 32) {
+        slices.push_back(static_cast<int32_t>(L.blob.size() - sec_start));
+        const int lanes = std::min(32, static_cast<int>(rows.size()) - w0);
+        int width = 0;
+        for (int l = 0; l < lanes; ++l) width = std::max(width, rows[w0 + l].n);
+        for (int j = 0; j < width; ++j)
+          for (int l = 0; l < 32; ++l) {
+            if (l < lanes && j < rows[w0 + l].n) w.put_value(raw, sec, rows[w0 + l].at + j);
+            else w.put(0.0, -1);
+          }
+      }
+    };
+    std::vector<int32_t> pslice, aslice;
+    // slice tables precede the sections they index: reserve, pack, then patch
+    const int pw = (ch.rows + 31) / 32, aw = (ch.arows + 31) / 32;
+    head.off[kImgPslice] = w.here();
+    const std::size_t ps_at = L.blob.size();
+    w.put_meta(std::vector<int32_t>(pw, 0));
+    head.off[kImgAslice] = w.here();
+    const std::size_t as_at = L.blob.size();
+    w.put_meta(std::vector<int32_t>(aw, 0));
+    head.off[kImgP] = w.here();
+    pack(prow, m.P, ro[kRawP], pslice);
+    head.off[kImgA] = w.here();
+    pack(arow, m.A, ro[kRawA], aslice);
+    if (!pslice.empty()) std::memcpy(&L.blob[ps_at], pslice.data(), pslice.size() * 4);
+    if (!aslice.empty()) std::memcpy(&L.blob[as_at], aslice.data(), aslice.size() * 4);
+    std::vector<StreamARow> ameta(ch.arows);
+    for (int a = 0; a < ch.arows; ++a) ameta[a] = StreamARow{arow[a].n, arow[a].base};
+    head.off[kImgAmeta] = w.here();
+    w.put_meta(ameta);
+    head.off[kImgAb] = w.here();
+    for (int a = 0; a < ch.arows; ++a) w.put_value(m.b, ro[kRawB], bsrc[a]);
+    w.align16();
+    const int sec_of[4] = {kRawC, kRawInv, kRawLo, kRawHi};
+    const double* raw_of[4] = {m.c, m.inv_copy, m.x_lo, m.x_hi};
+    for (int f = 0; f < 4; ++f) {
+      head.off[kImgCost + f] = w.here();
+      for (int e = 0; e < ch.icols; ++e) w.put_value(raw_of[f], ro[sec_of[f]], L.gcol[ch.icol0 + e]);
+      w.align16();
+    }
+    head.off[kImgOwner] = w.here();
+    w.put_meta(own);
+    head.off[kImgCptr] = w.here();
+    w.put_meta(cptr);
+    head.off[kImgCopies] = w.here();
+    w.put_meta(icopies);
+    ch.image_bytes = static_cast<int32_t>(w.here());
+    head.image_bytes = ch.image_bytes;
+    std::memcpy(&L.blob[head_at], &head, sizeof(ChunkHead));
+    StagePlan sp;
+    stage_plan(ch, sp);
+    const bool fits = sp.total <= static_cast<uint32_t>(L.stage_bytes) && ch.rows <= kStagedRows &&
+                      ch.arows <= kStagedRows;
+    (fits ? L.staged_ids : L.big_ids).push_back(q);
   }
-  for (int s : order) {
-    const double n = ns_of(s);
-    n2 += n * n;
-    mn += m.m_s[s] * n;
+  L.imp_ptr.assign(L.bcols + 1, 0);
+  for (int32_t c : L.bimp) ++L.imp_ptr[c + 1];
+  for (int32_t c = 0; c < L.bcols; ++c) L.imp_ptr[c + 1] += L.imp_ptr[c];
+  L.imp_slot.resize(L.bimp.size());
+  {
+    std::vector<int32_t> fill(L.imp_ptr.begin(), L.imp_ptr.end() - 1);
+    for (std::size_t e = 0; e < L.bimp.size(); ++e) L.imp_slot[fill[L.bimp[e]]++] = static_cast<int32_t>(e);
   }
-  // algorithmic bytes of this part (DESIGN.md section 4 restricted to it)
+
   if (nparts == 1) {  // signature for the re-upload fast path
     L.sig_z_offsets.assign(m.z_offsets, m.z_offsets + m.S + 1);
     L.sig_m_s.assign(m.m_s, m.m_s + m.S);
     L.sig_l2g.assign(m.l2g, m.l2g + m.N_z);
     L.sig_csr_ptr.assign(m.csr_ptr, m.csr_ptr + m.n + 1);
     L.sig_csr_copy.assign(m.csr_copy, m.csr_copy + m.N_z);
+  }
+  // algorithmic bytes of this part (DESIGN.md section 4 restricted to it)
+  double msum = 0, n2 = 0, mn = 0;
+  for (int s : order) {
+    const double n = ns_of(s);
+    n2 += n * n;
+    mn += m.m_s[s] * n;
+    msum += m.m_s[s];
   }
   L.bytes_per_iteration = 8.0 * (n2 + mn + msum) + 56.0 * L.rows + 48.0 * L.cols +
                           4.0 * (2.0 * L.rows + L.cols + 1) + 16.0 * static_cast<double>(order.size());

@@ -3,12 +3,20 @@
 // tiled 0.5M-bus feeder: ~10.7M local variables, ~1.5 GB of operators).
 //
 //  * Subsystems in the depth-first locality order (layout_builder.cpp) are
-//    cut into chunks of at most kStreamRows rows; one CTA processes one chunk
-//    per iteration (thread = row), so subsystem targets stay in shared memory.
-//  * P and A rows are sliced ELL per warp (entry j of lane l at
-//    slice + 32 j + l): every warp load is 256 contiguous bytes of HBM.
-//  * Columns keep the reference's CSR scatter (copies in ascending s) over
-//    device rows, so the global update sums in the reference order.
+//    cut into chunks of whole subsystems (thread = row inside a chunk).
+//  * Everything a chunk reads that does not change between iterations -- its
+//    P and A rows (sliced ELL per warp: entry j of lane l at slice + 32 j + l),
+//    v, b, row and equality-row metadata, and the data of its interior
+//    columns -- is packed into one contiguous, 16-byte aligned chunk IMAGE.
+//    The staged kernel moves a chunk with four bulk copies (image, z slice,
+//    lambda slice, imported boundary x): the bulk-copy engine's cost is per
+//    copy, not per byte.
+//  * Columns keep the reference's CSR scatter (copies in ascending s).
+//    Columns whose copies all sit in one chunk ("interior") are updated by
+//    that chunk's CTA from the z, lambda it loads anyway; only the boundary
+//    columns [0, bcols) -- copies in several chunks or on other ranks -- take
+//    the separate global-update kernel, which also writes each boundary x
+//    into the import slots of the chunks that read it.
 //  * Partitioned (multi-rank) layouts hold the rank's subsystems only; copies
 //    held by other ranks are read from a gathered "remote" array.
 #pragma once
@@ -17,16 +25,23 @@
 #include <vector>
 
 #include "../../../include/dopf_types.h"
+#include "layout.hpp"
 
 namespace dopf::cuda {
 
-constexpr int kStreamRows = 512;  // threads per CTA of the streaming kernels (>= widest subsystem)
+constexpr int kStreamRows = 512;   // rows of the widest chunk (direct-load kernel threads)
+// staged kernel: chunks of <= kStagedRows rows whose shared-memory stage
+// (image + z + lambda + imports) fits `stage_bytes`; `stages` stages per CTA
+constexpr int kStagedRows = 256;
+constexpr int kMaxStages = 8;
+constexpr int kDefaultStages = 2;
+constexpr int kDefaultStageBytes = 48 * 1024;
 
 struct StreamRow {
   int32_t n;      // n_s
   int32_t base;   // chunk-local row of (s, 0)
-  int32_t xcol;   // column index (into the rank's column arrays) of l2g(s, i)
-  int32_t pad;
+  int32_t xloc;   // interior column: index among the chunk's interior columns, else -1
+  int32_t xin;    // boundary column: slot in the chunk's import list, else -1
 };
 
 struct StreamARow {
@@ -37,44 +52,99 @@ struct StreamARow {
 struct StreamChunk {
   int32_t row0;   // first device row
   int32_t rows;
-  int32_t arow0;  // first equality row
-  int32_t arows;
-  int32_t icol0;  // first interior column (all copies in this chunk): updated by k_local
+  int32_t arows;  // equality rows
+  int32_t icol0;  // first interior column (all copies in this chunk)
   int32_t icols;
-  int32_t icopy0; // their copies: [icopy0, icopy0 + icopies) of `copies` (<= rows)
-  int32_t icopies;
-  int64_t p0, p1; // the chunk's P slab [p0, p1) and A slab [a0, a1) (doubles): bulk-prefetched to L2
-  int64_t a0, a1;
+  int32_t bimp0;  // boundary-column imports: ximp[bimp0, bimp0 + nbimp)
+  int32_t nbimp;
+  int32_t image_bytes;
+  int64_t image_off;  // byte offset of the chunk image in `blob`
 };
+static_assert(sizeof(StreamChunk) == 40, "StreamChunk layout");
+
+// byte offsets of the sections of a chunk image (relative to its start)
+enum ImageSection {
+  kImgRmeta, kImgV, kImgPslice, kImgAslice, kImgP, kImgA, kImgAmeta, kImgAb, kImgCost, kImgInv, kImgLo,
+  kImgHi, kImgOwner, kImgCptr, kImgCopies, kImgSections
+};
+struct ChunkHead {                 // the first 112 bytes of every chunk image
+  int32_t rows, arows, icols, icopies, nbimp;
+  int32_t row0, icol0, bimp0, image_bytes, pad[3];
+  uint32_t off[16];                // [kImgSections] byte offsets, 16-byte aligned
+};
+static_assert(sizeof(ChunkHead) == 112, "ChunkHead is 112 bytes");
+// pslice / aslice: int32 offsets (in doubles) of each warp's slice from the
+// start of the P / A section; cptr: int32 CSR offsets (icols + 1) into copies;
+// copies: int32 chunk-local rows; owner: uint8 per interior column.
+
+// Shared-memory stage of the staged kernel: the image, then the z and lambda
+// slices and the import slots, each copied with its source start rounded
+// down and end rounded up to 16 bytes (`shift` = first element's byte offset).
+struct StageSeg {
+  uint32_t dst, shift, bytes;
+};
+struct StagePlan {
+  StageSeg z, lam, ximp;
+  uint32_t total;
+};
+
+DOPF_HD inline StageSeg stage_seg(uint32_t& cursor, int64_t first, int64_t count, int es) {
+  StageSeg s{cursor, 0u, 0u};
+  if (count <= 0) return s;
+  const int64_t b0 = first * es, b1 = (first + count) * es;
+  const int64_t a0 = b0 & ~static_cast<int64_t>(15), a1 = (b1 + 15) & ~static_cast<int64_t>(15);
+  s.shift = static_cast<uint32_t>(b0 - a0);
+  s.bytes = static_cast<uint32_t>(a1 - a0);
+  cursor += s.bytes;
+  return s;
+}
+
+DOPF_HD inline void stage_plan(const StreamChunk& ch, StagePlan& sp) {
+  uint32_t cur = static_cast<uint32_t>(ch.image_bytes);
+  sp.z = stage_seg(cur, ch.row0, ch.rows, 8);
+  sp.lam = stage_seg(cur, ch.row0, ch.rows, 8);
+  sp.ximp = stage_seg(cur, ch.bimp0, ch.nbimp, 8);
+  sp.total = cur;
+}
 
 struct StreamLayout {
   int32_t S = 0, n = 0, N_z = 0;       // whole model
   int32_t rows = 0;                    // device rows (this rank)
   int32_t cols = 0;                    // columns this rank updates
-  int32_t bcols = 0;                   // boundary columns [0, bcols): copies in >1 chunk or remote
+  int32_t bcols = 0;                   // boundary columns [0, bcols)
+  int32_t stages = kDefaultStages, stage_bytes = kDefaultStageBytes;  // staged-kernel pipeline
   std::vector<StreamChunk> chunks;
-  std::vector<StreamRow> rmeta;        // per device row
-  std::vector<int64_t> pslice;         // per warp-slice of rows: offset into P
-  std::vector<int64_t> aslice;         // per warp-slice of equality rows: offset into A
-  std::vector<StreamARow> ameta;       // per equality row (chunk-major)
-  std::vector<double> P, A, ab, v, z0;
+  std::vector<int32_t> staged_ids;     // chunks whose stage fits stage_bytes (staged kernel)
+  std::vector<int32_t> big_ids;        // the rest (direct-load kernel, image read from HBM)
+  std::vector<double> blob;            // chunk images (8-byte units; metadata bit-packed)
+  std::vector<double> z0;              // per device row
   std::vector<int32_t> ref_of_dev;     // device row -> reference z index
-  // columns: CSR over copies; copy >= 0: device row, < 0: -(remote slot + 1)
-  std::vector<int32_t> col_ptr, copies, gcol;
-  std::vector<double> c, inv, lo, hi, x0;
-  std::vector<uint8_t> owner;          // 1: this rank writes x and adds c x to the objective
+  std::vector<int32_t> gcol;           // column -> global column
+  std::vector<uint8_t> owner;          // per column: this rank writes x and adds c x to the objective
+  // boundary columns: CSR over copies (copy >= 0: device row, < 0: -(remote slot + 1)) and data
+  std::vector<int32_t> col_ptr, copies;
+  std::vector<double> c, inv, lo, hi;
+  std::vector<int32_t> bimp;           // import slot -> boundary column (per chunk, first-use order)
+  std::vector<int32_t> imp_ptr, imp_slot;  // boundary column -> its import slots (CSR)
   int32_t remote_slots = 0;            // partitioned: size of the gathered remote u array
   double bytes_per_iteration = 0;      // algorithmic bytes of this rank's share
   // partitioned exchange: this rank's exported rows (u packed into slot
   // part * max_export + e of every rank's remote array, in this order)
   int32_t nparts = 1, part = 0, max_export = 0;
   std::vector<int32_t> export_rows;
-  // re-upload fast path: where every packed value comes from in the model
-  // view (P / A / b indices, -1 = zero padding) and the structure signature
-  std::vector<int64_t> p_src, a_src, ab_src;
+  // re-upload fast path: every model value the layout holds, as an index
+  // into the concatenation raw = [P | A | b | v | z0 | c | inv_copy | x_lo | x_hi]
+  // of the model view (blob_src: -1 zero padding, -2 metadata to keep)
+  std::vector<int32_t> blob_src;
+  int64_t raw_off[10] = {};            // section starts of raw (last = total)
   std::vector<int32_t> sig_z_offsets, sig_m_s, sig_l2g, sig_csr_ptr, sig_csr_copy;
   bool same_structure(const dopf_model_view& m) const;
 };
+
+enum RawSection { kRawP, kRawA, kRawB, kRawV, kRawZ0, kRawC, kRawInv, kRawLo, kRawHi, kRawEnd };
+
+/// Section starts of the raw value concatenation of a model view.
+void raw_offsets(const dopf_model_view& m, int64_t (&off)[10]);
 
 /// Whole-model streaming layout (one rank).
 StreamLayout build_stream_layout(const dopf_model_view& m);
