@@ -58,6 +58,8 @@
 // different (tree) order; they feed the stop test and the trace only.
 #include "admm_kernels.cuh"
 
+#include "div_rho.cuh"
+
 namespace dopf::cuda {
 
 namespace {
@@ -598,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
           v8[2] = v8[2] + bx * bx;
           v8[3] = v8[3] + z * z;
           v8[4] = v8[4] + ln * ln;
-          lr[k] = ln / rho;  // reused as lambda/rho by the next target (admm.cpp:136)
+          lr[k] = div_rho(ln, rho, p.rho_inv);  // = ln / rho; reused as lambda/rho by the next target (admm.cpp:136)
           const double u = z - lr[k];
           tu[r] = u;
           if (row_exported(rpk[k]))

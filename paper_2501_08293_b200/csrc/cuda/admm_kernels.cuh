@@ -53,6 +53,7 @@ struct KernelParams {
   double* maxinf;       // [instances]
   double* objective;    // [instances]
   double rho;
+  double rho_inv;  // RN(1 / rho) for div_rho (div_rho.cuh)
   double eps_rel;
   int64_t rows_total;
   int64_t trace_stride; // rows per instance in `trace`

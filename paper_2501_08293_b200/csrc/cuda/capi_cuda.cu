@@ -18,6 +18,7 @@
 #include "layout_gather.cuh"
 #include "precompute_kernels.cuh"
 #include "stream_kernels.cuh"
+#include "div_rho.cuh"
 
 using namespace dopf::cuda;
 
@@ -116,6 +117,7 @@ struct dopf_cuda_ctx {
   // re-upload fast path: the plan whose index maps / structure sit on the device
   const InstancePlan* dev_plan = nullptr;
   int staged_grid = 1;       // persistent CTAs of the staged streaming kernel
+  int staged_ctas = 2;       // of them per SM
   bool stream_maps = false;  // the streaming layout's maps are on the device
   int64_t* d_psrc = nullptr;
   int64_t* d_asrc = nullptr;
@@ -382,6 +384,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.maxinf = c->d_maxinf;
   p.objective = c->d_obj;
   p.rho = s->rho;
+  p.rho_inv = rho_reciprocal(s->rho);
   p.eps_rel = s->eps_rel;
   p.rows_total = L.rows_total;
   p.trace_stride = s->max_iter;
@@ -547,8 +550,12 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.lam = c->scratch<double>(k++, L.rows);
   d.u = c->scratch<double>(k++, L.rows);
   d.u_remote = c->scratch<double>(k++, std::max(1, L.remote_slots));
-  // persistent staged CTAs: two per SM, one SM left to the direct-load chunks if any
-  c->staged_grid = std::max(1, std::min<int>(kStagedCtasPerSm * (c->sm_count - (L.big_ids.empty() ? 0 : 1)),
+  // persistent staged CTAs per SM; the direct-load chunks get SMs of their own
+  // (kBigCtasPerSm each) so they run beside the staged kernel
+  c->staged_ctas = kDefaultStagedCtasPerSm;
+  if (const char* e = std::getenv("DOPF_STAGED_CTAS")) c->staged_ctas = std::atoi(e) >= 3 ? 3 : 2;
+  const int big_sms = static_cast<int>((L.big_ids.size() + kBigCtasPerSm - 1) / kBigCtasPerSm);
+  c->staged_grid = std::max(1, std::min<int>(c->staged_ctas * std::max(1, c->sm_count - big_sms),
                                              static_cast<int>(L.staged_ids.size())));
   d.part = c->scratch<double>(k++, static_cast<std::size_t>(c->staged_grid + L.big_ids.size()) * 8);
   d.objp = c->scratch<double>(k++, std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows));
@@ -592,6 +599,14 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   p.npart = c->staged_grid + p.n_big;
   p.stages = L.stages;
   p.stage_bytes = L.stage_bytes;
+  p.staged_ctas = c->staged_ctas;
+  p.prof = nullptr;
+
+  if (const char* e = std::getenv("DOPF_STREAM_PROF"); e && e[0] == '1') {
+    p.prof = c->scratch<long long>(126, static_cast<std::size_t>(c->staged_grid) * 8);
+    ck(cudaMemsetAsync(p.prof, 0, static_cast<std::size_t>(c->staged_grid) * 8 * sizeof(long long), c->stream),
+       "prof");
+  }
   p.col_ptr = d.col_ptr;
   p.copies = d.copies;
   p.cost = d.cost;
@@ -616,6 +631,7 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   p.n_export = static_cast<int32_t>(L.export_rows.size());
   p.max_export = L.max_export;
   p.rho = s->rho;
+  p.rho_inv = rho_reciprocal(s->rho);
   p.eps = s->eps_rel;
   p.max_iter = s->max_iter;
   p.nchunks = static_cast<int32_t>(L.chunks.size());
@@ -687,6 +703,16 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   StreamCtl ctl{};
   ck(cudaMemcpy(&ctl, d.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost), "d2h");
   c->kernels += 3ll * ctl.t;
+  if (const char* e = std::getenv("DOPF_STREAM_PROF"); e && e[0] == '1' && ctl.t > 0) {
+    std::vector<long long> h(static_cast<std::size_t>(c->staged_grid) * 8);
+    ck(cudaMemcpy(h.data(), c->bufs.at(126).p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "prof");
+    double sum[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < c->staged_grid; ++b)
+      for (int q = 0; q < 6; ++q) sum[q] += static_cast<double>(h[b * 8 + q]);
+    const double per = static_cast<double>(c->SL.staged_ids.size());  // the last iteration's chunks
+    std::fprintf(stderr, "staged phases (cycles per chunk): wait %.0f rows %.0f icol %.0f tgt %.0f gemv %.0f A %.0f\n",
+                 sum[0] / per, sum[1] / per, sum[2] / per, sum[3] / per, sum[4] / per, sum[5] / per);
+  }
   r->status = ctl.status;
   r->iterations = ctl.t;
   r->objective = ctl.objective;

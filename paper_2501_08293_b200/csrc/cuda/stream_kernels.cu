@@ -1,26 +1,33 @@
 // HBM-streaming fp64 ADMM iteration for instances whose operators do not fit
-// shared memory (the tiled 0.5M-bus feeder). Three kernels per iteration,
-// replayed by ONE CUDA-graph launch with a conditional while-node whose
-// condition the finalize kernel clears at the stop test -- no host round trip
-// per iteration:
+// shared memory (the tiled 0.5M-bus feeder). Per iteration, replayed by ONE
+// CUDA-graph launch with a conditional while-node whose condition the final
+// kernel clears at the stop test (no host round trip per iteration):
 //
 //  k_global   (thread per boundary column)  admm.cpp:118-129: acc = sum over
 //             the column's copies (CSR, ascending s) of u = z - lambda/rho;
-//             x = clamp((acc - c/rho) * inv_count, lo, hi); c'x partials.
-//  k_local    (CTA per chunk of whole subsystems, thread per row)
-//             the same global update for the chunk's interior columns (all
-//             copies in the chunk) from the z, lambda it loads anyway, then
-//             admm.cpp:131-143, 203-205, 150-163: target in shared memory,
-//             z = P target + v with P streamed from HBM (sliced ELL: 256
-//             contiguous bytes per warp load), dual update, u, ||A z - b||_inf,
-//             residual partials.
-//  k_final    (one CTA) admm.cpp:164-169, 223-234: fixed-order combine of the
-//             partials, trace row, running max, stop test.
+//             x = clamp((acc - c/rho) * inv_count, lo, hi); c'x partials; x is
+//             also written to the import slots of the chunks that read it.
+//  k_staged   (persistent, 2 CTAs/SM: 8 compute warps + 1 producer warp)
+//             the producer moves each chunk (image, z, lambda, imports) into
+//             a shared-memory stage with four bulk copies (TMA engine,
+//             mbarrier completion, two stages in flight); the compute warps
+//             run the chunk's iteration out of shared memory: interior
+//             columns' global update (all copies in the chunk), target, GEMV
+//             z = P target + v (admm.cpp:131-138), dual update (:140-143),
+//             ||A z - b||_inf (:203-205), residual partials (:150-163).
+//  k_local    the same chunk iteration for the few chunks whose stage would
+//             not fit shared memory (image read straight from HBM), on SMs
+//             the staged kernel leaves free (parallel graph branch).
+//  k_final    admm.cpp:164-169, 223-234: fixed-order combine of the partials,
+//             trace row, running max, stop test.
 //
-// Bitwise parity with the oracle: --fmad=false and the reference's operation
-// forms and summation orders for every iterate; only the residual/objective
+// Bitwise parity with the oracle: --fmad=false, the reference's operation
+// forms and summation orders for every iterate, and divisions by rho that are
+// exactly the IEEE quotient (div_rho.cuh); only the residual/objective
 // reductions are trees (stop test and trace only).
 #include "stream_kernels.cuh"
+
+#include "div_rho.cuh"
 
 #include <cstdlib>
 
@@ -30,13 +37,7 @@ namespace {
 
 __device__ __forceinline__ double sel_max(double a, double b) { return (a < b) ? b : a; }
 
-// one bulk (TMA-engine) prefetch of [ptr, ptr + bytes) into L2; bytes % 16 == 0
-__device__ __forceinline__ void bulk_prefetch_l2(const void* ptr, uint32_t bytes) {
-  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void prefetch_l1(const void* ptr) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
-}
+
 __device__ __forceinline__ double sel_min(double a, double b) { return (b < a) ? b : a; }
 
 // fixed-shape block reduction of `V` values (sum; index `imax` uses max)
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p)
       const int32_t rq = p.copies[q];
       acc = acc + (rq >= 0 ? p.u[rq] : p.u_remote[-rq - 1]);
     }
-    const double unclamped = (acc - p.cost[c] / p.rho) * p.inv[c];
+    const double unclamped = (acc - div_rho(p.cost[c], p.rho, p.rho_inv)) * p.inv[c];
     const double xv = sel_min(sel_max(unclamped, p.lo[c]), p.hi[c]);
     p.x[c] = xv;
     for (int e = p.imp_ptr[c]; e < p.imp_ptr[c + 1]; ++e) p.ximp[p.imp_slot[e]] = xv;  // chunk imports
@@ -135,6 +136,22 @@ __device__ __forceinline__ const T* sec(const unsigned char* img, const ChunkHea
   return reinterpret_cast<const T*>(img + h.off[id]);
 }
 
+// Sliced-ELL row dot product in the reference's sequential-j order
+// (admm.cpp:137): batches of 8 operator loads in flight, then the sum.
+template <typename Ld>
+__device__ __forceinline__ double row_dot(const double* pr, const double* tb, int n, Ld ld) {
+  double acc = 0.0;
+  for (int j0 = 0; j0 < n; j0 += 8) {
+    double pv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) pv[e] = j0 + e < n ? ld(pr + 32 * (j0 + e)) : 0.0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (j0 + e < n) acc = acc + pv[e] * tb[j0 + e];
+  }
+  return acc;
+}
+
 // One chunk's iteration, shared by the direct-load kernel (image in HBM) and
 // the staged kernel (image in shared memory): thread r = row r, interior
 // column r, equality row r. `img` is the chunk image, zin / lin / xin the
@@ -142,37 +159,52 @@ __device__ __forceinline__ const T* sec(const unsigned char* img, const ChunkHea
 // (`sync`) separate: u -> interior x -> target -> GEMV/dual -> A z - b.
 // Accumulates the residual partials into v (gap, step, bx2, z2, lam2, maxinf, c'x).
 template <int kRows, typename Sync, typename Ld>
-__device__ __forceinline__ void chunk_iteration(const StreamParams& p, const StreamChunk& ch,
-                                                const unsigned char* img, const ChunkHead& h,
-                                                const double* zin, const double* lin, const double* xin,
-                                                double* tgt, double* ush, double* xsh, double* zsh,
-                                                double (&v)[7], Sync sync, Ld ld) {
+__device__ __forceinline__ void chunk_iteration(const StreamParams& p, const unsigned char* img,
+                                                const ChunkHead& h, const double* zin, const double* lin,
+                                                const double* xin, double* tgt, double* ush, double* xsh,
+                                                double* zsh, double (&v)[7], Sync sync, Ld ld) {
   const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
   const double rho = p.rho;
-  const bool on = r < h.rows;
+  // the chunk's sections, read once (later smem stores could alias them for the compiler)
+  const int rows = h.rows, arows = h.arows, icols = h.icols, row0 = h.row0, icol0 = h.icol0;
+  const StreamRow* s_rm = reinterpret_cast<const StreamRow*>(img + h.off[kImgRmeta]);
+  const double* s_v = reinterpret_cast<const double*>(img + h.off[kImgV]);
+  const int2* s_ps = reinterpret_cast<const int2*>(img + h.off[kImgPslice]);
+  const int2* s_as = reinterpret_cast<const int2*>(img + h.off[kImgAslice]);
+  const double* s_P = reinterpret_cast<const double*>(img + h.off[kImgP]);
+  const double* s_A = reinterpret_cast<const double*>(img + h.off[kImgA]);
+  const StreamARow* s_am = reinterpret_cast<const StreamARow*>(img + h.off[kImgAmeta]);
+  const double* s_ab = reinterpret_cast<const double*>(img + h.off[kImgAb]);
+  const double* s_cost = reinterpret_cast<const double*>(img + h.off[kImgCost]);
+  const double* s_inv = reinterpret_cast<const double*>(img + h.off[kImgInv]);
+  const double* s_lo = reinterpret_cast<const double*>(img + h.off[kImgLo]);
+  const double* s_hi = reinterpret_cast<const double*>(img + h.off[kImgHi]);
+  const uint8_t* s_own = img + h.off[kImgOwner];
+  const int32_t* s_cp = reinterpret_cast<const int32_t*>(img + h.off[kImgCptr]);
+  const int32_t* s_cc = reinterpret_cast<const int32_t*>(img + h.off[kImgCopies]);
+  const bool on = r < rows;
   StreamRow rm{0, 0, -1, -1};
   double lamv = 0.0, q = 0.0;
   if (on) {
-    rm = sec<StreamRow>(img, h, kImgRmeta)[r];
+    rm = s_rm[r];
     lamv = lin[r];
     const double zprev = zin[r];
-    q = lamv / rho;
+    q = div_rho(lamv, rho, p.rho_inv);
     ush[r] = zprev - q;  // the u = z - lambda/rho the previous iteration produced
     zsh[r] = zprev;
   }
   sync();
-  if (r < h.icols) {  // interior column: admm.cpp:118-129 over the chunk's own copies
-    const int32_t* cp = sec<int32_t>(img, h, kImgCptr);
-    const int32_t* cc = sec<int32_t>(img, h, kImgCopies);
-    const int q1 = cp[r + 1];
+  if (r < icols) {  // interior column: admm.cpp:118-129 over the chunk's own copies
+    const int q1 = s_cp[r + 1];
     double acc = 0.0;
-    for (int e = cp[r]; e < q1; ++e) acc = acc + ush[cc[e]];  // ascending s
-    const double cost = sec<double>(img, h, kImgCost)[r];
-    const double unclamped = (acc - cost / rho) * sec<double>(img, h, kImgInv)[r];
-    const double xv = sel_min(sel_max(unclamped, sec<double>(img, h, kImgLo)[r]), sec<double>(img, h, kImgHi)[r]);
+#pragma unroll 1
+    for (int e = s_cp[r]; e < q1; ++e) acc = acc + ush[s_cc[e]];  // ascending s
+    const double cost = s_cost[r];
+    const double unclamped = (acc - div_rho(cost, rho, p.rho_inv)) * s_inv[r];
+    const double xv = sel_min(sel_max(unclamped, s_lo[r]), s_hi[r]);
     xsh[r] = xv;
-    p.x[ch.icol0 + r] = xv;
-    if (sec<uint8_t>(img, h, kImgOwner)[r]) v[6] = v[6] + cost * xv;
+    p.x[icol0 + r] = xv;
+    if (s_own[r]) v[6] = v[6] + cost * xv;
   }
   sync();
   double bx = 0.0;
@@ -182,24 +214,14 @@ __device__ __forceinline__ void chunk_iteration(const StreamParams& p, const Str
   }
   sync();
   if (on) {
-    const double* pr = sec<double>(img, h, kImgP) + sec<int32_t>(img, h, kImgPslice)[warp] + lane;
-    const double* tb = tgt + rm.base;
-    double acc = 0.0;
-    for (int j0 = 0; j0 < rm.n; j0 += 8) {  // 8 operator loads in flight, then the sequential-j sum
-      double pv[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) pv[e] = j0 + e < rm.n ? ld(pr + 32 * (j0 + e)) : 0.0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (j0 + e < rm.n) acc = acc + pv[e] * tb[j0 + e];  // admm.cpp:137
-    }
-    const double z = acc + sec<double>(img, h, kImgV)[r];
+    const double acc = row_dot(s_P + s_ps[warp].x + lane, tgt + rm.base, rm.n, ld);
+    const double z = acc + s_v[r];
     const double dd = bx - z;
     const double ln = lamv + rho * dd;  // admm.cpp:142
-    const int d = ch.row0 + r;
+    const int d = row0 + r;
     p.z[d] = z;
     p.lam[d] = ln;
-    if (rm.xin >= 0) p.u[d] = z - ln / rho;  // read by the next boundary update / exports
+    if (rm.xin >= 0) p.u[d] = z - div_rho(ln, rho, p.rho_inv);  // read by the next boundary update / exports
     v[0] = v[0] + dd * dd;
     const double dz = z - zsh[r];
     v[1] = v[1] + dz * dz;
@@ -209,20 +231,10 @@ __device__ __forceinline__ void chunk_iteration(const StreamParams& p, const Str
     ush[r] = z;  // every read of u happened before the previous barrier
   }
   sync();
-  if (r < h.arows) {  // ||A_s z_s - b_s||_inf (admm.cpp:203-205)
-    const StreamARow am = sec<StreamARow>(img, h, kImgAmeta)[r];
-    const double* ar = sec<double>(img, h, kImgA) + sec<int32_t>(img, h, kImgAslice)[warp] + lane;
-    const double* zb = ush + am.base;
-    double acc = 0.0;
-    for (int j0 = 0; j0 < am.n; j0 += 8) {
-      double av[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) av[e] = j0 + e < am.n ? ld(ar + 32 * (j0 + e)) : 0.0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (j0 + e < am.n) acc = acc + av[e] * zb[j0 + e];
-    }
-    v[5] = sel_max(v[5], fabs(acc - sec<double>(img, h, kImgAb)[r]));
+  if (r < arows) {  // ||A_s z_s - b_s||_inf (admm.cpp:203-205)
+    const StreamARow am = s_am[r];
+    const double acc = row_dot(s_A + s_as[warp].x + lane, ush + am.base, am.n, ld);
+    v[5] = sel_max(v[5], fabs(acc - s_ab[r]));
   }
 }
 
@@ -259,7 +271,7 @@ __device__ __forceinline__ void write_partials(const StreamParams& p, double (&v
 
 // Direct-load kernel for chunks whose stage would not fit shared memory:
 // one CTA per chunk, image read straight from HBM.
-__global__ void __launch_bounds__(kStreamRows, 1) k_local(const StreamParams p) {
+__global__ void __launch_bounds__(kStreamRows, 2) k_local(const StreamParams p) {
   __shared__ double tgt[kStreamRows], ush[kStreamRows], xsh[kStreamRows], zsh[kStreamRows];
   __shared__ double red[7 * (kStreamRows / 32)];
   __shared__ ChunkHead hsh;
@@ -272,8 +284,8 @@ __global__ void __launch_bounds__(kStreamRows, 1) k_local(const StreamParams p) 
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   auto sync = [] { __syncthreads(); };
   auto ld = [](const double* a) { return __ldcs(a); };
-  chunk_iteration<kStreamRows>(p, ch, img, hsh, p.z + ch.row0, p.lam + ch.row0, p.ximp + ch.bimp0, tgt, ush,
-                               xsh, zsh, v, sync, ld);
+  chunk_iteration<kStreamRows>(p, img, hsh, p.z + ch.row0, p.lam + ch.row0, p.ximp + ch.bimp0, tgt, ush, xsh,
+                               zsh, v, sync, ld);
   __syncthreads();
   write_partials<kStreamRows>(p, v, red, p.staged_grid + blockIdx.x, sync);
 }
@@ -322,12 +334,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// barrier of the 16 compute warps only (the producer warp never joins)
+// clock read ordered after the preceding barrier (a dependent shared load)
+__device__ __forceinline__ long long clock_after(const void* smem_word) {
+  long long c;
+  asm volatile("{ .reg .u32 t; ld.volatile.shared.u32 t, [%1]; mov.u64 %0, %%clock64; }"
+               : "=l"(c)
+               : "r"(smem_u32(smem_word))
+               : "memory");
+  return c;
+}
+
+// barrier of the compute warps only (the producer warp never joins)
 __device__ __forceinline__ void compute_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kStagedRows) : "memory");
 }
 
-__global__ void __launch_bounds__(kStagedThreads, kStagedCtasPerSm) k_staged(const StreamParams p) {
+template <int kCtasPerSm>
+__global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const StreamParams p) {
   extern __shared__ __align__(128) unsigned char stages[];  // [p.stages][p.stage_bytes]
   __shared__ double tgt[kStagedRows], ush[kStagedRows], xsh[kStagedRows], zsh[kStagedRows];
   __shared__ double red[7 * (kStagedRows / 32)];
@@ -377,12 +400,32 @@ __global__ void __launch_bounds__(kStagedThreads, kStagedCtasPerSm) k_staged(con
 
   // ---------------- compute warps
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  auto sync = [] { compute_sync(); };
+  // optional phase clock (thread 0): [0] data wait, [1] rows/u, [2] interior x,
+  // [3] target, [4] GEMV/dual, [5] A z - b + release
+  const bool prof = p.prof != nullptr && tid == 0;
+  long long ph[6] = {0, 0, 0, 0, 0, 0}, last = 0;
+  int phase = 0;
+  auto sync = [&] {
+    compute_sync();
+    if (prof) {
+      const long long c = clock_after(ush);
+      ph[phase < 5 ? phase : 5] += c - last;
+      last = c;
+      ++phase;
+    }
+  };
   auto ld = [](const double* a) { return *a; };
   int i = 0;
   for (int k = blockIdx.x; k < p.n_staged; k += G, ++i) {
     const int s = i % p.stages;
-    mbar_wait(&full[s], static_cast<unsigned>(i / p.stages) & 1u);
+    if (prof) last = clock64();
+    mbar_wait(&full[s], static_cast<unsigned>(i / p.stages) & 1u);  // every compute thread acquires the stage
+    if (prof) {
+      const long long c = clock64();
+      ph[0] += c - last;
+      last = c;
+      phase = 1;
+    }
     const unsigned char* st = stages + s * p.stage_bytes;
     const ChunkHead& h = *reinterpret_cast<const ChunkHead*>(st);
     StreamChunk ch{};  // the fields the stage plan and the iteration use, from the image head
@@ -394,13 +437,15 @@ __global__ void __launch_bounds__(kStagedThreads, kStagedCtasPerSm) k_staged(con
     ch.image_bytes = h.image_bytes;
     StagePlan sp;
     stage_plan(ch, sp);
-    chunk_iteration<kStagedRows>(p, ch, st, h, reinterpret_cast<const double*>(st + sp.z.dst + sp.z.shift),
+    chunk_iteration<kStagedRows>(p, st, h, reinterpret_cast<const double*>(st + sp.z.dst + sp.z.shift),
                                  reinterpret_cast<const double*>(st + sp.lam.dst + sp.lam.shift),
                                  reinterpret_cast<const double*>(st + sp.ximp.dst + sp.ximp.shift), tgt, ush,
                                  xsh, zsh, v, sync, ld);
-    compute_sync();  // the stage and the scratch arrays are free again
+    sync();  // the stage and the scratch arrays are free again
     if (tid == 0) mbar_arrive(&empty[s]);
   }
+  if (prof)
+    for (int q = 0; q < 6; ++q) p.prof[static_cast<int64_t>(blockIdx.x) * 8 + q] = ph[q];
   write_partials<kStagedRows>(p, v, red, blockIdx.x, sync);
 }
 
@@ -507,14 +552,22 @@ using LocalKernel = void (*)(const StreamParams);
 LocalKernel local_kernel() { return &k_local; }
 
 cudaError_t stream_prepare() {
-  static cudaError_t e = cudaFuncSetAttribute(k_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              100 * 1024);
+  static cudaError_t e = [] {
+    cudaError_t e2 = cudaFuncSetAttribute(k_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    if (e2 == cudaSuccess)
+      e2 = cudaFuncSetAttribute(k_staged<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+    return e2;
+  }();
   return e;
 }
 
+using StagedKernel = void (*)(const StreamParams);
+StagedKernel staged_kernel(int ctas_per_sm) { return ctas_per_sm >= 3 ? &k_staged<3> : &k_staged<2>; }
+
 void launch_local_all(const StreamParams& p, cudaStream_t s) {
   if (p.n_big > 0) local_kernel()<<<p.n_big, kStreamRows, 0, s>>>(p);
-  if (p.n_staged > 0) k_staged<<<p.staged_grid, kStagedThreads, p.stages * p.stage_bytes, s>>>(p);
+  if (p.n_staged > 0)
+    staged_kernel(p.staged_ctas)<<<p.staged_grid, kStagedThreads, p.stages * p.stage_bytes, s>>>(p);
 }
 
 void stream_launch_iteration(const StreamParams& p, cudaStream_t s) {
@@ -567,7 +620,7 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   kb.func = reinterpret_cast<void*>(local_kernel());
   kb.gridDim = dim3(p.n_big);
   ks = kg;
-  ks.func = reinterpret_cast<void*>(k_staged);
+  ks.func = reinterpret_cast<void*>(staged_kernel(p.staged_ctas));
   ks.gridDim = dim3(p.staged_grid);
   ks.blockDim = dim3(kStagedThreads);
   ks.sharedMemBytes = p.stages * p.stage_bytes;

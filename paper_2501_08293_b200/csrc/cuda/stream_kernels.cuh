@@ -19,7 +19,8 @@ struct StreamCtl {      // device-side loop state
 };
 
 constexpr int kStagedThreads = kStagedRows + 32;  // compute warps + 1 producer warp
-constexpr int kStagedCtasPerSm = 2;
+constexpr int kDefaultStagedCtasPerSm = 2;  // 2 or 3 (DOPF_STAGED_CTAS)
+constexpr int kBigCtasPerSm = 2;            // direct-load kernel residency
 
 struct StreamParams {
   const StreamChunk* chunks;
@@ -53,12 +54,16 @@ struct StreamParams {
   double* send;          // [max_export] packed exports
   int32_t n_export, max_export;
   double rho, eps;
+  double rho_inv;        // RN(1 / rho) (div_rho)
   int32_t max_iter;
   int32_t nchunks;
   int32_t n_staged, n_big;
   int32_t staged_grid;   // persistent CTAs of the staged kernel (partials [0, staged_grid))
   int32_t npart;         // partial slots: staged_grid + n_big
   int32_t stages, stage_bytes;  // staged-kernel pipeline (dynamic smem = stages * stage_bytes)
+  int32_t staged_ctas;   // staged CTAs per SM (2 or 3)
+  long long* prof;
+       // optional [staged_grid][8] phase cycles of the staged kernel (thread 0)
   int32_t cols;
   int32_t bcols;         // boundary columns [0, bcols) (k_global); the rest are per-chunk interior
   int32_t col_blocks;    // k_global CTAs (>= 1)

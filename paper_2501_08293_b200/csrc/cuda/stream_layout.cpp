@@ -307,10 +307,11 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     auto pack = [&](const std::vector<Src>& rows, const double* raw, int64_t sec, std::vector<int32_t>& slices) {
       const std::size_t sec_start = L.blob.size();
       for (int w0 = 0; w0 < static_cast<int>(rows.size()); w0 += 32) {
-        slices.push_back(static_cast<int32_t>(L.blob.size() - sec_start));
         const int lanes = std::min(32, static_cast<int>(rows.size()) - w0);
         int width = 0;
         for (int l = 0; l < lanes; ++l) width = std::max(width, rows[w0 + l].n);
+        slices.push_back(static_cast<int32_t>(L.blob.size() - sec_start));  // {offset, width} per warp
+        slices.push_back(width);
         for (int j = 0; j < width; ++j)
           for (int l = 0; l < 32; ++l) {
             if (l < lanes && j < rows[w0 + l].n) w.put_value(raw, sec, rows[w0 + l].at + j);
@@ -323,10 +324,10 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     const int pw = (ch.rows + 31) / 32, aw = (ch.arows + 31) / 32;
     head.off[kImgPslice] = w.here();
     const std::size_t ps_at = L.blob.size();
-    w.put_meta(std::vector<int32_t>(pw, 0));
+    w.put_meta(std::vector<int32_t>(2 * pw, 0));
     head.off[kImgAslice] = w.here();
     const std::size_t as_at = L.blob.size();
-    w.put_meta(std::vector<int32_t>(aw, 0));
+    w.put_meta(std::vector<int32_t>(2 * aw, 0));
     head.off[kImgP] = w.here();
     pack(prow, m.P, ro[kRawP], pslice);
     head.off[kImgA] = w.here();

@@ -73,8 +73,8 @@ struct ChunkHead {                 // the first 112 bytes of every chunk image
   uint32_t off[16];                // [kImgSections] byte offsets, 16-byte aligned
 };
 static_assert(sizeof(ChunkHead) == 112, "ChunkHead is 112 bytes");
-// pslice / aslice: int32 offsets (in doubles) of each warp's slice from the
-// start of the P / A section; cptr: int32 CSR offsets (icols + 1) into copies;
+// pslice / aslice: per warp {int32 offset (in doubles) of its slice from the
+// start of the P / A section, int32 slice width}; cptr: int32 CSR offsets (icols + 1) into copies;
 // copies: int32 chunk-local rows; owner: uint8 per interior column.
 
 // Shared-memory stage of the staged kernel: the image, then the z and lambda
