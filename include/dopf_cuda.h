@@ -111,6 +111,10 @@ int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out, int32_t max_b
 /* With profiling on: %globaltimer stamps (ns) per CTA for 64 iterations from
  * t = 100 -- [CTA][iteration][u published, boundary update start, end]. */
 int dopf_cuda_timeline(const dopf_cuda_ctx* ctx, uint64_t* out, int64_t cap);
+/* Self-check of the kernels' division by rho (div_rho.cuh: reciprocal plus
+ * two exact-residual corrections): out[i] = a[i] / rho as the kernels
+ * compute it, for comparison with the IEEE quotient. Host arrays of n. */
+int dopf_cuda_div_rho_check(dopf_cuda_ctx* ctx, const double* a, int64_t n, double rho, double* out);
 
 /* ---- Partitioned solve over several ranks (one process per GPU) ----------
  * Subsystem s lives on rank part_of_s[s]. Each rank updates the columns its

@@ -1226,6 +1226,22 @@ int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask
   });
 }
 
+int dopf_cuda_div_rho_check(dopf_cuda_ctx* c, const double* a, int64_t n, double rho, double* out) {
+  if (!c || n < 0 || (n > 0 && (!a || !out))) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    double *da = nullptr, *dout = nullptr;
+    ck(cudaMalloc(&da, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
+    ck(cudaMalloc(&dout, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
+    ck(cudaMemcpy(da, a, n * sizeof(double), cudaMemcpyHostToDevice), "h2d");
+    ck(launch_div_rho_check(da, n, rho, rho_reciprocal(rho), dout, c->stream), "div_rho");
+    ck(cudaMemcpyAsync(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "div_rho");
+    cudaFree(da);
+    cudaFree(dout);
+  });
+}
+
 int dopf_cuda_timeline(const dopf_cuda_ctx* c, uint64_t* out, int64_t cap) {
   if (!c || !out || !c->d_timeline) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(const_cast<dopf_cuda_ctx*>(c), [&] {

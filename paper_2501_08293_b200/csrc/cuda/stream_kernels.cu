@@ -540,7 +540,18 @@ __global__ void k_regather(const StreamRegather g) {
   }
 }
 
+__global__ void k_div_rho_check(const double* a, int64_t n, double rho, double rinv, double* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = div_rho(a[i], rho, rinv);
+}
+
 }  // namespace
+
+cudaError_t launch_div_rho_check(const double* a, int64_t n, double rho, double rinv, double* out, cudaStream_t s) {
+  k_div_rho_check<<<1024, 256, 0, s>>>(a, n, rho, rinv, out);
+  return cudaGetLastError();
+}
 
 cudaError_t stream_launch_regather(const StreamRegather& g, int sm_count, cudaStream_t s) {
   k_regather<<<8 * sm_count, 256, 0, s>>>(g);

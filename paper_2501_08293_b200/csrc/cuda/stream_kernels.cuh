@@ -88,6 +88,9 @@ struct StreamRegather {
 };
 cudaError_t stream_launch_regather(const StreamRegather& g, int sm_count, cudaStream_t s);
 
+/// div_rho self-check (dopf_cuda_div_rho_check).
+cudaError_t launch_div_rho_check(const double* a, int64_t n, double rho, double rinv, double* out, cudaStream_t s);
+
 /// One-time kernel attributes (dynamic shared memory of the staged kernel).
 cudaError_t stream_prepare();
 /// The whole solve as one graph: a while-node over {k_global, k_big, k_staged, k_final}.
