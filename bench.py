@@ -519,13 +519,14 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_iteration": b_iter,
+                         "traffic_per": "launch" if info["sync"] != "stream-graph" else "iteration",
                          "note": "algorithmic bytes (DESIGN.md s4) x iterations / kernel time; " +
                                  ("operators are staged in shared memory once per launch, so "
                                   "DRAM traffic is far below the algorithmic bytes"
                                   if info["sync"] != "stream-graph" else
                                   "operators are streamed from HBM every iteration")},
             "kernel": {"name": "admm_persistent" if info["sync"] != "stream-graph"
-                       else "k_global+k_local+k_final (graph while-node)",
+                       else "k_global+k_staged(+k_local)+k_final (graph while-node)",
                        "ctas_per_instance": info["blocks"],
                        "instances": info["instances"], "threads": info["threads"],
                        "smem_bytes": info["smem_bytes"], "resident": info["resident"],

@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const Str
 }
 
 constexpr int kFinalThreads = 256;
-constexpr int kFinalBlocks = 128;
+constexpr int kFinalBlocks = 128;  // (a single CTA measured slower even for ~2k partials)
 
 // Two-level fixed-order reduction of the chunk partials and objective
 // partials: CTA g folds a contiguous range into level-2 slot g; the last CTA
@@ -461,8 +461,9 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
   if (p.ctl->done) return;
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gap, step, bx2, z2, lam2, maxinf, objective
   const int g = blockIdx.x;
-  const int c0 = static_cast<int>(static_cast<int64_t>(p.npart) * g / kFinalBlocks);
-  const int c1 = static_cast<int>(static_cast<int64_t>(p.npart) * (g + 1) / kFinalBlocks);
+  const int G = gridDim.x;
+  const int c0 = static_cast<int>(static_cast<int64_t>(p.npart) * g / G);
+  const int c1 = static_cast<int>(static_cast<int64_t>(p.npart) * (g + 1) / G);
   for (int k = c0 + threadIdx.x; k < c1; k += kFinalThreads) {
     const double* q = p.part + static_cast<int64_t>(k) * 8;
 #pragma unroll
@@ -470,8 +471,8 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
     v[5] = sel_max(v[5], __ldcg(q + 5));
     v[6] = v[6] + __ldcg(q + 6);  // interior columns' c'x
   }
-  const int o0 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * g / kFinalBlocks);
-  const int o1 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * (g + 1) / kFinalBlocks);
+  const int o0 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * g / G);
+  const int o1 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * (g + 1) / G);
   for (int k = o0 + threadIdx.x; k < o1; k += kFinalThreads) v[6] = v[6] + __ldcg(p.objp + k);
   block_reduce<7, kFinalThreads>(v, sh, 5);
   if (threadIdx.x == 0) {
@@ -480,13 +481,13 @@ __global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
     for (int q = 0; q < 7; ++q) slot[q] = v[q];
     __threadfence();
     const unsigned done_blocks = atomicAdd(p.final_count, 1u);
-    last = done_blocks == kFinalBlocks - 1;
+    last = done_blocks == static_cast<unsigned>(G - 1);
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   double w[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  if (threadIdx.x < kFinalBlocks) {
+  if (threadIdx.x < G) {
     const double* q = p.part2 + threadIdx.x * 8;
 #pragma unroll
     for (int i = 0; i < 7; ++i) w[i] = __ldcg(q + i);
