@@ -111,6 +111,10 @@ int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out, int32_t max_b
 /* With profiling on: %globaltimer stamps (ns) per CTA for 64 iterations from
  * t = 100 -- [CTA][iteration][u published, boundary update start, end]. */
 int dopf_cuda_timeline(const dopf_cuda_ctx* ctx, uint64_t* out, int64_t cap);
+/* Streaming layout of the uploaded model (zeros for the resident path):
+ * out[0] chunks, [1] staged-kernel chunks, [2] direct-load chunks,
+ * [3] boundary columns, [4] staged CTAs, [5] stage bytes, [6] stages. */
+int dopf_cuda_stream_info(const dopf_cuda_ctx* ctx, int64_t* out7);
 /* Self-check of the kernels' division by rho (div_rho.cuh: reciprocal plus
  * two exact-residual corrections): out[i] = a[i] / rho as the kernels
  * compute it, for comparison with the IEEE quotient. Host arrays of n. */

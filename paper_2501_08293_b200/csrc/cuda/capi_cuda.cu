@@ -1226,6 +1226,21 @@ int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask
   });
 }
 
+int dopf_cuda_stream_info(const dopf_cuda_ctx* c, int64_t* out) {
+  if (!c || !out) return DOPF_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < 7; ++i) out[i] = 0;
+  if (!c->streaming) return DOPF_OK;
+  const StreamLayout& L = c->SL;
+  out[0] = static_cast<int64_t>(L.chunks.size());
+  out[1] = static_cast<int64_t>(L.staged_ids.size());
+  out[2] = static_cast<int64_t>(L.big_ids.size());
+  out[3] = L.bcols;
+  out[4] = c->staged_grid;
+  out[5] = L.stage_bytes;
+  out[6] = L.stages;
+  return DOPF_OK;
+}
+
 int dopf_cuda_div_rho_check(dopf_cuda_ctx* c, const double* a, int64_t n, double rho, double* out) {
   if (!c || n < 0 || (n > 0 && (!a || !out))) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {

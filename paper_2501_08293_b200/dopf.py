@@ -551,6 +551,14 @@ class CudaSolver:
                 "smem_bytes": i.smem_bytes, "resident": bool(i.resident),
                 "sync": {0: "block", 1: "cluster", 2: "grid", 3: "stream-graph"}.get(i.sync_mode, "?")}
 
+    def stream_info(self) -> dict:
+        """Streaming layout of the uploaded model (zeros on the resident path)."""
+        out = np.zeros(7, dtype=np.int64)
+        self._err(self._lib.dopf_cuda_stream_info(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        keys = ("chunks", "staged_chunks", "direct_chunks", "boundary_columns", "staged_ctas", "stage_bytes",
+                "stages")
+        return {k: int(v) for k, v in zip(keys, out)}
+
     def set_path(self, path: str) -> None:
         """'auto' | 'resident' | 'stream' for the next upload."""
         self._err(self._lib.dopf_cuda_set_path(self._h, {"auto": 0, "resident": 1, "stream": 2}[path]))

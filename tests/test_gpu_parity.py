@@ -349,3 +349,26 @@ def test_div_rho_is_the_ieee_quotient(solver, rho):
         ref = a / rho
     same = (out.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(out) & np.isnan(ref))
     assert same.all(), (a[~same][:5], out[~same][:5], ref[~same][:5])
+
+
+@pytest.mark.parametrize("stage_kb,ctas,direct", [(8, "2", True), (16, "3", True), (32, "3", False)])
+def test_stream_direct_and_staged_chunk_mix_bitwise(monkeypatch, stage_kb, ctas, direct):
+    """Small pipeline stages push many chunks onto the direct-load kernel
+    (image read from HBM) beside the staged kernel; 3 staged CTAs per SM
+    exercises the other residency. Both chunk kernels share one iteration
+    routine and must stay bitwise equal to the oracle."""
+    monkeypatch.setenv("DOPF_STAGE_KB", str(stage_kb))
+    monkeypatch.setenv("DOPF_STAGED_CTAS", ctas)
+    f = dopf.synthetic_feeder("ieee8500", 8500)
+    _, _, model = dopf.load_model(f, workers=8)
+    model.precompute(8)
+    s = dopf.CudaSolver(0)
+    s.set_path("stream")
+    s.upload(model)
+    info = s.stream_info()
+    assert (info["direct_chunks"] > 0) == direct and info["staged_chunks"] > 0, info
+    assert info["stage_bytes"] == stage_kb * 1024
+    settings = dopf.Settings(max_iter=150)
+    gpu = s.solve(settings)
+    ref = O.solve(model, dopf.Settings(max_iter=150, workers=8))
+    assert_same(gpu, ref, bitwise=True)
