@@ -13,6 +13,8 @@ timeout 600 python bench.py --impl reference > gpurun_out/${TAG}_ref_ieee8500.lo
 tail -1 gpurun_out/${TAG}_ref_ieee8500.log | cut -c1-200
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python tools/ncu_target.py ieee8500 8500 3 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:admm -s 1 -c 1 -o gpurun_out/${TAG}_prof python tools/ncu_target.py ieee8500 8500 2 > gpurun_out/${TAG}_ncu.log 2>&1
-DOPF_STREAM_NOGRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(global|local|final)" -s 3 -c 3 -o gpurun_out/${TAG}_tiled_prof python tools/ncu_tiled.py 64 3 > gpurun_out/${TAG}_tiled_ncu.log 2>&1
+DOPF_STREAM_NOGRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_" --csv --log-file gpurun_out/${TAG}_tiled_launches.csv python tools/ncu_tiled.py 64 2 > /dev/null 2>&1
+DOPF_STREAM_NOGRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_staged" -s 1 -c 1 -o gpurun_out/${TAG}_tiled_prof python tools/ncu_tiled.py 64 3 > gpurun_out/${TAG}_tiled_ncu.log 2>&1
+DOPF_STREAM_PROF=1 timeout 600 python tools/ncu_tiled.py 64 200 > gpurun_out/${TAG}_tiled_phase.log 2>&1
 timeout 300 python tools/phase_clock.py > gpurun_out/${TAG}_phase.log 2>&1
 ls gpurun_out/ | grep ${TAG} | wc -l
