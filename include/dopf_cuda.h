@@ -111,6 +111,12 @@ int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out, int32_t max_b
 /* With profiling on: %globaltimer stamps (ns) per CTA for 64 iterations from
  * t = 100 -- [CTA][iteration][u published, boundary update start, end]. */
 int dopf_cuda_timeline(const dopf_cuda_ctx* ctx, uint64_t* out, int64_t cap);
+/* Page-lock the value arrays of a host model view (P, A, b, v, z0, c,
+ * inv_copy, x_lo, x_hi) with cudaHostRegister, so that later uploads of models
+ * living in the same memory copy at DMA speed. Ranges stay registered until
+ * dopf_cuda_unpin_model or dopf_cuda_destroy; pinning a range twice is a no-op. */
+int dopf_cuda_pin_model(dopf_cuda_ctx* ctx, const dopf_model_view* model);
+int dopf_cuda_unpin_model(dopf_cuda_ctx* ctx, const dopf_model_view* model);
 /* Streaming layout of the uploaded model (zeros for the resident path):
  * out[0] chunks, [1] staged-kernel chunks, [2] direct-load chunks,
  * [3] boundary columns, [4] staged CTAs, [5] stage bytes, [6] stages. */

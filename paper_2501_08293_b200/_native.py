@@ -147,6 +147,8 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_reconstruct", C.c_int, vp, P(ModelView_t), P(f64), P(f64), P(f64))
     _sig(lib, "dopf_cuda_timeline", C.c_int, vp, P(u64), i64)
     _sig(lib, "dopf_cuda_stream_info", C.c_int, vp, P(i64))
+    _sig(lib, "dopf_cuda_pin_model", C.c_int, vp, P(ModelView_t))
+    _sig(lib, "dopf_cuda_unpin_model", C.c_int, vp, P(ModelView_t))
     _sig(lib, "dopf_cuda_div_rho_check", C.c_int, vp, P(f64), i64, f64, P(f64))
     _sig(lib, "dopf_cuda_bytes_per_iteration", f64, vp)
     _sig(lib, "dopf_cuda_last_kernel_seconds", f64, vp)

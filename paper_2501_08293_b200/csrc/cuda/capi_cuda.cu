@@ -1,6 +1,7 @@
 // Drop-in C ABI (include/dopf_cuda.h) over the persistent ADMM kernel.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
@@ -128,6 +129,7 @@ struct dopf_cuda_ctx {
   double* d_raw = nullptr;       // streaming re-upload: raw value concatenation
   double *d_rawP = nullptr, *d_rawA = nullptr, *d_rawb = nullptr, *d_rawv = nullptr, *d_rawz0 = nullptr,
          *d_rawc = nullptr, *d_rawinv = nullptr, *d_rawlo = nullptr, *d_rawhi = nullptr;
+  std::vector<const void*> pinned;  // host ranges registered by dopf_cuda_pin_model
   // pinned staging for results copied back to the host
   void* h_stage = nullptr;
   std::size_t h_stage_cap = 0;
@@ -1106,11 +1108,20 @@ int dopf_cuda_upload_part(dopf_cuda_ctx* c, const dopf_model_view* m, int32_t np
     if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
     c->uploaded = false;
     c->dev_plan = nullptr;
-    c->stream_maps = false;
     c->L.reset();
+    const bool same = c->stream_maps && c->streaming && c->partitioned &&
+                      c->SL.same_structure(*m, nparts, part, part_of_s);
     c->streaming = true;
     c->partitioned = true;
+    if (same) {
+      upload_stream_values(c, *m);  // structure and partition unchanged: values only
+      c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
+      c->uploaded = true;
+      return;
+    }
+    c->stream_maps = false;
     upload_stream(c, *m, nparts, part, part_of_s);
+    upload_stream_maps(c, *m);
     c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
     c->inst_nz = {m->N_z};
     c->inst_n = {m->n};
@@ -1226,6 +1237,45 @@ int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask
   });
 }
 
+namespace {
+// the value arrays of a model view and their lengths (doubles)
+std::vector<std::pair<const double*, int64_t>> value_ranges(const dopf_model_view& m) {
+  return {{m.P, m.p_offsets[m.S]}, {m.A, m.a_offsets[m.S]}, {m.b, m.b_offsets[m.S]}, {m.v, m.N_z},
+          {m.z0, m.N_z}, {m.c, m.n}, {m.inv_copy, m.n}, {m.x_lo, m.n}, {m.x_hi, m.n}};
+}
+}  // namespace
+
+int dopf_cuda_pin_model(dopf_cuda_ctx* c, const dopf_model_view* m) {
+  if (!c || !m || !m->has_pre) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    for (auto [ptr, n] : value_ranges(*m)) {
+      if (!ptr || n <= 0 || std::find(c->pinned.begin(), c->pinned.end(), ptr) != c->pinned.end()) continue;
+      const cudaError_t e = cudaHostRegister(const_cast<double*>(ptr), static_cast<std::size_t>(n) * sizeof(double),
+                                             cudaHostRegisterDefault);
+      if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+        continue;
+      }
+      ck(e, "cudaHostRegister");
+      c->pinned.push_back(ptr);
+    }
+  });
+}
+
+int dopf_cuda_unpin_model(dopf_cuda_ctx* c, const dopf_model_view* m) {
+  if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    for (auto [ptr, n] : value_ranges(*m)) {
+      (void)n;
+      auto it = std::find(c->pinned.begin(), c->pinned.end(), ptr);
+      if (it == c->pinned.end()) continue;
+      ck(cudaHostUnregister(const_cast<double*>(ptr)), "cudaHostUnregister");
+      c->pinned.erase(it);
+    }
+  });
+}
+
 int dopf_cuda_stream_info(const dopf_cuda_ctx* c, int64_t* out) {
   if (!c || !out) return DOPF_ERR_INVALID_ARGUMENT;
   for (int i = 0; i < 7; ++i) out[i] = 0;
@@ -1285,6 +1335,7 @@ const char* dopf_cuda_last_error(const dopf_cuda_ctx* c) { return c ? c->err.c_s
 void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  for (const void* ptr : c->pinned) cudaHostUnregister(const_cast<void*>(ptr));
   c->free_model();
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->ev0) cudaEventDestroy(c->ev0);

@@ -11,11 +11,14 @@
 
 namespace dopf::cuda {
 
-bool StreamLayout::same_structure(const dopf_model_view& m) const {
+bool StreamLayout::same_structure(const dopf_model_view& m, int nparts_, int part_,
+                                  const int32_t* part_of_s) const {
   auto eq = [](const std::vector<int32_t>& v, const int32_t* p, std::size_t n) {
     return v.size() == n && (n == 0 || std::memcmp(v.data(), p, n * sizeof(int32_t)) == 0);
   };
-  return nparts == 1 && m.has_pre && S == m.S && n == m.n && N_z == m.N_z &&
+  if (nparts_ != nparts || part_ != part) return false;
+  if (nparts > 1 && (!part_of_s || !eq(sig_part_of_s, part_of_s, static_cast<std::size_t>(m.S)))) return false;
+  return m.has_pre && S == m.S && n == m.n && N_z == m.N_z &&
          eq(sig_z_offsets, m.z_offsets, m.S + 1) && eq(sig_m_s, m.m_s, m.S) &&
          eq(sig_l2g, m.l2g, m.N_z) && eq(sig_csr_ptr, m.csr_ptr, m.n + 1) &&
          eq(sig_csr_copy, m.csr_copy, m.N_z);
@@ -372,7 +375,8 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     for (std::size_t e = 0; e < L.bimp.size(); ++e) L.imp_slot[fill[L.bimp[e]]++] = static_cast<int32_t>(e);
   }
 
-  if (nparts == 1) {  // signature for the re-upload fast path
+  {  // signature for the re-upload fast path
+    if (nparts > 1) L.sig_part_of_s.assign(part_of_s, part_of_s + m.S);
     L.sig_z_offsets.assign(m.z_offsets, m.z_offsets + m.S + 1);
     L.sig_m_s.assign(m.m_s, m.m_s + m.S);
     L.sig_l2g.assign(m.l2g, m.l2g + m.N_z);

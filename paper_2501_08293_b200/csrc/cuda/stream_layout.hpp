@@ -137,8 +137,10 @@ struct StreamLayout {
   // of the model view (blob_src: -1 zero padding, -2 metadata to keep)
   std::vector<int32_t> blob_src;
   int64_t raw_off[10] = {};            // section starts of raw (last = total)
-  std::vector<int32_t> sig_z_offsets, sig_m_s, sig_l2g, sig_csr_ptr, sig_csr_copy;
-  bool same_structure(const dopf_model_view& m) const;
+  std::vector<int32_t> sig_z_offsets, sig_m_s, sig_l2g, sig_csr_ptr, sig_csr_copy, sig_part_of_s;
+  /// m has the structure (and, partitioned, the partition) this layout was built for
+  bool same_structure(const dopf_model_view& m, int nparts_ = 1, int part_ = 0,
+                      const int32_t* part_of_s = nullptr) const;
 };
 
 enum RawSection { kRawP, kRawA, kRawB, kRawV, kRawZ0, kRawC, kRawInv, kRawLo, kRawHi, kRawEnd };

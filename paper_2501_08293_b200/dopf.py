@@ -551,6 +551,16 @@ class CudaSolver:
                 "smem_bytes": i.smem_bytes, "resident": bool(i.resident),
                 "sync": {0: "block", 1: "cluster", 2: "grid", 3: "stream-graph"}.get(i.sync_mode, "?")}
 
+    def pin(self, model: "DecomposedModel") -> None:
+        """Page-lock the model's value arrays (cudaHostRegister): later uploads of
+        this model copy host -> device at DMA speed. Released on destroy."""
+        if not model.has_precompute:
+            model.precompute()
+        self._err(self._lib.dopf_cuda_pin_model(self._h, C.byref(model.view())))
+
+    def unpin(self, model: "DecomposedModel") -> None:
+        self._err(self._lib.dopf_cuda_unpin_model(self._h, C.byref(model.view())))
+
     def stream_info(self) -> dict:
         """Streaming layout of the uploaded model (zeros on the resident path)."""
         out = np.zeros(7, dtype=np.int64)

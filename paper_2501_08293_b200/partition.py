@@ -82,9 +82,14 @@ class PartitionedSolver:
                                                   self.part_of_s.ctypes.data_as(C.POINTER(N.i32))))
         info = N.PartInfo_t()
         self._err(self._lib.dopf_cuda_part_info(self._h, C.byref(info)))
-        self.info = info
         torch = self.torch
         dev = f"cuda:{self.device}"
+        key = (info.send, info.recv, info.partials, info.ranks, info.max_export)
+        if getattr(self, "_buf_key", None) == key:
+            self.info = info  # same-structure re-upload: buffers, stream and captured graph stay valid
+            return
+        self.info = info
+        self._buf_key = key
         mx = max(1, info.max_export)
         self.send = torch.as_tensor(_DevArray(info.send, mx), device=dev)[:info.max_export]
         self.recv = torch.as_tensor(_DevArray(info.recv, max(1, self.world * info.max_export)),
@@ -93,8 +98,9 @@ class PartitionedSolver:
         self.ranks = torch.as_tensor(_DevArray(info.ranks, 8 * self.world), device=dev)
         # one dedicated stream for the kernels AND the collectives (made current
         # around the loop), so they are ordered (a NULL handle would mean "own stream")
-        self.stream = torch.cuda.Stream(device=dev)
-        self._err(self._lib.dopf_cuda_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
+        if getattr(self, "stream", None) is None:
+            self.stream = torch.cuda.Stream(device=dev)
+            self._err(self._lib.dopf_cuda_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
         self._graph_key = None
         # eager collective: communicator set-up must not happen inside a graph capture
         with torch.cuda.stream(self.stream):
