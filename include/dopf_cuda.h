@@ -117,6 +117,10 @@ int dopf_cuda_timeline(const dopf_cuda_ctx* ctx, uint64_t* out, int64_t cap);
  * dopf_cuda_unpin_model or dopf_cuda_destroy; pinning a range twice is a no-op. */
 int dopf_cuda_pin_model(dopf_cuda_ctx* ctx, const dopf_model_view* model);
 int dopf_cuda_unpin_model(dopf_cuda_ctx* ctx, const dopf_model_view* model);
+/* The same for any caller buffer (e.g. the result arrays x, z, lambda, trace:
+ * results are copied straight into them). */
+int dopf_cuda_pin_host(dopf_cuda_ctx* ctx, const void* ptr, int64_t bytes);
+int dopf_cuda_unpin_host(dopf_cuda_ctx* ctx, const void* ptr);
 /* Streaming layout of the uploaded model (zeros for the resident path):
  * out[0] chunks, [1] staged-kernel chunks, [2] direct-load chunks,
  * [3] boundary columns, [4] staged CTAs, [5] stage bytes, [6] stages. */

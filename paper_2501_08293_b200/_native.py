@@ -149,6 +149,8 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_stream_info", C.c_int, vp, P(i64))
     _sig(lib, "dopf_cuda_pin_model", C.c_int, vp, P(ModelView_t))
     _sig(lib, "dopf_cuda_unpin_model", C.c_int, vp, P(ModelView_t))
+    _sig(lib, "dopf_cuda_pin_host", C.c_int, vp, vp, i64)
+    _sig(lib, "dopf_cuda_unpin_host", C.c_int, vp, vp)
     _sig(lib, "dopf_cuda_div_rho_check", C.c_int, vp, P(f64), i64, f64, P(f64))
     _sig(lib, "dopf_cuda_bytes_per_iteration", f64, vp)
     _sig(lib, "dopf_cuda_last_kernel_seconds", f64, vp)

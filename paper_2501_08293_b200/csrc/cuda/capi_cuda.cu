@@ -132,6 +132,7 @@ struct dopf_cuda_ctx {
   std::vector<const void*> pinned;  // host ranges registered by dopf_cuda_pin_model
   // pinned staging for results copied back to the host
   void* h_stage = nullptr;
+  void* h_small = nullptr;
   std::size_t h_stage_cap = 0;
 
   int64_t launches = 0;
@@ -181,6 +182,11 @@ struct dopf_cuda_ctx {
   template <typename T>
   T* scratch(int slot, std::size_t count) {
     return static_cast<T*>(ensure(slot, count * sizeof(T)));
+  }
+
+  void* small_stage() {  // 64 pinned bytes for packed scalar results
+    if (!h_small) ck(cudaMallocHost(&h_small, 64), "cudaMallocHost");
+    return h_small;
   }
 
   void* stage(std::size_t bytes) {
@@ -311,6 +317,49 @@ void finish_upload(dopf_cuda_ctx* c) {
 }
 
 // Runs the kernel; copies scalars (and optionally vectors/trace) back.
+// Results of a single-instance solve (the resident path's common case).
+void finish_single(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view& r, bool copy_vectors,
+                   std::chrono::steady_clock::time_point t_up0) {
+  const HostLayout& L = c->L;
+  const std::size_t R = static_cast<std::size_t>(L.rows_total);
+  double* d_res = c->scratch<double>(122, 2 * R + 8);
+  ck(launch_final_single(c->d_z, c->d_lam, L.rows_total, c->d_refdev, c->d_iters, kZRing, c->d_status,
+                         c->d_maxinf, c->d_obj, d_res, d_res + R, d_res + 2 * R, c->sm_count, c->stream),
+     "final iterate");
+  ++c->kernels;
+  double* scal = static_cast<double*>(c->small_stage());
+  ck(cudaMemcpyAsync(scal, d_res + 2 * R, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  if (copy_vectors) {
+    const InstDesc& id = L.inst[0];
+    if (r.x)
+      ck(cudaMemcpyAsync(r.x, c->d_x + id.x_off, sizeof(double) * id.n, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (r.z) ck(cudaMemcpyAsync(r.z, d_res, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (r.lambda)
+      ck(cudaMemcpyAsync(r.lambda, d_res + R, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  }
+  ck(cudaStreamSynchronize(c->stream), "solve");
+  ck(cudaGetLastError(), "kernel");
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "elapsed");
+  c->last_kernel_s = ms * 1e-3;
+  const auto t_dn0 = std::chrono::steady_clock::now();
+  r.iterations = static_cast<int32_t>(scal[0]);
+  r.status = static_cast<int32_t>(scal[1]);
+  r.max_local_infeasibility = scal[2];
+  r.objective = scal[3];
+  r.time_solve = c->last_kernel_s;
+  r.time_global = r.time_local = r.time_dual = 0.0;
+  if (r.trace && r.iterations > 0) {
+    ck(cudaMemcpyAsync(r.trace, c->d_trace, static_cast<std::size_t>(r.iterations) * 6 * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->stream),
+       "trace d2h");
+    ck(cudaStreamSynchronize(c->stream), "trace d2h");
+  }
+  r.time_download = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_dn0).count();
+  r.time_upload = std::chrono::duration<double>(t_dn0 - t_up0).count() - c->last_kernel_s;
+  (void)s;
+}
+
 void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, int count,
          bool copy_vectors) {
   check_settings(s);
@@ -400,6 +449,13 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   ck(cudaEventRecord(c->ev1, c->stream), "event");
   ++c->launches;
   ++c->kernels;
+  if (count == 1 && I == 1 && c->dev_plan) {
+    // one instance: everything comes back with the kernel still in the stream
+    // order -- device permutation to reference order, direct copies into the
+    // caller's arrays, one synchronisation (plus one for the trace)
+    finish_single(c, s, results[0], copy_vectors, t_up0);
+    return;
+  }
   ck(cudaEventSynchronize(c->ev1), "kernel");
   ck(cudaGetLastError(), "kernel");
   float ms = 0;
@@ -695,16 +751,33 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
     ck(cudaGraphLaunch(c->graph, c->stream), "graph launch");
   }
   ck(cudaEventRecord(c->ev1, c->stream), "event");
-  ck(cudaEventSynchronize(c->ev1), "graph");
+  ++c->launches;
+  // results follow in stream order: loop state, then (single rank, value maps
+  // on the device) z / lambda / x permuted to reference order on the device
+  // and copied straight into the caller's arrays
+  StreamCtl* ctl_h = static_cast<StreamCtl*>(c->small_stage());
+  ck(cudaMemcpyAsync(ctl_h, d.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  const bool vectors = copy_vectors && (r->x || r->z || r->lambda);
+  const bool direct = vectors && c->stream_maps && !c->partitioned && L.rows == L.N_z && L.cols == L.n;
+  if (direct) {
+    const std::size_t Nz = static_cast<std::size_t>(L.N_z), n = static_cast<std::size_t>(L.n);
+    double* out = c->scratch<double>(123, 2 * Nz + n);
+    ck(stream_launch_results(d.z, d.lam, d.x, c->d_refdev, c->d_gcol, L.rows, L.cols, out, out + Nz, out + 2 * Nz,
+                             c->sm_count, c->stream),
+       "results");
+    if (r->z) ck(cudaMemcpyAsync(r->z, out, Nz * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (r->lambda)
+      ck(cudaMemcpyAsync(r->lambda, out + Nz, Nz * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    if (r->x) ck(cudaMemcpyAsync(r->x, out + 2 * Nz, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  }
+  ck(cudaStreamSynchronize(c->stream), "graph");
   ck(cudaGetLastError(), "graph");
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "elapsed");
   c->last_kernel_s = ms * 1e-3;
-  ++c->launches;
   const auto t_dn0 = std::chrono::steady_clock::now();
-  StreamCtl ctl{};
-  ck(cudaMemcpy(&ctl, d.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost), "d2h");
-  c->kernels += 3ll * ctl.t;
+  const StreamCtl ctl = *ctl_h;
+  c->kernels += 3ll * ctl.t + (direct ? 1 : 0);
   if (const char* e = std::getenv("DOPF_STREAM_PROF"); e && e[0] == '1' && ctl.t > 0) {
     std::vector<long long> h(static_cast<std::size_t>(c->staged_grid) * 8);
     ck(cudaMemcpy(h.data(), c->bufs.at(126).p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "prof");
@@ -721,7 +794,7 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   r->max_local_infeasibility = ctl.maxinf;
   r->time_solve = c->last_kernel_s;
   r->time_global = r->time_local = r->time_dual = 0.0;
-  if (copy_vectors && (r->x || r->z || r->lambda)) {
+  if (vectors && !direct) {
     const std::size_t R = static_cast<std::size_t>(L.rows);
     double* st = static_cast<double*>(c->stage((2 * R + L.cols) * sizeof(double)));
     ck(cudaMemcpyAsync(st, d.z, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
@@ -736,10 +809,12 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
       if (r->lambda) r->lambda[ref] = st[R + dd];
     }
   }
-  if (r->trace && ctl.t > 0)
-    ck(cudaMemcpy(r->trace, c->d_trace, static_cast<std::size_t>(ctl.t) * 6 * sizeof(double),
-                  cudaMemcpyDeviceToHost),
+  if (r->trace && ctl.t > 0) {
+    ck(cudaMemcpyAsync(r->trace, c->d_trace, static_cast<std::size_t>(ctl.t) * 6 * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->stream),
        "trace d2h");
+    ck(cudaStreamSynchronize(c->stream), "trace d2h");
+  }
   r->time_download = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_dn0).count();
   r->time_upload = std::chrono::duration<double>(t_dn0 - t_up0).count() - c->last_kernel_s;
 }
@@ -1263,6 +1338,32 @@ int dopf_cuda_pin_model(dopf_cuda_ctx* c, const dopf_model_view* m) {
   });
 }
 
+int dopf_cuda_pin_host(dopf_cuda_ctx* c, const void* ptr, int64_t bytes) {
+  if (!c || !ptr || bytes <= 0) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (std::find(c->pinned.begin(), c->pinned.end(), ptr) != c->pinned.end()) return;
+    const cudaError_t e =
+        cudaHostRegister(const_cast<void*>(ptr), static_cast<std::size_t>(bytes), cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      cudaGetLastError();
+      return;
+    }
+    ck(e, "cudaHostRegister");
+    c->pinned.push_back(ptr);
+  });
+}
+
+int dopf_cuda_unpin_host(dopf_cuda_ctx* c, const void* ptr) {
+  if (!c || !ptr) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    auto it = std::find(c->pinned.begin(), c->pinned.end(), ptr);
+    if (it == c->pinned.end()) return;
+    ck(cudaHostUnregister(const_cast<void*>(ptr)), "cudaHostUnregister");
+    c->pinned.erase(it);
+  });
+}
+
 int dopf_cuda_unpin_model(dopf_cuda_ctx* c, const dopf_model_view* m) {
   if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
@@ -1338,6 +1439,7 @@ void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   for (const void* ptr : c->pinned) cudaHostUnregister(const_cast<void*>(ptr));
   c->free_model();
   if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->h_small) cudaFreeHost(c->h_small);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);

@@ -26,4 +26,11 @@ cudaError_t launch_final_iterates(const double* zring, const double* lring, int6
                                   const int32_t* row0, const int32_t* rows, const int32_t* iters,
                                   int instances, int ring, double* zout, double* lout, cudaStream_t s);
 
+/// Single instance: the stopping iterate (ring slot iters[0] % ring) of z and
+/// lambda permuted to reference order, and {iters, status, maxinf, objective}.
+cudaError_t launch_final_single(const double* zring, const double* lring, int64_t rows, const int32_t* ref_of_dev,
+                                const int32_t* iters, int ring, const int32_t* status, const double* maxinf,
+                                const double* obj, double* zout, double* lout, double* scalars, int sm_count,
+                                cudaStream_t s);
+
 }  // namespace dopf::cuda

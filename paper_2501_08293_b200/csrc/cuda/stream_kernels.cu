@@ -541,6 +541,21 @@ __global__ void k_regather(const StreamRegather g) {
   }
 }
 
+// results to reference order on the device: z, lambda by device row -> reference
+// copy index, x by column -> global column
+__global__ void k_stream_results(const double* z, const double* lam, const double* x, const int32_t* ref_of_dev,
+                                 const int32_t* gcol, int64_t rows, int64_t cols, double* zout, double* lout,
+                                 double* xout) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t d = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; d < rows; d += stride) {
+    const int32_t ref = ref_of_dev[d];
+    zout[ref] = z[d];
+    lout[ref] = lam[d];
+  }
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < cols; q += stride)
+    xout[gcol[q]] = x[q];
+}
+
 __global__ void k_div_rho_check(const double* a, int64_t n, double rho, double rinv, double* out) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -548,6 +563,13 @@ __global__ void k_div_rho_check(const double* a, int64_t n, double rho, double r
 }
 
 }  // namespace
+
+cudaError_t stream_launch_results(const double* z, const double* lam, const double* x, const int32_t* ref_of_dev,
+                                  const int32_t* gcol, int64_t rows, int64_t cols, double* zout, double* lout,
+                                  double* xout, int sm_count, cudaStream_t s) {
+  k_stream_results<<<4 * sm_count, 256, 0, s>>>(z, lam, x, ref_of_dev, gcol, rows, cols, zout, lout, xout);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_div_rho_check(const double* a, int64_t n, double rho, double rinv, double* out, cudaStream_t s) {
   k_div_rho_check<<<1024, 256, 0, s>>>(a, n, rho, rinv, out);

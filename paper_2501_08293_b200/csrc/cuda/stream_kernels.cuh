@@ -88,6 +88,11 @@ struct StreamRegather {
 };
 cudaError_t stream_launch_regather(const StreamRegather& g, int sm_count, cudaStream_t s);
 
+/// Final iterates in reference order (z, lambda: N_z; x: n) for a direct copy back.
+cudaError_t stream_launch_results(const double* z, const double* lam, const double* x, const int32_t* ref_of_dev,
+                                  const int32_t* gcol, int64_t rows, int64_t cols, double* zout, double* lout,
+                                  double* xout, int sm_count, cudaStream_t s);
+
 /// div_rho self-check (dopf_cuda_div_rho_check).
 cudaError_t launch_div_rho_check(const double* a, int64_t n, double rho, double rinv, double* out, cudaStream_t s);
 

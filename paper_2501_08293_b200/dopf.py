@@ -558,6 +558,11 @@ class CudaSolver:
             model.precompute()
         self._err(self._lib.dopf_cuda_pin_model(self._h, C.byref(model.view())))
 
+    def pin_array(self, a: np.ndarray) -> None:
+        """Page-lock a caller buffer (keep it alive while pinned)."""
+        if a.nbytes:
+            self._err(self._lib.dopf_cuda_pin_host(self._h, C.c_void_p(a.ctypes.data), a.nbytes))
+
     def unpin(self, model: "DecomposedModel") -> None:
         self._err(self._lib.dopf_cuda_unpin_model(self._h, C.byref(model.view())))
 
