@@ -777,7 +777,9 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   c->last_kernel_s = ms * 1e-3;
   const auto t_dn0 = std::chrono::steady_clock::now();
   const StreamCtl ctl = *ctl_h;
-  c->kernels += 3ll * ctl.t + (direct ? 1 : 0);
+  // per iteration: k_global, k_final, and the staged and/or direct chunk kernels
+  const long long per_it = 2 + (c->SL.staged_ids.empty() ? 0 : 1) + (c->SL.big_ids.empty() ? 0 : 1);
+  c->kernels += per_it * ctl.t + (direct ? 1 : 0);
   if (const char* e = std::getenv("DOPF_STREAM_PROF"); e && e[0] == '1' && ctl.t > 0) {
     std::vector<long long> h(static_cast<std::size_t>(c->staged_grid) * 8);
     ck(cudaMemcpy(h.data(), c->bufs.at(126).p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "prof");
@@ -1249,7 +1251,7 @@ int dopf_cuda_part_step(dopf_cuda_ctx* c, int32_t phase) {
       c->kernels += 1;
     } else if (phase == 1) {
       stream_launch_local(p, c->stream);
-      c->kernels += p.max_export > 0 ? 3 : 2;
+      c->kernels += 1 + (p.n_staged > 0 ? 1 : 0) + (p.n_big > 0 ? 1 : 0) + (p.max_export > 0 ? 1 : 0);
     } else if (phase == 2) {
       stream_launch_decide(p, c->sd.ranks, c->SL.nparts, c->stream);
       c->kernels += 1;
