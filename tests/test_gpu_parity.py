@@ -372,3 +372,40 @@ def test_stream_direct_and_staged_chunk_mix_bitwise(monkeypatch, stage_kb, ctas,
     gpu = s.solve(settings)
     ref = O.solve(model, dopf.Settings(max_iter=150, workers=8))
     assert_same(gpu, ref, bitwise=True)
+
+
+@pytest.mark.parametrize("path", ["resident", "stream"])
+def test_pinned_inputs_and_results_bitwise(path):
+    """Page-locked model arrays (dopf_cuda_pin_model) and result buffers: the
+    uploads take the DMA path and results are copied straight into the
+    caller's arrays -- same bits as the oracle."""
+    import ctypes as C
+    from paper_2501_08293_b200 import _native as N
+    f = dopf.synthetic_feeder("ieee123", 123)
+    _, _, model = dopf.load_model(f, workers=4)
+    model.precompute(4)
+    s = dopf.CudaSolver(0)
+    s.set_path(path)
+    s.pin(model)
+    s.pin(model)  # pinning twice is a no-op
+    settings = dopf.Settings()
+    ref = O.solve(model, dopf.Settings(workers=8))
+    v = model.view()
+    x, z, lam = np.zeros(v.n), np.zeros(v.N_z), np.zeros(v.N_z)
+    tr = np.zeros((settings.max_iter, 6))
+    for a in (x, z, lam, tr):
+        s.pin_array(a)
+    lib = N.cuda()
+    for _ in range(2):  # second upload: same structure, values-only path
+        assert lib.dopf_cuda_upload(s._h, C.byref(v)) == 0
+        r = N.ResultView_t()
+        r.x = x.ctypes.data_as(C.POINTER(C.c_double))
+        r.z = z.ctypes.data_as(C.POINTER(C.c_double))
+        r.lambda_ = lam.ctypes.data_as(C.POINTER(C.c_double))
+        r.trace = tr.ctypes.data_as(C.POINTER(C.c_double))
+        assert lib.dopf_cuda_solve(s._h, C.byref(settings.to_c()), C.byref(r)) == 0
+        assert r.iterations == ref.iterations and r.status == ref.status
+        for a, b in ((x, ref.x), (z, ref.z), (lam, ref.lam)):
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+        np.testing.assert_allclose(tr[:r.iterations, 1:], ref.trace[:, 1:], rtol=1e-9, atol=1e-13)
+    s.unpin(model)
