@@ -127,9 +127,10 @@ def cuda() -> C.CDLL:
     if _cuda is not None:
         return _cuda
     host()
-    if not os.path.exists(CUDA_SO):
-        raise RuntimeError(f"CUDA solver library missing: {CUDA_SO} (run __graft_entry__.build())")
-    lib = C.CDLL(CUDA_SO, mode=C.RTLD_GLOBAL)
+    path = os.environ.get("DOPF_CUDA_SO", CUDA_SO)  # alternative build, for A/B measurements only
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA solver library missing: {path} (run __graft_entry__.build())")
+    lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
     _sig(lib, "dopf_cuda_create", C.c_int, C.c_int, P(vp))
     _sig(lib, "dopf_cuda_upload", C.c_int, vp, P(ModelView_t))
     _sig(lib, "dopf_cuda_solve", C.c_int, vp, P(Settings_t), P(ResultView_t))

@@ -167,26 +167,19 @@ __device__ __forceinline__ void chunk_iteration(const StreamParams& p, const uns
   const double rho = p.rho;
   // the chunk's sections, read once (later smem stores could alias them for the compiler)
   const int rows = h.rows, arows = h.arows, icols = h.icols, row0 = h.row0, icol0 = h.icol0;
-  const StreamRow* s_rm = reinterpret_cast<const StreamRow*>(img + h.off[kImgRmeta]);
-  const double* s_v = reinterpret_cast<const double*>(img + h.off[kImgV]);
-  const int2* s_ps = reinterpret_cast<const int2*>(img + h.off[kImgPslice]);
-  const int2* s_as = reinterpret_cast<const int2*>(img + h.off[kImgAslice]);
+  const StreamRow* s_rows = reinterpret_cast<const StreamRow*>(img + h.off[kImgRows]);
+  const int2* s_sl = reinterpret_cast<const int2*>(img + h.off[kImgSlices]);
   const double* s_P = reinterpret_cast<const double*>(img + h.off[kImgP]);
   const double* s_A = reinterpret_cast<const double*>(img + h.off[kImgA]);
-  const StreamARow* s_am = reinterpret_cast<const StreamARow*>(img + h.off[kImgAmeta]);
-  const double* s_ab = reinterpret_cast<const double*>(img + h.off[kImgAb]);
-  const double* s_cost = reinterpret_cast<const double*>(img + h.off[kImgCost]);
-  const double* s_inv = reinterpret_cast<const double*>(img + h.off[kImgInv]);
-  const double* s_lo = reinterpret_cast<const double*>(img + h.off[kImgLo]);
-  const double* s_hi = reinterpret_cast<const double*>(img + h.off[kImgHi]);
-  const uint8_t* s_own = img + h.off[kImgOwner];
-  const int32_t* s_cp = reinterpret_cast<const int32_t*>(img + h.off[kImgCptr]);
-  const int32_t* s_cc = reinterpret_cast<const int32_t*>(img + h.off[kImgCopies]);
+  const StreamARow* s_ar = reinterpret_cast<const StreamARow*>(img + h.off[kImgArows]);
+  const StreamCol* s_cols = reinterpret_cast<const StreamCol*>(img + h.off[kImgCols]);
+  const uint32_t* s_cm = reinterpret_cast<const uint32_t*>(img + h.off[kImgCmeta]);
+  const int16_t* s_cc = reinterpret_cast<const int16_t*>(img + h.off[kImgCopies]);
   const bool on = r < rows;
-  StreamRow rm{0, 0, -1, -1};
+  StreamRow rm{0, 0, -1, -1, 0.0};
   double lamv = 0.0, q = 0.0;
   if (on) {
-    rm = s_rm[r];
+    rm = s_rows[r];
     lamv = lin[r];
     const double zprev = zin[r];
     q = div_rho(lamv, rho, p.rho_inv);
@@ -195,16 +188,18 @@ __device__ __forceinline__ void chunk_iteration(const StreamParams& p, const uns
   }
   sync();
   if (r < icols) {  // interior column: admm.cpp:118-129 over the chunk's own copies
-    const int q1 = s_cp[r + 1];
+    const uint32_t cm = s_cm[r];
+    const int16_t* cc = s_cc + cmeta_start(cm);
+    const int cnt = cmeta_count(cm);
     double acc = 0.0;
 #pragma unroll 1
-    for (int e = s_cp[r]; e < q1; ++e) acc = acc + ush[s_cc[e]];  // ascending s
-    const double cost = s_cost[r];
-    const double unclamped = (acc - div_rho(cost, rho, p.rho_inv)) * s_inv[r];
-    const double xv = sel_min(sel_max(unclamped, s_lo[r]), s_hi[r]);
+    for (int e = 0; e < cnt; ++e) acc = acc + ush[cc[e]];  // ascending s
+    const StreamCol col = s_cols[r];
+    const double unclamped = (acc - div_rho(col.cost, rho, p.rho_inv)) * col.inv;
+    const double xv = sel_min(sel_max(unclamped, col.lo), col.hi);
     xsh[r] = xv;
     p.x[icol0 + r] = xv;
-    if (s_own[r]) v[6] = v[6] + cost * xv;
+    if (cmeta_owner(cm)) v[6] = v[6] + col.cost * xv;
   }
   sync();
   double bx = 0.0;
@@ -214,8 +209,8 @@ __device__ __forceinline__ void chunk_iteration(const StreamParams& p, const uns
   }
   sync();
   if (on) {
-    const double acc = row_dot(s_P + s_ps[warp].x + lane, tgt + rm.base, rm.n, ld);
-    const double z = acc + s_v[r];
+    const double acc = row_dot(s_P + s_sl[warp].x + lane, tgt + rm.base, rm.n, ld);
+    const double z = acc + rm.v;
     const double dd = bx - z;
     const double ln = lamv + rho * dd;  // admm.cpp:142
     const int d = row0 + r;
@@ -232,9 +227,9 @@ __device__ __forceinline__ void chunk_iteration(const StreamParams& p, const uns
   }
   sync();
   if (r < arows) {  // ||A_s z_s - b_s||_inf (admm.cpp:203-205)
-    const StreamARow am = s_am[r];
-    const double acc = row_dot(s_A + s_as[warp].x + lane, ush + am.base, am.n, ld);
-    v[5] = sel_max(v[5], fabs(acc - s_ab[r]));
+    const StreamARow ar = s_ar[r];
+    const double acc = row_dot(s_A + s_sl[warp].y + lane, ush + ar.base, ar.n, ld);
+    v[5] = sel_max(v[5], fabs(acc - ar.b));
   }
 }
 
@@ -349,7 +344,7 @@ __device__ __forceinline__ void compute_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kStagedRows) : "memory");
 }
 
-template <int kCtasPerSm>
+template <int kCtasPerSm, bool kProf>
 __global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const StreamParams p) {
   extern __shared__ __align__(128) unsigned char stages[];  // [p.stages][p.stage_bytes]
   __shared__ double tgt[kStagedRows], ush[kStagedRows], xsh[kStagedRows], zsh[kStagedRows];
@@ -402,7 +397,7 @@ __global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const Str
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   // optional phase clock (thread 0): [0] data wait, [1] rows/u, [2] interior x,
   // [3] target, [4] GEMV/dual, [5] A z - b + release
-  const bool prof = p.prof != nullptr && tid == 0;
+  const bool prof = kProf && tid == 0;  // compiled out unless profiling
   long long ph[6] = {0, 0, 0, 0, 0, 0}, last = 0;
   int phase = 0;
   auto sync = [&] {
@@ -587,21 +582,26 @@ LocalKernel local_kernel() { return &k_local; }
 
 cudaError_t stream_prepare() {
   static cudaError_t e = [] {
-    cudaError_t e2 = cudaFuncSetAttribute(k_staged<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    if (e2 == cudaSuccess)
-      e2 = cudaFuncSetAttribute(k_staged<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+    cudaError_t e2 = cudaSuccess;
+    for (auto k : {&k_staged<2, false>, &k_staged<2, true>})
+      if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (auto k : {&k_staged<3, false>, &k_staged<3, true>})
+      if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
     return e2;
   }();
   return e;
 }
 
 using StagedKernel = void (*)(const StreamParams);
-StagedKernel staged_kernel(int ctas_per_sm) { return ctas_per_sm >= 3 ? &k_staged<3> : &k_staged<2>; }
+StagedKernel staged_kernel(int ctas_per_sm, bool prof) {
+  if (ctas_per_sm >= 3) return prof ? &k_staged<3, true> : &k_staged<3, false>;
+  return prof ? &k_staged<2, true> : &k_staged<2, false>;
+}
 
 void launch_local_all(const StreamParams& p, cudaStream_t s) {
   if (p.n_big > 0) local_kernel()<<<p.n_big, kStreamRows, 0, s>>>(p);
   if (p.n_staged > 0)
-    staged_kernel(p.staged_ctas)<<<p.staged_grid, kStagedThreads, p.stages * p.stage_bytes, s>>>(p);
+    staged_kernel(p.staged_ctas, p.prof != nullptr)<<<p.staged_grid, kStagedThreads, p.stages * p.stage_bytes, s>>>(p);
 }
 
 void stream_launch_iteration(const StreamParams& p, cudaStream_t s) {
@@ -654,7 +654,7 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   kb.func = reinterpret_cast<void*>(local_kernel());
   kb.gridDim = dim3(p.n_big);
   ks = kg;
-  ks.func = reinterpret_cast<void*>(staged_kernel(p.staged_ctas));
+  ks.func = reinterpret_cast<void*>(staged_kernel(p.staged_ctas, p.prof != nullptr));
   ks.gridDim = dim3(p.staged_grid);
   ks.blockDim = dim3(kStagedThreads);
   ks.sharedMemBytes = p.stages * p.stage_bytes;

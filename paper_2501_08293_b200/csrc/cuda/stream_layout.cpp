@@ -258,19 +258,20 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
       }
     }
     // row metadata: interior column index or boundary import slot
-    std::vector<StreamRow> rmeta(ch.rows);
+    struct RowMeta { int16_t n, base, xloc, xin; };
+    std::vector<RowMeta> rmeta(ch.rows);
     ch.bimp0 = static_cast<int32_t>(L.bimp.size());
     for (int r = 0; r < ch.rows; ++r) {
       const int32_t ref = L.ref_of_dev[ch.row0 + r];
       const int32_t col = loc_of_col[m.l2g[ref]];
-      StreamRow rm{prow[r].n, prow[r].base, -1, -1};
+      RowMeta rm{static_cast<int16_t>(prow[r].n), static_cast<int16_t>(prow[r].base), -1, -1};
       if (col >= L.bcols) {
-        rm.xloc = col - ch.icol0;
+        rm.xloc = static_cast<int16_t>(col - ch.icol0);
       } else {
         for (int e = ch.bimp0; e < static_cast<int>(L.bimp.size()); ++e)
-          if (L.bimp[e] == col) rm.xin = e - ch.bimp0;
+          if (L.bimp[e] == col) rm.xin = static_cast<int16_t>(e - ch.bimp0);
         if (rm.xin < 0) {
-          rm.xin = static_cast<int32_t>(L.bimp.size()) - ch.bimp0;
+          rm.xin = static_cast<int16_t>(L.bimp.size() - ch.bimp0);
           L.bimp.push_back(col);
         }
       }
@@ -278,14 +279,15 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     }
     ch.nbimp = static_cast<int32_t>(L.bimp.size()) - ch.bimp0;
     // interior columns: chunk-local CSR over their copies (ascending s)
-    std::vector<int32_t> cptr(1, 0), icopies;
-    std::vector<uint8_t> own;
+    std::vector<uint32_t> cmeta;
+    std::vector<int16_t> icopies;
     for (int e = 0; e < ch.icols; ++e) {
       const int32_t gc = L.gcol[ch.icol0 + e];
+      const uint32_t start = static_cast<uint32_t>(icopies.size());
       for (int k2 = m.csr_ptr[gc]; k2 < m.csr_ptr[gc + 1]; ++k2)
-        icopies.push_back(dev_of_ref[m.csr_copy[k2]] - ch.row0);
-      cptr.push_back(static_cast<int32_t>(icopies.size()));
-      own.push_back(L.owner[ch.icol0 + e]);
+        icopies.push_back(static_cast<int16_t>(dev_of_ref[m.csr_copy[k2]] - ch.row0));
+      const uint32_t cnt = static_cast<uint32_t>(icopies.size()) - start;
+      cmeta.push_back(start | (cnt << 12) | (L.owner[ch.icol0 + e] ? 0x80000000u : 0u));
     }
     // the image
     ch.image_off = static_cast<int64_t>(8 * L.blob.size());
@@ -294,18 +296,22 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     head.rows = ch.rows;
     head.arows = ch.arows;
     head.icols = ch.icols;
-    head.icopies = static_cast<int32_t>(icopies.size());
     head.nbimp = ch.nbimp;
     head.row0 = ch.row0;
     head.icol0 = ch.icol0;
     head.bimp0 = ch.bimp0;
     const std::size_t head_at = L.blob.size();
     for (std::size_t i = 0; i < sizeof(ChunkHead) / 8; ++i) w.put(0.0, -2);  // ChunkHead (filled below)
-    head.off[kImgRmeta] = w.here();
-    w.put_meta(rmeta);
-    head.off[kImgV] = w.here();
-    for (int r = 0; r < ch.rows; ++r) w.put_value(m.v, ro[kRawV], L.ref_of_dev[ch.row0 + r]);
-    w.align16();
+    auto put_meta_word = [&](const void* p8) {  // 8 bytes of metadata as one word
+      double d;
+      std::memcpy(&d, p8, 8);
+      w.put(d, -2);
+    };
+    head.off[kImgRows] = w.here();
+    for (int r = 0; r < ch.rows; ++r) {  // {n, base, xloc, xin | v}
+      put_meta_word(&rmeta[r]);
+      w.put_value(m.v, ro[kRawV], L.ref_of_dev[ch.row0 + r]);
+    }
     // sliced ELL of P and A per warp of 32 rows
     auto pack = [&](const std::vector<Src>& rows, const double* raw, int64_t sec, std::vector<int32_t>& slices) {
       const std::size_t sec_start = L.blob.size();
@@ -313,8 +319,7 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
         const int lanes = std::min(32, static_cast<int>(rows.size()) - w0);
         int width = 0;
         for (int l = 0; l < lanes; ++l) width = std::max(width, rows[w0 + l].n);
-        slices.push_back(static_cast<int32_t>(L.blob.size() - sec_start));  // {offset, width} per warp
-        slices.push_back(width);
+        slices.push_back(static_cast<int32_t>(L.blob.size() - sec_start));
         for (int j = 0; j < width; ++j)
           for (int l = 0; l < 32; ++l) {
             if (l < lanes && j < rows[w0 + l].n) w.put_value(raw, sec, rows[w0 + l].at + j);
@@ -323,38 +328,37 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
       }
     };
     std::vector<int32_t> pslice, aslice;
-    // slice tables precede the sections they index: reserve, pack, then patch
-    const int pw = (ch.rows + 31) / 32, aw = (ch.arows + 31) / 32;
-    head.off[kImgPslice] = w.here();
-    const std::size_t ps_at = L.blob.size();
-    w.put_meta(std::vector<int32_t>(2 * pw, 0));
-    head.off[kImgAslice] = w.here();
-    const std::size_t as_at = L.blob.size();
-    w.put_meta(std::vector<int32_t>(2 * aw, 0));
+    // the slice table precedes the sections it indexes: reserve, pack, then patch
+    const int nw = std::max((ch.rows + 31) / 32, (ch.arows + 31) / 32);
+    head.off[kImgSlices] = w.here();
+    const std::size_t sl_at = L.blob.size();
+    w.put_meta(std::vector<int32_t>(2 * nw, 0));
     head.off[kImgP] = w.here();
     pack(prow, m.P, ro[kRawP], pslice);
     head.off[kImgA] = w.here();
     pack(arow, m.A, ro[kRawA], aslice);
-    if (!pslice.empty()) std::memcpy(&L.blob[ps_at], pslice.data(), pslice.size() * 4);
-    if (!aslice.empty()) std::memcpy(&L.blob[as_at], aslice.data(), aslice.size() * 4);
-    std::vector<StreamARow> ameta(ch.arows);
-    for (int a = 0; a < ch.arows; ++a) ameta[a] = StreamARow{arow[a].n, arow[a].base};
-    head.off[kImgAmeta] = w.here();
-    w.put_meta(ameta);
-    head.off[kImgAb] = w.here();
-    for (int a = 0; a < ch.arows; ++a) w.put_value(m.b, ro[kRawB], bsrc[a]);
-    w.align16();
-    const int sec_of[4] = {kRawC, kRawInv, kRawLo, kRawHi};
-    const double* raw_of[4] = {m.c, m.inv_copy, m.x_lo, m.x_hi};
-    for (int f = 0; f < 4; ++f) {
-      head.off[kImgCost + f] = w.here();
-      for (int e = 0; e < ch.icols; ++e) w.put_value(raw_of[f], ro[sec_of[f]], L.gcol[ch.icol0 + e]);
-      w.align16();
+    {
+      std::vector<int32_t> sl(2 * nw, 0);
+      for (std::size_t i = 0; i < pslice.size(); ++i) sl[2 * i] = pslice[i];
+      for (std::size_t i = 0; i < aslice.size(); ++i) sl[2 * i + 1] = aslice[i];
+      std::memcpy(&L.blob[sl_at], sl.data(), sl.size() * 4);
     }
-    head.off[kImgOwner] = w.here();
-    w.put_meta(own);
-    head.off[kImgCptr] = w.here();
-    w.put_meta(cptr);
+    head.off[kImgArows] = w.here();
+    for (int a = 0; a < ch.arows; ++a) {  // {n, base | b}
+      const int32_t nb[2] = {arow[a].n, arow[a].base};
+      put_meta_word(nb);
+      w.put_value(m.b, ro[kRawB], bsrc[a]);
+    }
+    head.off[kImgCols] = w.here();
+    for (int e = 0; e < ch.icols; ++e) {  // {cost, inv, lo, hi}
+      const int32_t gc = L.gcol[ch.icol0 + e];
+      w.put_value(m.c, ro[kRawC], gc);
+      w.put_value(m.inv_copy, ro[kRawInv], gc);
+      w.put_value(m.x_lo, ro[kRawLo], gc);
+      w.put_value(m.x_hi, ro[kRawHi], gc);
+    }
+    head.off[kImgCmeta] = w.here();
+    w.put_meta(cmeta);
     head.off[kImgCopies] = w.here();
     w.put_meta(icopies);
     ch.image_bytes = static_cast<int32_t>(w.here());

@@ -37,16 +37,24 @@ constexpr int kMaxStages = 8;
 constexpr int kDefaultStages = 2;
 constexpr int kDefaultStageBytes = 48 * 1024;
 
-struct StreamRow {
-  int32_t n;      // n_s
-  int32_t base;   // chunk-local row of (s, 0)
-  int32_t xloc;   // interior column: index among the chunk's interior columns, else -1
-  int32_t xin;    // boundary column: slot in the chunk's import list, else -1
+struct StreamRow {   // one row of a chunk image (16 bytes: one 128-bit shared-memory load)
+  int16_t n;         // n_s
+  int16_t base;      // chunk-local row of (s, 0)
+  int16_t xloc;      // interior column: index among the chunk's interior columns, else -1
+  int16_t xin;       // boundary column: slot in the chunk's import list, else -1
+  double v;          // min-norm shift v_s entry (admm.cpp:137)
 };
+static_assert(sizeof(StreamRow) == 16, "StreamRow is 16 bytes");
 
-struct StreamARow {
-  int32_t n;      // n_s (0: no equality row for this thread)
-  int32_t base;   // chunk-local row of (s, 0)
+struct StreamARow {  // one equality row (16 bytes)
+  int32_t n;         // n_s
+  int32_t base;      // chunk-local row of (s, 0)
+  double b;          // b_s entry
+};
+static_assert(sizeof(StreamARow) == 16, "StreamARow is 16 bytes");
+
+struct StreamCol {   // one interior column (32 bytes)
+  double cost, inv, lo, hi;
 };
 
 struct StreamChunk {
@@ -63,19 +71,20 @@ struct StreamChunk {
 static_assert(sizeof(StreamChunk) == 40, "StreamChunk layout");
 
 // byte offsets of the sections of a chunk image (relative to its start)
-enum ImageSection {
-  kImgRmeta, kImgV, kImgPslice, kImgAslice, kImgP, kImgA, kImgAmeta, kImgAb, kImgCost, kImgInv, kImgLo,
-  kImgHi, kImgOwner, kImgCptr, kImgCopies, kImgSections
+enum ImageSection { kImgRows, kImgSlices, kImgP, kImgA, kImgArows, kImgCols, kImgCmeta, kImgCopies, kImgSections };
+struct ChunkHead {                 // the first 64 bytes of every chunk image
+  int32_t rows, arows, icols, nbimp;
+  int32_t row0, icol0, bimp0, image_bytes;
+  uint32_t off[kImgSections];      // byte offsets, 16-byte aligned
 };
-struct ChunkHead {                 // the first 112 bytes of every chunk image
-  int32_t rows, arows, icols, icopies, nbimp;
-  int32_t row0, icol0, bimp0, image_bytes, pad[3];
-  uint32_t off[16];                // [kImgSections] byte offsets, 16-byte aligned
-};
-static_assert(sizeof(ChunkHead) == 112, "ChunkHead is 112 bytes");
-// pslice / aslice: per warp {int32 offset (in doubles) of its slice from the
-// start of the P / A section, int32 slice width}; cptr: int32 CSR offsets (icols + 1) into copies;
-// copies: int32 chunk-local rows; owner: uint8 per interior column.
+static_assert(sizeof(ChunkHead) == 64, "ChunkHead is 64 bytes");
+// rows: StreamRow per row; slices: per warp {int32 P offset, int32 A offset}
+// (in doubles, from the P / A section starts); arows: StreamARow per equality
+// row; cols: StreamCol per interior column; cmeta: per interior column
+// first copy | count << 12 | owner << 31; copies: int16 chunk-local rows.
+DOPF_HD constexpr int cmeta_start(uint32_t m) { return static_cast<int>(m & 0xfffu); }
+DOPF_HD constexpr int cmeta_count(uint32_t m) { return static_cast<int>((m >> 12) & 0x7ffffu); }
+DOPF_HD constexpr bool cmeta_owner(uint32_t m) { return (m >> 31) != 0; }
 
 // Shared-memory stage of the staged kernel: the image, then the z and lambda
 // slices and the import slots, each copied with its source start rounded
