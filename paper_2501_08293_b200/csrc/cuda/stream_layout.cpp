@@ -1,6 +1,8 @@
 #include "stream_layout.hpp"
 
 #include <algorithm>
+#include <functional>
+#include <map>
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
@@ -108,23 +110,50 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
       StreamChunk ch{};
       ch.row0 = row;
       int rows = 0, arows = 0;
-      double est = 1024.0;
+      // exact sliced-ELL sizes of the chunk's P and A (rows sorted widest first,
+      // a warp slice as wide as its first row) from per-width row counts, plus
+      // upper bounds for everything else in the stage -- a chunk built here
+      // always fits
+      std::map<int, int, std::greater<int>> prow_w, arow_w;  // width -> rows
+      auto ell_bytes = [](const std::map<int, int, std::greater<int>>& hist) {
+        int64_t bytes = 0, row = 0;
+        for (const auto& [width, count] : hist) {
+          const int64_t first_warp = (row + 31) / 32, end_warp = (row + count + 31) / 32;
+          bytes += 8 * 32 * static_cast<int64_t>(width) * (end_warp - first_warp);
+          row += count;
+        }
+        return bytes;
+      };
+      auto stage_bound = [&](int r, int a) {
+        const int64_t nw = (std::max(r, a) + 31) / 32;
+        return 64 + 16 * ((8 * nw + 15) / 16) + ell_bytes(prow_w) + ell_bytes(arow_w) + 16LL * a +
+               16LL * r                                      // row records
+               + (32 + 4 + 2 + 8) * static_cast<int64_t>(r)  // interior columns, copies, imports (<= rows)
+               + 16LL * r + 128;                              // z, lambda slices + alignment
+      };
       std::vector<int> members;
       while (k < order.size()) {
         const int s = order[k];
         const int n = ns_of(s), ms = m.m_s[s];
-        // stage estimate (operators with sliced-ELL padding headroom + per-row/column data)
-        const double add =
-            1.25 * 8.0 * (static_cast<double>(n) * n + static_cast<double>(ms) * n) + 100.0 * n + 24.0 * ms;
         // several subsystems share a chunk only within the staged kernel's
         // limits; a wider one gets a chunk of its own (direct-load kernel)
-        if (!members.empty() &&
-            (rows + n > kStagedRows || arows + ms > kStagedRows || est + add > 0.9 * L.stage_bytes))
-          break;
+        if (!members.empty()) {
+          if (rows + n > kStagedRows || arows + ms > kStagedRows) break;
+          prow_w[n] += n;
+          if (ms) arow_w[n] += ms;
+          const bool fits = stage_bound(rows + n, arows + ms) <= L.stage_bytes;
+          if (!fits) {
+            if ((prow_w[n] -= n) == 0) prow_w.erase(n);
+            if (ms && (arow_w[n] -= ms) == 0) arow_w.erase(n);
+            break;
+          }
+        } else {
+          prow_w[n] += n;
+          if (ms) arow_w[n] += ms;
+        }
         members.push_back(s);
         rows += n;
         arows += ms;
-        est += add;
         ++k;
       }
       // widest first inside the chunk: the 32 rows of a warp slice then have
