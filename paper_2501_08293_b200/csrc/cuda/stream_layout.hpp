@@ -32,7 +32,10 @@ namespace dopf::cuda {
 constexpr int kStreamRows = 512;   // rows of the widest chunk (direct-load kernel threads)
 // staged kernel: chunks of <= kStagedRows rows whose shared-memory stage
 // (image + z + lambda + imports) fits `stage_bytes`; `stages` stages per CTA
-constexpr int kStagedRows = 256;
+#ifndef DOPF_STAGED_ROWS
+#define DOPF_STAGED_ROWS 256
+#endif
+constexpr int kStagedRows = DOPF_STAGED_ROWS;
 constexpr int kMaxStages = 8;
 constexpr int kDefaultStages = 2;
 constexpr int kDefaultStageBytes = 48 * 1024;
