@@ -103,13 +103,17 @@ __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p)
   const int c = blockIdx.x * kStreamRows + threadIdx.x;
   double o[1] = {0.0};
   if (c < p.bcols) {
-    // the column's first four copies: index loads, then value loads, all in
-    // flight before the ascending-s sum
-    const int q0 = p.col_ptr[c], q1 = p.col_ptr[c + 1];
+    // every load that does not depend on another goes out first (column data,
+    // import range, copy range), then the copies' indices, then their u
+    const int q0 = __ldg(p.col_ptr + c), q1 = __ldg(p.col_ptr + c + 1);
+    const double cost = __ldg(p.cost + c), inv = __ldg(p.inv + c), lo = __ldg(p.lo + c), hi = __ldg(p.hi + c);
+    const int i0 = __ldg(p.imp_ptr + c), i1 = __ldg(p.imp_ptr + c + 1);
+    const bool own = __ldg(p.owner + c) != 0;
     int32_t ref[4];
     double uv[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) ref[e] = q0 + e < q1 ? p.copies[q0 + e] : 0;
+    for (int e = 0; e < 4; ++e) ref[e] = q0 + e < q1 ? __ldg(p.copies + q0 + e) : 0;
+    const double cr = div_rho(cost, p.rho, p.rho_inv);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       uv[e] = q0 + e < q1 ? (ref[e] >= 0 ? p.u[ref[e]] : p.u_remote[-ref[e] - 1]) : 0.0;
@@ -121,11 +125,11 @@ __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p)
       const int32_t rq = p.copies[q];
       acc = acc + (rq >= 0 ? p.u[rq] : p.u_remote[-rq - 1]);
     }
-    const double unclamped = (acc - div_rho(p.cost[c], p.rho, p.rho_inv)) * p.inv[c];
-    const double xv = sel_min(sel_max(unclamped, p.lo[c]), p.hi[c]);
+    const double unclamped = (acc - cr) * inv;
+    const double xv = sel_min(sel_max(unclamped, lo), hi);
     p.x[c] = xv;
-    for (int e = p.imp_ptr[c]; e < p.imp_ptr[c + 1]; ++e) p.ximp[p.imp_slot[e]] = xv;  // chunk imports
-    if (p.owner[c]) o[0] = p.cost[c] * xv;
+    for (int e = i0; e < i1; ++e) p.ximp[__ldg(p.imp_slot + e)] = xv;  // chunk imports
+    if (own) o[0] = cost * xv;
   }
   block_reduce<1, kStreamRows>(o, sh, -1);
   if (threadIdx.x == 0) p.objp[blockIdx.x] = o[0];
