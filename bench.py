@@ -357,7 +357,9 @@ def main():
     import torch
     if world > 1:
         import torch.distributed as td
-        backend = os.environ.get("DOPF_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        shared = os.environ.get("DOPF_SHARE_GPU") == "1"  # NCCL refuses two ranks on one GPU
+        backend = os.environ.get("DOPF_DIST_BACKEND") or (
+            "nccl" if torch.cuda.is_available() and not shared else "gloo")
         td.init_process_group(backend=backend)
     if args.impl == "reference":
         run_reference(args, rank, world)
