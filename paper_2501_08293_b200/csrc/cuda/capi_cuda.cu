@@ -779,7 +779,9 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   const StreamCtl ctl = *ctl_h;
   // per iteration: k_global, k_final, and the staged and/or direct chunk kernels
   const long long per_it = 2 + (c->SL.staged_ids.empty() ? 0 : 1) + (c->SL.big_ids.empty() ? 0 : 1);
-  c->kernels += per_it * ctl.t + (direct ? 1 : 0);
+  const char* ng = std::getenv("DOPF_STREAM_NOGRAPH");
+  const long long unroll = (ng && ng[0] == '1') ? 1 : stream_graph_unroll();  // whole bodies run
+  c->kernels += per_it * ((ctl.t + unroll - 1) / unroll) * unroll + (direct ? 1 : 0);
   if (const char* e = std::getenv("DOPF_STREAM_PROF"); e && e[0] == '1' && ctl.t > 0) {
     std::vector<long long> h(static_cast<std::size_t>(c->staged_grid) * 8);
     ck(cudaMemcpy(h.data(), c->bufs.at(126).p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost), "prof");

@@ -29,6 +29,7 @@
 
 #include "div_rho.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace dopf::cuda {
@@ -629,6 +630,14 @@ void stream_launch_decide(const StreamParams& p, const double* ranks, int nranks
   k_decide<<<1, 1, 0, s>>>(p, ranks, nranks);
 }
 
+int stream_graph_unroll() {
+  static const int u = [] {
+    const char* env = std::getenv("DOPF_GRAPH_UNROLL");
+    return env ? std::max(1, std::min(16, std::atoi(env))) : 4;
+  }();
+  return u;
+}
+
 cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaGraphCreate(&g, 0);
@@ -668,13 +677,20 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   kf.blockDim = dim3(kFinalThreads);
   // the direct-load chunks run beside the staged kernel (which leaves one SM
   // for them), not after it
-  cudaGraphNode_t ng, dep[2], nf;
-  int ndep = 0;
-  if ((e = cudaGraphAddKernelNode(&ng, body, nullptr, 0, &kg)) != cudaSuccess) return e;
-  if (p.n_big > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &kb)) != cudaSuccess) return e;
-  if (p.n_staged > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &ks)) != cudaSuccess) return e;
-  if (ndep == 0) dep[ndep++] = ng;
-  if ((e = cudaGraphAddKernelNode(&nf, body, dep, ndep, &kf)) != cudaSuccess) return e;
+  // the body holds `unroll` iterations (the condition is evaluated once per
+  // body; kernels after the stop return at once, so the result is the same)
+  const int unroll = stream_graph_unroll();
+  cudaGraphNode_t prev = nullptr;
+  for (int it = 0; it < unroll; ++it) {
+    cudaGraphNode_t ng, dep[2], nf;
+    int ndep = 0;
+    if ((e = cudaGraphAddKernelNode(&ng, body, prev ? &prev : nullptr, prev ? 1 : 0, &kg)) != cudaSuccess) return e;
+    if (p.n_big > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &kb)) != cudaSuccess) return e;
+    if (p.n_staged > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &ks)) != cudaSuccess) return e;
+    if (ndep == 0) dep[ndep++] = ng;
+    if ((e = cudaGraphAddKernelNode(&nf, body, dep, ndep, &kf)) != cudaSuccess) return e;
+    prev = nf;
+  }
   e = cudaGraphInstantiate(exec, g, 0);
   cudaGraphDestroy(g);
   return e;

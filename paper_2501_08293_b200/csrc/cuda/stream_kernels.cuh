@@ -98,6 +98,8 @@ cudaError_t launch_div_rho_check(const double* a, int64_t n, double rho, double 
 
 /// One-time kernel attributes (dynamic shared memory of the staged kernel).
 cudaError_t stream_prepare();
+/// Iterations per while-node body (kernels after the stop return at once).
+int stream_graph_unroll();
 /// The whole solve as one graph: a while-node over {k_global, k_big, k_staged, k_final}.
 cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec);
 /// One iteration, stream-ordered (no graph).
