@@ -345,7 +345,7 @@ def run_partitioned(args, rank, world, local):
                          "frac": achieved / (peak * world), "traffic": None, "peak_kind": peak_kind,
                          "bytes_per_iteration": bytes_job,
                          "note": "whole job: algorithmic bytes of all ranks / max rank time vs world x HBM peak"},
-            "kernel": {"name": "k_global+k_local+k_pack+k_final+k_decide per iteration", "ranks": world},
+            "kernel": {"name": "k_global+k_staged(+k_local)+k_pack+k_decide per iteration", "ranks": world},
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -541,7 +541,7 @@ def main():
                                   if info["sync"] != "stream-graph" else
                                   "operators are streamed from HBM every iteration")},
             "kernel": {"name": "admm_persistent" if info["sync"] != "stream-graph"
-                       else "k_global+k_staged(+k_local)+k_final (graph while-node)",
+                       else "k_global+k_staged(+k_local), last chunk CTA folds + decides (graph while-node)",
                        "ctas_per_instance": info["blocks"],
                        "instances": info["instances"], "threads": info["threads"],
                        "smem_bytes": info["smem_bytes"], "resident": info["resident"],

@@ -99,7 +99,7 @@ struct dopf_cuda_ctx {
     double *cost = nullptr, *inv = nullptr, *lo = nullptr, *hi = nullptr;
     uint8_t* owner = nullptr;
     double *x = nullptr, *z = nullptr, *lam = nullptr, *u = nullptr, *u_remote = nullptr;
-    double *part = nullptr, *objp = nullptr, *partials = nullptr, *part2 = nullptr;
+    double *part = nullptr, *objp = nullptr, *partials = nullptr;
     unsigned* final_count = nullptr;
     StreamCtl* ctl = nullptr;
     int32_t* export_rows = nullptr;
@@ -619,7 +619,7 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.objp = c->scratch<double>(k++, std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows));
   d.partials = c->scratch<double>(k++, 8);
   d.ctl = c->scratch<StreamCtl>(k++, 1);
-  d.part2 = c->scratch<double>(k++, 128 * 8);
+  k++;  // (slot of the former level-2 partials)
   d.final_count = c->scratch<unsigned>(k++, 1);
   d.export_rows = c->put(k++, L.export_rows);
   d.send = c->scratch<double>(k++, std::max(1, L.max_export));
@@ -679,7 +679,6 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   p.u_remote = d.u_remote;
   p.part = d.part;
   p.objp = d.objp;
-  p.part2 = d.part2;
   p.final_count = d.final_count;
   p.trace = trace;
   p.ctl = d.ctl;
@@ -777,8 +776,8 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   c->last_kernel_s = ms * 1e-3;
   const auto t_dn0 = std::chrono::steady_clock::now();
   const StreamCtl ctl = *ctl_h;
-  // per iteration: k_global, k_final, and the staged and/or direct chunk kernels
-  const long long per_it = 2 + (c->SL.staged_ids.empty() ? 0 : 1) + (c->SL.big_ids.empty() ? 0 : 1);
+  // per iteration: k_global and the staged and/or direct chunk kernels
+  const long long per_it = 1 + (c->SL.staged_ids.empty() ? 0 : 1) + (c->SL.big_ids.empty() ? 0 : 1);
   const char* ng = std::getenv("DOPF_STREAM_NOGRAPH");
   const long long unroll = (ng && ng[0] == '1') ? 1 : stream_graph_unroll();  // whole bodies run
   c->kernels += per_it * ((ctl.t + unroll - 1) / unroll) * unroll + (direct ? 1 : 0);
@@ -1253,7 +1252,7 @@ int dopf_cuda_part_step(dopf_cuda_ctx* c, int32_t phase) {
       c->kernels += 1;
     } else if (phase == 1) {
       stream_launch_local(p, c->stream);
-      c->kernels += 1 + (p.n_staged > 0 ? 1 : 0) + (p.n_big > 0 ? 1 : 0) + (p.max_export > 0 ? 1 : 0);
+      c->kernels += (p.n_staged > 0 ? 1 : 0) + (p.n_big > 0 ? 1 : 0) + (p.max_export > 0 ? 1 : 0);
     } else if (phase == 2) {
       stream_launch_decide(p, c->sd.ranks, c->SL.nparts, c->stream);
       c->kernels += 1;

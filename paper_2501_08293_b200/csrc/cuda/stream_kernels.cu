@@ -18,8 +18,10 @@
 //  k_local    the same chunk iteration for the few chunks whose stage would
 //             not fit shared memory (image read straight from HBM), on SMs
 //             the staged kernel leaves free (parallel graph branch).
-//  k_final    admm.cpp:164-169, 223-234: fixed-order combine of the partials,
-//             trace row, running max, stop test.
+//  (final)    the last chunk CTA of the iteration (k_staged or k_local)
+//             folds the partials in a fixed order and takes the stop test
+//             (admm.cpp:164-169, 223-234): trace row, running max, graph
+//             condition -- no separate kernel.
 //
 // Bitwise parity with the oracle: --fmad=false, the reference's operation
 // forms and summation orders for every iterate, and divisions by rho that are
@@ -269,12 +271,68 @@ __device__ __forceinline__ void write_partials(const StreamParams& p, double (&v
   }
 }
 
+// The CTA that writes the last partial of the iteration folds all of them
+// (fixed order, fixed 256-thread shape whichever kernel it belongs to) and
+// takes the stop decision (admm.cpp:164-169, 223-234) -- no separate kernel.
+constexpr int kFoldThreads = 256;
+__device__ __forceinline__ void fold_barrier() { asm volatile("bar.sync 2, %0;" ::"n"(kFoldThreads) : "memory"); }
+
+__device__ void arrive_and_finish(const StreamParams& p, double* red, bool* last) {
+  const int tid = threadIdx.x;
+  if (tid >= kFoldThreads) return;
+  if (tid == 0) {
+    __threadfence();  // this CTA's partial (written by thread 0) before the count
+    *last = atomicAdd(p.final_count, 1u) == static_cast<unsigned>(p.npart - 1);
+  }
+  fold_barrier();
+  if (!*last) return;
+  __threadfence();
+  double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gap, step, bx2, z2, lam2, maxinf, objective
+  for (int k = tid; k < p.npart; k += kFoldThreads) {
+    const double* q = p.part + static_cast<int64_t>(k) * 8;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) v[i] = v[i] + __ldcg(q + i);
+    v[5] = sel_max(v[5], __ldcg(q + 5));
+    v[6] = v[6] + __ldcg(q + 6);  // interior columns' c'x
+  }
+  for (int k = tid; k < p.col_blocks; k += kFoldThreads) v[6] = v[6] + __ldcg(p.objp + k);  // boundary c'x
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v[q], off);
+      v[q] = q == 5 ? sel_max(v[q], o) : v[q] + o;
+    }
+  constexpr int W = kFoldThreads / 32;
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) red[q * W + warp] = v[q];
+  fold_barrier();
+  if (tid == 0) {
+    double w[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      w[q] = red[q * W];
+      for (int k = 1; k < W; ++k) w[q] = q == 5 ? sel_max(w[q], red[q * W + k]) : w[q] + red[q * W + k];
+    }
+    *p.final_count = 0;  // ready for the next iteration (kernel boundary orders it)
+    if (p.partials_out) {  // partitioned: the host combines ranks, then calls k_decide
+#pragma unroll
+      for (int q = 0; q < 7; ++q) p.partials_out[q] = w[q];
+      return;
+    }
+    finalize_iteration(p, w);
+  }
+}
+
 // Direct-load kernel for chunks whose stage would not fit shared memory:
 // one CTA per chunk, image read straight from HBM.
 __global__ void __launch_bounds__(kStreamRows, 2) k_local(const StreamParams p) {
   __shared__ double tgt[kStreamRows], ush[kStreamRows], xsh[kStreamRows], zsh[kStreamRows];
   __shared__ double red[7 * (kStreamRows / 32)];
   __shared__ ChunkHead hsh;
+  __shared__ bool lastflag;
   if (p.ctl->done) return;
   const StreamChunk ch = p.chunks[p.big_ids[blockIdx.x]];
   const unsigned char* img = p.blob + ch.image_off;
@@ -288,6 +346,8 @@ __global__ void __launch_bounds__(kStreamRows, 2) k_local(const StreamParams p) 
                                zsh, v, sync, ld);
   __syncthreads();
   write_partials<kStreamRows>(p, v, red, p.staged_grid + blockIdx.x, sync);
+  __syncthreads();  // red is reused by the fold
+  arrive_and_finish(p, red, &lastflag);
 }
 
 // ---------------------------------------------------------------- staged kernel
@@ -355,6 +415,7 @@ __global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const Str
   __shared__ double tgt[kStagedRows], ush[kStagedRows], xsh[kStagedRows], zsh[kStagedRows];
   __shared__ double red[7 * (kStagedRows / 32)];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ bool lastflag;
   if (p.ctl->done) return;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -447,61 +508,8 @@ __global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const Str
   if (prof)
     for (int q = 0; q < 6; ++q) p.prof[static_cast<int64_t>(blockIdx.x) * 8 + q] = ph[q];
   write_partials<kStagedRows>(p, v, red, blockIdx.x, sync);
-}
-
-constexpr int kFinalThreads = 256;
-constexpr int kFinalBlocks = 128;  // (a single CTA measured slower even for ~2k partials)
-
-// Two-level fixed-order reduction of the chunk partials and objective
-// partials: CTA g folds a contiguous range into level-2 slot g; the last CTA
-// to finish (device-scope counter) folds the 128 slots in order and decides.
-__global__ void __launch_bounds__(kFinalThreads) k_final(const StreamParams p) {
-  __shared__ double sh[7 * (kFinalThreads / 32)];
-  __shared__ bool last;
-  if (p.ctl->done) return;
-  double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // gap, step, bx2, z2, lam2, maxinf, objective
-  const int g = blockIdx.x;
-  const int G = gridDim.x;
-  const int c0 = static_cast<int>(static_cast<int64_t>(p.npart) * g / G);
-  const int c1 = static_cast<int>(static_cast<int64_t>(p.npart) * (g + 1) / G);
-  for (int k = c0 + threadIdx.x; k < c1; k += kFinalThreads) {
-    const double* q = p.part + static_cast<int64_t>(k) * 8;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) v[i] = v[i] + __ldcg(q + i);
-    v[5] = sel_max(v[5], __ldcg(q + 5));
-    v[6] = v[6] + __ldcg(q + 6);  // interior columns' c'x
-  }
-  const int o0 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * g / G);
-  const int o1 = static_cast<int>(static_cast<int64_t>(p.col_blocks) * (g + 1) / G);
-  for (int k = o0 + threadIdx.x; k < o1; k += kFinalThreads) v[6] = v[6] + __ldcg(p.objp + k);
-  block_reduce<7, kFinalThreads>(v, sh, 5);
-  if (threadIdx.x == 0) {
-    double* slot = p.part2 + g * 8;
-#pragma unroll
-    for (int q = 0; q < 7; ++q) slot[q] = v[q];
-    __threadfence();
-    const unsigned done_blocks = atomicAdd(p.final_count, 1u);
-    last = done_blocks == static_cast<unsigned>(G - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double w[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  if (threadIdx.x < G) {
-    const double* q = p.part2 + threadIdx.x * 8;
-#pragma unroll
-    for (int i = 0; i < 7; ++i) w[i] = __ldcg(q + i);
-  }
-  block_reduce<7, kFinalThreads>(w, sh, 5);
-  if (threadIdx.x == 0) {
-    *p.final_count = 0;  // ready for the next iteration (kernel boundary orders it)
-    if (p.partials_out) {  // partitioned: the host combines ranks, then calls k_decide
-#pragma unroll
-      for (int q = 0; q < 7; ++q) p.partials_out[q] = w[q];
-      return;
-    }
-    finalize_iteration(p, w);
-  }
+  compute_sync();  // red is reused by the fold
+  arrive_and_finish(p, red, &lastflag);
 }
 
 __global__ void k_pack(const StreamParams p) {
@@ -611,17 +619,15 @@ void launch_local_all(const StreamParams& p, cudaStream_t s) {
 
 void stream_launch_iteration(const StreamParams& p, cudaStream_t s) {
   k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
-  launch_local_all(p, s);
-  k_final<<<kFinalBlocks, kFinalThreads, 0, s>>>(p);
+  launch_local_all(p, s);  // the last chunk CTA folds the partials and decides
 }
 
 void stream_launch_global(const StreamParams& p, cudaStream_t s) {
   k_global<<<p.col_blocks, kStreamRows, 0, s>>>(p);
 }
 void stream_launch_local(const StreamParams& p, cudaStream_t s) {
-  launch_local_all(p, s);
+  launch_local_all(p, s);  // the last chunk CTA writes this rank's partials
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
-  k_final<<<kFinalBlocks, kFinalThreads, 0, s>>>(p);
 }
 void stream_launch_pack(const StreamParams& p, cudaStream_t s) {
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
@@ -658,7 +664,7 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   p.use_cond = 1;
   p.partials_out = nullptr;
   void* args[] = {&p};
-  cudaKernelNodeParams kg = {}, kb = {}, ks = {}, kf = {};
+  cudaKernelNodeParams kg = {}, kb = {}, ks = {};
   kg.func = reinterpret_cast<void*>(k_global);
   kg.gridDim = dim3(p.col_blocks);
   kg.blockDim = dim3(kStreamRows);
@@ -671,25 +677,23 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   ks.gridDim = dim3(p.staged_grid);
   ks.blockDim = dim3(kStagedThreads);
   ks.sharedMemBytes = p.stages * p.stage_bytes;
-  kf = kg;
-  kf.func = reinterpret_cast<void*>(k_final);
-  kf.gridDim = dim3(kFinalBlocks);
-  kf.blockDim = dim3(kFinalThreads);
   // the direct-load chunks run beside the staged kernel (which leaves one SM
   // for them), not after it
   // the body holds `unroll` iterations (the condition is evaluated once per
   // body; kernels after the stop return at once, so the result is the same)
   const int unroll = stream_graph_unroll();
-  cudaGraphNode_t prev = nullptr;
+  cudaGraphNode_t prev[2];
+  int nprev = 0;
   for (int it = 0; it < unroll; ++it) {
-    cudaGraphNode_t ng, dep[2], nf;
+    // k_global, then the chunk kernels side by side; the last chunk CTA to
+    // finish folds the partials and decides (no final kernel)
+    cudaGraphNode_t ng, dep[2];
     int ndep = 0;
-    if ((e = cudaGraphAddKernelNode(&ng, body, prev ? &prev : nullptr, prev ? 1 : 0, &kg)) != cudaSuccess) return e;
+    if ((e = cudaGraphAddKernelNode(&ng, body, prev, nprev, &kg)) != cudaSuccess) return e;
     if (p.n_big > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &kb)) != cudaSuccess) return e;
     if (p.n_staged > 0 && (e = cudaGraphAddKernelNode(&dep[ndep++], body, &ng, 1, &ks)) != cudaSuccess) return e;
-    if (ndep == 0) dep[ndep++] = ng;
-    if ((e = cudaGraphAddKernelNode(&nf, body, dep, ndep, &kf)) != cudaSuccess) return e;
-    prev = nf;
+    for (int q = 0; q < ndep; ++q) prev[q] = dep[q];
+    nprev = ndep;
   }
   e = cudaGraphInstantiate(exec, g, 0);
   cudaGraphDestroy(g);

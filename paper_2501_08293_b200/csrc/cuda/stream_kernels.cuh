@@ -45,8 +45,7 @@ struct StreamParams {
   const double* u_remote;  // partitioned: gathered copies of other ranks
   double* part;          // [npart][8]
   double* objp;          // [col_blocks] boundary columns' c'x
-  double* part2;         // [128][8] level-2 partials (k_final)
-  unsigned* final_count; // k_final's last-block counter (zero between iterations)
+  unsigned* final_count; // chunk CTAs done this iteration (the last folds; zero between iterations)
   double* trace;         // [max_iter][6] or null
   StreamCtl* ctl;
   double* partials_out;  // partitioned: this rank's 7 combined partials (null: decide here)
@@ -100,7 +99,7 @@ cudaError_t launch_div_rho_check(const double* a, int64_t n, double rho, double 
 cudaError_t stream_prepare();
 /// Iterations per while-node body (kernels after the stop return at once).
 int stream_graph_unroll();
-/// The whole solve as one graph: a while-node over {k_global, k_big, k_staged, k_final}.
+/// The whole solve as one graph: a while-node over {k_global, k_local | k_staged}.
 cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec);
 /// One iteration, stream-ordered (no graph).
 void stream_launch_iteration(const StreamParams& p, cudaStream_t s);
