@@ -1399,15 +1399,14 @@ int dopf_cuda_div_rho_check(dopf_cuda_ctx* c, const double* a, int64_t n, double
   if (!c || n < 0 || (n > 0 && (!a || !out))) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    double *da = nullptr, *dout = nullptr;
-    ck(cudaMalloc(&da, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
-    ck(cudaMalloc(&dout, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
-    ck(cudaMemcpy(da, a, n * sizeof(double), cudaMemcpyHostToDevice), "h2d");
+    // scratch slots of the context (freed with it), not raw allocations that
+    // would leak when a step throws
+    double* da = c->scratch<double>(124, static_cast<std::size_t>(std::max<int64_t>(n, 1)));
+    double* dout = c->scratch<double>(125, static_cast<std::size_t>(std::max<int64_t>(n, 1)));
+    ck(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
     ck(launch_div_rho_check(da, n, rho, rho_reciprocal(rho), dout, c->stream), "div_rho");
     ck(cudaMemcpyAsync(out, dout, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaStreamSynchronize(c->stream), "div_rho");
-    cudaFree(da);
-    cudaFree(dout);
   });
 }
 
