@@ -166,6 +166,14 @@ int dopf_cuda_part_finish(dopf_cuda_ctx* ctx, dopf_result_view* result, uint8_t*
  * (contiguous, cost-balanced pieces of the depth-first component walk; every
  * rank computes the same), and one rank's layout sizes. */
 int dopf_partition_subsystems(const dopf_model_view* model, int32_t nparts, int32_t* part_of_s);
+/* Streaming layout of a model built on the host (no device): checks its
+ * invariants (every row in exactly one chunk; staged chunks fit their stage;
+ * image heads, row / column records and interior copy lists consistent;
+ * imports are boundary columns) and returns, in out[0..11]: chunks, staged,
+ * direct, boundary columns, import slots, largest staged stage (bytes), stage
+ * limit, image bytes, rows, columns, interior copies, widest chunk (rows).
+ * DOPF_ERR_LOGIC when an invariant fails. */
+int dopf_stream_layout_check(const dopf_model_view* model, int64_t* out12);
 int dopf_layout_probe_part(const dopf_model_view* model, int32_t nparts, int32_t part,
                            const int32_t* part_of_s, dopf_part_info* out);
 

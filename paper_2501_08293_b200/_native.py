@@ -161,6 +161,7 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_layout_probe_batch", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))
     _sig(lib, "dopf_partition_subsystems", C.c_int, P(ModelView_t), i32, P(i32))
     _sig(lib, "dopf_layout_probe_part", C.c_int, P(ModelView_t), i32, i32, P(i32), P(PartInfo_t))
+    _sig(lib, "dopf_stream_layout_check", C.c_int, P(ModelView_t), P(i64))
     _sig(lib, "dopf_cuda_upload_part", C.c_int, vp, P(ModelView_t), i32, i32, P(i32))
     _sig(lib, "dopf_cuda_part_info", C.c_int, vp, P(PartInfo_t))
     _sig(lib, "dopf_cuda_set_stream", C.c_int, vp, vp)

@@ -1532,6 +1532,73 @@ int dopf_partition_subsystems(const dopf_model_view* m, int32_t nparts, int32_t*
   }
 }
 
+int dopf_stream_layout_check(const dopf_model_view* m, int64_t* out) {
+  if (!m || !out) return DOPF_ERR_INVALID_ARGUMENT;
+  try {
+    const StreamLayout L = build_stream_layout(*m);
+    auto fail_if = [](bool bad, const char* what) {
+      if (bad) throw std::logic_error(what);
+    };
+    const unsigned char* blob = reinterpret_cast<const unsigned char*>(L.blob.data());
+    std::vector<int> seen(L.rows, 0);
+    int64_t max_stage = 0, icopies = 0, widest = 0;
+    std::vector<char> staged(L.chunks.size(), 0);
+    for (int32_t q : L.staged_ids) staged[q] = 1;
+    for (std::size_t q = 0; q < L.chunks.size(); ++q) {
+      const StreamChunk& ch = L.chunks[q];
+      widest = std::max<int64_t>(widest, ch.rows);
+      for (int r = 0; r < ch.rows; ++r) ++seen[ch.row0 + r];
+      ChunkHead h;
+      std::memcpy(&h, blob + ch.image_off, sizeof h);
+      fail_if(h.rows != ch.rows || h.arows != ch.arows || h.icols != ch.icols || h.row0 != ch.row0 ||
+                  h.icol0 != ch.icol0 || h.bimp0 != ch.bimp0 || h.nbimp != ch.nbimp ||
+                  h.image_bytes != ch.image_bytes || ch.image_off % 16 || ch.image_bytes % 16,
+              "chunk head");
+      for (int i = 0; i < kImgSections; ++i) fail_if(h.off[i] % 16 || h.off[i] > h.image_bytes, "section offset");
+      StagePlan sp;
+      stage_plan(ch, sp);
+      if (staged[q]) {
+        fail_if(sp.total > static_cast<uint32_t>(L.stage_bytes) || ch.rows > kStagedRows, "stage overflow");
+        max_stage = std::max<int64_t>(max_stage, sp.total);
+      }
+      const StreamRow* rows = reinterpret_cast<const StreamRow*>(blob + ch.image_off + h.off[kImgRows]);
+      const uint32_t* cm = reinterpret_cast<const uint32_t*>(blob + ch.image_off + h.off[kImgCmeta]);
+      const int16_t* cc = reinterpret_cast<const int16_t*>(blob + ch.image_off + h.off[kImgCopies]);
+      std::vector<int> covered(ch.rows, 0);
+      for (int e = 0; e < ch.icols; ++e) {
+        fail_if(L.owner[ch.icol0 + e] != (cmeta_owner(cm[e]) ? 1 : 0), "owner flag");
+        for (int k = 0; k < cmeta_count(cm[e]); ++k) {
+          const int row = cc[cmeta_start(cm[e]) + k];
+          fail_if(row < 0 || row >= ch.rows || rows[row].xloc != e, "interior copy");
+          ++covered[row];
+          ++icopies;
+        }
+      }
+      for (int r = 0; r < ch.rows; ++r) {
+        const StreamRow& rm = rows[r];
+        fail_if((rm.xloc >= 0) == (rm.xin >= 0), "row column kind");
+        if (rm.xloc >= 0) fail_if(covered[r] != 1, "row not covered by its interior column");
+        if (rm.xin >= 0)
+          fail_if(rm.xin >= ch.nbimp || L.bimp[ch.bimp0 + rm.xin] >= L.bcols, "import slot");
+        fail_if(rm.base < 0 || rm.base + rm.n > ch.rows || rm.n < 1, "row subsystem range");
+      }
+    }
+    for (int v : seen) fail_if(v != 1, "row coverage");
+    const int64_t vals[12] = {static_cast<int64_t>(L.chunks.size()), static_cast<int64_t>(L.staged_ids.size()),
+                              static_cast<int64_t>(L.big_ids.size()), L.bcols, static_cast<int64_t>(L.bimp.size()),
+                              max_stage, L.stage_bytes, static_cast<int64_t>(8 * L.blob.size()), L.rows, L.cols,
+                              icopies, widest};
+    for (int i = 0; i < 12; ++i) out[i] = vals[i];
+    return DOPF_OK;
+  } catch (const std::logic_error&) {
+    return DOPF_ERR_LOGIC;
+  } catch (const std::invalid_argument&) {
+    return DOPF_ERR_INVALID_ARGUMENT;
+  } catch (const std::exception&) {
+    return DOPF_ERR_RUNTIME;
+  }
+}
+
 int dopf_layout_probe_part(const dopf_model_view* m, int32_t nparts, int32_t part,
                            const int32_t* part_of_s, dopf_part_info* out) {
   if (!m || !out || !part_of_s) return DOPF_ERR_INVALID_ARGUMENT;

@@ -73,6 +73,32 @@ def test_layout_invariants(shape, seed):
         assert st.remote_copies < 0.2 * st.local_copies   # locality of the DFS partition
 
 
+@pytest.mark.parametrize("shape,seed,stage_kb", [("ieee123", 123, None), ("ieee8500", 8500, None),
+                                                 ("ieee8500", 8500, 8), ("tiled2", 850064, None)])
+def test_stream_layout_invariants(monkeypatch, shape, seed, stage_kb):
+    """The HBM-streaming layout (chunk images, stages, interior/boundary
+    columns, imports), built on the host and checked by the library itself."""
+    if stage_kb:
+        monkeypatch.setenv("DOPF_STAGE_KB", str(stage_kb))
+    f = dopf.tiled_feeder("ieee8500", 2, seed) if shape == "tiled2" else dopf.synthetic_feeder(shape, seed)
+    _, _, m = dopf.load_model(f, workers=4)
+    m.precompute(4)
+    out = np.zeros(12, dtype=np.int64)
+    rc = N.cuda().dopf_stream_layout_check(C.byref(m.view()), out.ctypes.data_as(C.POINTER(C.c_int64)))
+    assert rc == 0
+    (chunks, staged, direct, bcols, imports, max_stage, stage_limit, image_bytes, rows, cols, icopies,
+     widest) = (int(x) for x in out)
+    assert staged + direct == chunks and staged > 0
+    assert max_stage <= stage_limit == (stage_kb or 48) * 1024
+    assert rows == m.total_local_vars and cols == m.global_cols
+    assert icopies <= rows                                       # interior copies are rows of their chunk
+    assert bcols < cols and imports >= 2 * bcols                 # a boundary column spans >= 2 chunks
+    assert widest <= 512
+    if stage_kb is None:
+        assert direct <= 1                                       # only the widest subsystem streams directly
+        assert max_stage >= 0.8 * stage_limit                    # the exact bound fills the stages
+
+
 def test_layout_probe_rejects_bad_arguments():
     _, _, m = dopf.load_model(fixture_path("two_bus"))
     st = N.LayoutStats_t()
