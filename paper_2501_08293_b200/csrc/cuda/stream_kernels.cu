@@ -353,12 +353,13 @@ __global__ void __launch_bounds__(kStreamRows, 2) k_local(const StreamParams p) 
 // ---------------------------------------------------------------- staged kernel
 //
 // Persistent, two CTAs per SM, each 8 compute warps + 1 producer warp. Every
-// chunk the CTA owns (static round robin over staged_ids) is brought into
-// shared memory by ~18 bulk copies (cp.async.bulk, TMA engine) into one of
-// kStages pipeline stages, completing on the stage's "full" mbarrier; the
-// producer warp also gathers the chunk's boundary x values. While the compute
-// warps work on chunk i entirely out of shared memory, the next chunks are in
-// flight. The compute warps release a stage through its "empty" mbarrier.
+// chunk the CTA owns (static round robin over staged_ids) is brought into one
+// of the CTA's pipeline stages in shared memory by four bulk copies
+// (cp.async.bulk, TMA engine): the chunk image, its z and lambda slices and
+// its imported boundary x, completing on the stage's "full" mbarrier (armed
+// with the byte count). While the compute warps work on chunk i entirely out
+// of shared memory, the next chunk is in flight; the compute warps release a
+// stage through its "empty" mbarrier.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
