@@ -591,6 +591,7 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
                    const int32_t* part_of_s = nullptr) {
   c->SL = nparts > 1 ? build_stream_layout_part(m, nparts, part, part_of_s) : build_stream_layout(m);
   const StreamLayout& L = c->SL;
+  if (L.chunks.empty()) throw std::invalid_argument("streaming layout without rows");
   auto& d = c->sd;
   int k = 32;  // slots 32.. (the resident path uses 0..31)
   d.chunks = c->put(k++, L.chunks);
@@ -613,9 +614,13 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   c->staged_ctas = kDefaultStagedCtasPerSm;
   if (const char* e = std::getenv("DOPF_STAGED_CTAS")) c->staged_ctas = std::atoi(e) >= 3 ? 3 : 2;
   const int big_sms = static_cast<int>((L.big_ids.size() + kBigCtasPerSm - 1) / kBigCtasPerSm);
-  c->staged_grid = std::max(1, std::min<int>(c->staged_ctas * std::max(1, c->sm_count - big_sms),
-                                             static_cast<int>(L.staged_ids.size())));
-  d.part = c->scratch<double>(k++, static_cast<std::size_t>(c->staged_grid + L.big_ids.size()) * 8);
+  // (0 when every chunk takes the direct path: the partial slots and the fold
+  // count then cover the direct-load CTAs only)
+  c->staged_grid = L.staged_ids.empty()
+                       ? 0
+                       : std::max(1, std::min<int>(c->staged_ctas * std::max(1, c->sm_count - big_sms),
+                                                   static_cast<int>(L.staged_ids.size())));
+  d.part = c->scratch<double>(k++, std::max<std::size_t>(1, c->staged_grid + L.big_ids.size()) * 8);
   d.objp = c->scratch<double>(k++, std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows));
   d.partials = c->scratch<double>(k++, 8);
   d.ctl = c->scratch<StreamCtl>(k++, 1);

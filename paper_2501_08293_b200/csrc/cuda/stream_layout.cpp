@@ -83,7 +83,7 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
   StreamLayout L;
   // pipeline shape of the staged kernel (DOPF_STAGES / DOPF_STAGE_KB for experiments)
   if (const char* e = std::getenv("DOPF_STAGES")) L.stages = std::max(1, std::min(kMaxStages, std::atoi(e)));
-  if (const char* e = std::getenv("DOPF_STAGE_KB")) L.stage_bytes = std::max(8, std::atoi(e)) * 1024;
+  if (const char* e = std::getenv("DOPF_STAGE_KB")) L.stage_bytes = std::max(1, std::atoi(e)) * 1024;
   if (L.stages * L.stage_bytes > 100 * 1024) throw std::invalid_argument("staged pipeline exceeds 100 KB per CTA");
   L.S = m.S;
   L.n = m.n;

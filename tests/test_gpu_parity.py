@@ -351,7 +351,8 @@ def test_div_rho_is_the_ieee_quotient(solver, rho):
     assert same.all(), (a[~same][:5], out[~same][:5], ref[~same][:5])
 
 
-@pytest.mark.parametrize("stage_kb,ctas,direct", [(8, "2", True), (16, "3", True), (32, "3", False)])
+@pytest.mark.parametrize("stage_kb,ctas,direct", [(1, "2", True), (8, "2", True), (16, "3", True),
+                                                  (32, "3", False)])
 def test_stream_direct_and_staged_chunk_mix_bitwise(monkeypatch, stage_kb, ctas, direct):
     """Small pipeline stages push many chunks onto the direct-load kernel
     (image read from HBM) beside the staged kernel; 3 staged CTAs per SM
@@ -366,7 +367,9 @@ def test_stream_direct_and_staged_chunk_mix_bitwise(monkeypatch, stage_kb, ctas,
     s.set_path("stream")
     s.upload(model)
     info = s.stream_info()
-    assert (info["direct_chunks"] > 0) == direct and info["staged_chunks"] > 0, info
+    assert (info["direct_chunks"] > 0) == direct, info
+    if stage_kb > 1:
+        assert info["staged_chunks"] > 0, info
     assert info["stage_bytes"] == stage_kb * 1024
     settings = dopf.Settings(max_iter=150)
     gpu = s.solve(settings)
