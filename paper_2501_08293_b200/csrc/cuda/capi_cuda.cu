@@ -795,6 +795,13 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
     const double per = static_cast<double>(c->SL.staged_ids.size());  // the last iteration's chunks
     std::fprintf(stderr, "staged phases (cycles per chunk): wait %.0f rows %.0f icol %.0f tgt %.0f gemv %.0f A %.0f\n",
                  sum[0] / per, sum[1] / per, sum[2] / per, sum[3] / per, sum[4] / per, sum[5] / per);
+    std::vector<double> tot(c->staged_grid, 0.0);  // per-CTA busy cycles of the last iteration
+    for (int b = 0; b < c->staged_grid; ++b)
+      for (int q = 0; q < 6; ++q) tot[b] += static_cast<double>(h[b * 8 + q]);
+    std::sort(tot.begin(), tot.end());
+    if (!tot.empty())
+      std::fprintf(stderr, "staged CTA cycles (last iteration): min %.0f median %.0f max %.0f\n", tot.front(),
+                   tot[tot.size() / 2], tot.back());
   }
   r->status = ctl.status;
   r->iterations = ctl.t;
