@@ -412,3 +412,18 @@ def test_pinned_inputs_and_results_bitwise(path):
             assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
         np.testing.assert_allclose(tr[:r.iterations, 1:], ref.trace[:, 1:], rtol=1e-9, atol=1e-13)
     s.unpin(model)
+
+
+def test_stream_path_run_to_run_deterministic(stream_solver):
+    """The streaming path's residual partials are folded in a fixed order
+    (whichever chunk CTA finishes last): two solves give the same trace bits."""
+    f = dopf.synthetic_feeder("ieee8500", 8500)
+    _, _, model = dopf.load_model(f, workers=8)
+    model.precompute(8)
+    stream_solver.upload(model)
+    settings = dopf.Settings(max_iter=300)
+    a = stream_solver.solve(settings)
+    b = stream_solver.solve(settings)
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.trace.view(np.uint64), b.trace.view(np.uint64))
+    assert a.objective == b.objective and a.max_local_infeasibility == b.max_local_infeasibility
