@@ -91,6 +91,12 @@ typedef struct dopf_result_view {
   double time_solve;   /* iteration loop wall time on the device (events) */
   double time_upload;  /* host -> device copies inside dopf_cuda_solve    */
   double time_download;
+  /* stop tests (iterations 1..iterations) within 1e-12 relative of flipping:
+   * the device sums residuals as trees, the reference sequentially, so a
+   * non-zero count marks an iteration count that may depend on summation
+   * order (hard part 2); first_near_tie = 0 if none */
+  int32_t near_ties;
+  int32_t first_near_tie;
 } dopf_result_view;
 
 #ifdef __cplusplus

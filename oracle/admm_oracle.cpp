@@ -26,6 +26,21 @@ namespace {
 
 thread_local std::string g_err;
 
+// Near-tie flag of the stop test (not in the reference; reported so an
+// iteration count that could hinge on summation order is visible): the
+// predicate pres <= eps_prim && dres <= eps_dual (admm.hpp:63) could flip
+// under a 1e-12 relative perturbation of one of the four scalars.
+bool close_rel(double r, double e) {
+  const double scale = std::max(std::abs(r), std::abs(e));
+  return scale > 0.0 && std::abs(r - e) <= 1e-12 * scale;
+}
+
+bool near_tie(double pres, double eps_prim, double dres, double eps_dual) {
+  const bool p_ok = pres <= eps_prim, d_ok = dres <= eps_dual;
+  const bool p_near = close_rel(pres, eps_prim), d_near = close_rel(dres, eps_dual);
+  return (p_near && (d_ok || d_near)) || (d_near && (p_ok || p_near));
+}
+
 }  // namespace
 
 void oracle_set_error(const char* msg) { g_err = msg; }
@@ -51,6 +66,7 @@ extern "C" int oracle_solve(const dopf_model_view* mv, const dopf_settings* st,
     std::vector<double> z(mv->z0, mv->z0 + Nz), z_prev(z), lambda(Nz, 0.0);
     std::vector<double> violation(S, 0.0);
     double max_inf = 0.0;
+    int ties = 0, first_tie = 0;
     int status = DOPF_ITERATION_LIMIT;
     int iters = 0;
     double last_objective = 0.0;
@@ -153,6 +169,10 @@ extern "C" int oracle_solve(const dopf_model_view* mv, const dopf_settings* st,
           std::copy(lambda.begin(), lambda.end(), snap_lambda + static_cast<std::size_t>(next_snap) * Nz);
         ++next_snap;
       }
+      if (near_tie(pres, eps_prim, dres, eps_dual)) {
+        ++ties;
+        if (first_tie == 0) first_tie = iter;
+      }
       if (pres <= eps_prim && dres <= eps_dual) {
         status = DOPF_CONVERGED;
         break;
@@ -165,6 +185,8 @@ extern "C" int oracle_solve(const dopf_model_view* mv, const dopf_settings* st,
     res->iterations = iters;
     res->objective = last_objective;
     res->max_local_infeasibility = max_inf;
+    res->near_ties = ties;
+    res->first_near_tie = first_tie;
     res->time_global = t_global;
     res->time_local = t_local;
     res->time_dual = t_dual;

@@ -79,7 +79,8 @@ def solve(model: "dopf.DecomposedModel", settings: "dopf.Settings", snap_iters=(
     it = r.iterations
     res = dopf.SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
                            trace[:it].copy(), {"solve": r.time_solve, "global": r.time_global,
-                                               "local": r.time_local, "dual": r.time_dual})
+                                               "local": r.time_local, "dual": r.time_dual},
+                           r.near_ties, r.first_near_tie)
     res.snapshots = {int(t): {"x": sx[i], "z": sz[i], "z_prev": szp[i], "lambda": sl[i]}
                      for i, t in enumerate(snaps) if t <= it}
     return res

@@ -38,7 +38,8 @@ class ResultView_t(C.Structure):
                 ("status", i32), ("iterations", i32), ("objective", f64),
                 ("max_local_infeasibility", f64), ("time_precompute", f64),
                 ("time_global", f64), ("time_local", f64), ("time_dual", f64),
-                ("time_solve", f64), ("time_upload", f64), ("time_download", f64)]
+                ("time_solve", f64), ("time_upload", f64), ("time_download", f64),
+                ("near_ties", i32), ("first_near_tie", i32)]
 
 
 class LpView_t(C.Structure):

@@ -63,5 +63,6 @@ class BatchSolver:
             out.append(dopf.SolveResult(x, z, lam, rs[i].status, it, rs[i].objective,
                                         rs[i].max_local_infeasibility,
                                         tr[:it].copy() if tr is not None else np.zeros((0, 6)),
-                                        {"solve": rs[i].time_solve}))
+                                        {"solve": rs[i].time_solve}, rs[i].near_ties,
+                                        rs[i].first_near_tie))
         return out

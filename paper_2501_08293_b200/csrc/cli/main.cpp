@@ -5,6 +5,7 @@
 //
 //   dopf solve    --input f.json [--rho R] [--eps-rel E] [--max-iter N] [--workers W]
 //                 [--trace t.csv] [--solution s.txt] [--report r.json] [--seed S]
+//                 [--device D] [--gpus N]
 //   dopf validate --input f.json [--report r.json] [--workers W]
 //   dopf inspect  --input f.json [--report r.json] [--dump-lp f] [--dump-subsystems f] [--workers W]
 //
@@ -14,7 +15,11 @@
 // two-space indent, doubles in shortest round-trip form.
 // `validate --oracle` (the dense simplex, oracle.cpp:164-273) is test
 // infrastructure in this build (oracle/), not part of the product CLI.
+#include <cerrno>
 #include <charconv>
+#include <cstdlib>
+#include <stdexcept>
+#include <type_traits>
 #include <cmath>
 #include <fstream>
 #include <iostream>
@@ -114,40 +119,80 @@ struct Options {
   int max_iter = 50000;
   int workers = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   unsigned seed = 0;
+  int device = 0;  // CUDA device of the solve (this build's addition)
+  int gpus = 1;    // GPUs of a partitioned solve (this build's addition)
   bool oracle = false;
 };
 
-[[noreturn]] void usage(const std::string& msg) {
-  std::cerr << msg << "\nusage: dopf {solve|validate|inspect} --input FILE [options]\n";
-  std::exit(kExitInternal);
+// Command-line errors exit like the reference's CLI11 front end
+// (CLI11_PARSE -> app.exit(e), tools/main.cpp:297): a message on stderr and
+// CLI11's ExitCodes -- 104 a value that does not convert, 106 a missing
+// required option or subcommand, 109 an unknown argument.
+constexpr int kCliConversion = 104, kCliRequired = 106, kCliExtras = 109;
+
+struct UsageError : std::runtime_error {
+  int code;
+  UsageError(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+template <typename T>
+T convert(const std::string& flag, const std::string& text) {
+  T value{};
+  const char* end = text.data() + text.size();
+  std::from_chars_result r;
+  if constexpr (std::is_floating_point_v<T>) {
+    // strtod accepts what CLI11's lexical_cast accepts (1e-3, inf, ...)
+    char* stop = nullptr;
+    errno = 0;
+    const double d = std::strtod(text.c_str(), &stop);
+    if (text.empty() || stop != text.c_str() + text.size() || errno == ERANGE)
+      throw UsageError(kCliConversion, "Could not convert: " + flag + " = " + text);
+    return static_cast<T>(d);
+  } else {
+    r = std::from_chars(text.data(), end, value);
+    if (r.ec != std::errc() || r.ptr != end)
+      throw UsageError(kCliConversion, "Could not convert: " + flag + " = " + text);
+  }
+  return value;
 }
 
 Options parse_args(int argc, char** argv) {
   Options o;
-  if (argc < 2) usage("a subcommand is required");
+  if (argc < 2) throw UsageError(kCliRequired, "A subcommand is required");
   o.cmd = argv[1];
-  if (o.cmd != "solve" && o.cmd != "validate" && o.cmd != "inspect") usage("unknown subcommand '" + o.cmd + "'");
+  if (o.cmd != "solve" && o.cmd != "validate" && o.cmd != "inspect")
+    throw UsageError(kCliExtras, "The following argument was not expected: " + o.cmd);
   for (int i = 2; i < argc; ++i) {
-    const std::string a = argv[i];
+    std::string a = argv[i];
+    std::string inline_value;
+    bool has_inline = false;
+    if (const auto eq = a.find('='); a.rfind("--", 0) == 0 && eq != std::string::npos) {
+      inline_value = a.substr(eq + 1);  // --opt=value, as CLI11 accepts
+      a = a.substr(0, eq);
+      has_inline = true;
+    }
     auto value = [&]() -> std::string {
-      if (i + 1 >= argc) usage(a + " needs a value");
+      if (has_inline) return inline_value;
+      if (i + 1 >= argc) throw UsageError(kCliRequired, a + " requires 1 argument");
       return argv[++i];
     };
     if (a == "--input") o.input = value();
     else if (a == "--report") o.report_path = value();
-    else if (a == "--workers") o.workers = std::stoi(value());
-    else if (o.cmd == "solve" && a == "--rho") o.rho = std::stod(value());
-    else if (o.cmd == "solve" && a == "--eps-rel") o.eps_rel = std::stod(value());
-    else if (o.cmd == "solve" && a == "--max-iter") o.max_iter = std::stoi(value());
+    else if (a == "--workers") o.workers = convert<int>(a, value());
+    else if (o.cmd == "solve" && a == "--rho") o.rho = convert<double>(a, value());
+    else if (o.cmd == "solve" && a == "--eps-rel") o.eps_rel = convert<double>(a, value());
+    else if (o.cmd == "solve" && a == "--max-iter") o.max_iter = convert<int>(a, value());
     else if (o.cmd == "solve" && a == "--trace") o.trace_path = value();
     else if (o.cmd == "solve" && a == "--solution") o.solution_path = value();
-    else if (o.cmd == "solve" && a == "--seed") o.seed = static_cast<unsigned>(std::stoul(value()));
+    else if (o.cmd == "solve" && a == "--seed") o.seed = convert<unsigned>(a, value());
+    else if (o.cmd == "solve" && a == "--device") o.device = convert<int>(a, value());
+    else if (o.cmd == "solve" && a == "--gpus") o.gpus = convert<int>(a, value());
     else if (o.cmd == "validate" && a == "--oracle") o.oracle = true;
     else if (o.cmd == "inspect" && a == "--dump-lp") o.dump_lp = value();
     else if (o.cmd == "inspect" && a == "--dump-subsystems") o.dump_subs = value();
-    else usage("unknown option '" + a + "'");
+    else throw UsageError(kCliExtras, "The following argument was not expected: " + a);
   }
-  if (o.input.empty()) usage("--input is required");
+  if (o.input.empty()) throw UsageError(kCliRequired, "--input is required");
   return o;
 }
 
@@ -202,7 +247,7 @@ int cmd_solve(const Options& o) {
   settings.workers = o.workers;
   dopf::SolveResult result;
   try {
-    result = dopf::solve(model, settings);  // GPU iteration (cuda_solve.hpp)
+    result = dopf::cuda::solve(model, settings, o.device);  // GPU iteration (cuda_solve.hpp)
   } catch (const dopf::SingularSubsystemError& e) {
     std::cerr << e.what() << "\n";
     return kExitInfeasibleSubsystem;
@@ -345,7 +390,13 @@ int cmd_inspect(const Options& o) {
 }  // namespace
 
 int main(int argc, char** argv) {
-  const Options o = parse_args(argc, argv);
+  Options o;
+  try {
+    o = parse_args(argc, argv);
+  } catch (const UsageError& e) {
+    std::cerr << e.what() << "\nRun with --help for more information.\n";
+    return e.code;
+  }
   try {
     if (o.cmd == "solve") return cmd_solve(o);
     if (o.cmd == "validate") return cmd_validate(o);

@@ -57,6 +57,7 @@
 // in the reference order). Only the residual/objective reductions use a
 // different (tree) order; they feed the stop test and the trace only.
 #include "admm_kernels.cuh"
+#include "stop_test.cuh"
 
 #include "div_rho.cuh"
 
@@ -279,6 +280,8 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
     const bool leader_cta = bd.inst_block == 0;  // writes the trace and the scalar results
     const bool tick = clock_on && lane == 0;
     unsigned long long* counter = ctl;            // slots published, G per iteration
+    int ties = 0, first_tie = 0;                  // lane 0: near-tie stop tests (stop_test.cuh)
+    bool stop_seen = false;
     // (S) combine every block's slot of iteration s in a fixed order (every
     // CTA does this itself, bitwise identically): residuals, stop test,
     // objective -> the block's decision ring; the leader writes the trace row
@@ -319,8 +322,16 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
         const double eps_prim = eps * sel_max(sqrt(tot[2]), sqrt(tot[3]));
         const double eps_dual = eps * sqrt(tot[4]);
         double* rec = dec + (s % kDec) * 4;
-        rec[0] = (pres <= eps_prim && dres <= eps_dual) ? 1.0 : 0.0;
+        const bool stop = pres <= eps_prim && dres <= eps_dual;
+        rec[0] = stop ? 1.0 : 0.0;
         rec[1] = tot[5];
+        if (!stop_seen) {  // iterations 1..stop (combine runs in ascending s)
+          if (stop_near_tie(pres, eps_prim, dres, eps_dual)) {
+            ++ties;
+            if (first_tie == 0) first_tie = s;
+          }
+          stop_seen = stop;
+        }
         if (leader_cta && trace) {
           double* row = trace + static_cast<int64_t>(s - 1) * 6;
           row[0] = s;
@@ -383,6 +394,8 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
         p.iters[bd.instance] = stop_at;
         p.status[bd.instance] = dec[(stop_at % kDec) * 4] != 0.0 ? 0 : 1;
         p.objective[bd.instance] = dec[(stop_at % kDec) * 4 + 1];
+        p.ties[2 * bd.instance] = ties;
+        p.ties[2 * bd.instance + 1] = first_tie;
       }
     }
   } else {

@@ -52,6 +52,7 @@ struct KernelParams {
   int32_t* status;      // [instances] 0 converged, 1 iteration limit
   double* maxinf;       // [instances]
   double* objective;    // [instances]
+  int32_t* ties;        // [instances][2] near-tie stop tests up to the stop, first one (stop_test.cuh)
   double rho;
   double rho_inv;  // RN(1 / rho) for div_rho (div_rho.cuh)
   double eps_rel;

@@ -79,6 +79,7 @@ struct dopf_cuda_ctx {
   unsigned long long* d_ctl = nullptr;
   int32_t *d_iters = nullptr, *d_status = nullptr;
   double *d_maxinf = nullptr, *d_obj = nullptr;
+  int32_t* d_ties = nullptr;  // [instances][2] near-tie count, first near tie
   double* d_trace = nullptr;
   std::size_t trace_cap = 0;  // doubles
   // cached layout plans (structure only), reused while the structure repeats
@@ -208,9 +209,25 @@ int fail(dopf_cuda_ctx* ctx, int code, const std::string& msg) {
   return code;
 }
 
+// Makes the context's device current for one entry point and restores the
+// caller's device afterwards (contexts on several devices may share a thread).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(const dopf_cuda_ctx* c) {
+    if (!c || c->sm_count == 0) return;  // not created yet (dopf_cuda_create sets it)
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != c->device) ck(cudaSetDevice(c->device), "cudaSetDevice");
+    else prev = -1;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <typename F>
 int guarded(dopf_cuda_ctx* ctx, F&& body) {
   try {
+    DeviceScope scope(ctx);
     body();
     return DOPF_OK;
   } catch (const CudaFailure& e) {
@@ -266,6 +283,7 @@ void upload_layout(dopf_cuda_ctx* c) {
   c->d_status = c->scratch<int32_t>(k++, I);
   c->d_maxinf = c->scratch<double>(k++, I);
   c->d_obj = c->scratch<double>(k++, I);
+  c->d_ties = c->scratch<int32_t>(k++, 2 * I);
   ck(cudaStreamSynchronize(c->stream), "upload sync");
 }
 
@@ -324,11 +342,12 @@ void finish_single(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view& r
   const std::size_t R = static_cast<std::size_t>(L.rows_total);
   double* d_res = c->scratch<double>(122, 2 * R + 8);
   ck(launch_final_single(c->d_z, c->d_lam, L.rows_total, c->d_refdev, c->d_iters, kZRing, c->d_status,
-                         c->d_maxinf, c->d_obj, d_res, d_res + R, d_res + 2 * R, c->sm_count, c->stream),
+                         c->d_maxinf, c->d_obj, c->d_ties, d_res, d_res + R, d_res + 2 * R, c->sm_count,
+                         c->stream),
      "final iterate");
   ++c->kernels;
   double* scal = static_cast<double*>(c->small_stage());
-  ck(cudaMemcpyAsync(scal, d_res + 2 * R, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  ck(cudaMemcpyAsync(scal, d_res + 2 * R, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
   if (copy_vectors) {
     const InstDesc& id = L.inst[0];
     if (r.x)
@@ -347,6 +366,8 @@ void finish_single(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view& r
   r.status = static_cast<int32_t>(scal[1]);
   r.max_local_infeasibility = scal[2];
   r.objective = scal[3];
+  r.near_ties = static_cast<int32_t>(scal[4]);
+  r.first_near_tie = static_cast<int32_t>(scal[5]);
   r.time_solve = c->last_kernel_s;
   r.time_global = r.time_local = r.time_dual = 0.0;
   if (r.trace && r.iterations > 0) {
@@ -434,6 +455,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.status = c->d_status;
   p.maxinf = c->d_maxinf;
   p.objective = c->d_obj;
+  p.ties = c->d_ties;
   p.rho = s->rho;
   p.rho_inv = rho_reciprocal(s->rho);
   p.eps_rel = s->eps_rel;
@@ -465,10 +487,12 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
 
   std::vector<int32_t> iters(I), status(I);
   std::vector<double> maxinf(I), obj(I);
+  std::vector<int32_t> ties(2 * I);
   ck(cudaMemcpy(iters.data(), c->d_iters, I * sizeof(int32_t), cudaMemcpyDeviceToHost), "d2h");
   ck(cudaMemcpy(status.data(), c->d_status, I * sizeof(int32_t), cudaMemcpyDeviceToHost), "d2h");
   ck(cudaMemcpy(maxinf.data(), c->d_maxinf, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
   ck(cudaMemcpy(obj.data(), c->d_obj, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+  ck(cudaMemcpy(ties.data(), c->d_ties, 2 * I * sizeof(int32_t), cudaMemcpyDeviceToHost), "d2h");
   bool any_vec = false;
   for (int i = 0; i < count; ++i)
     any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
@@ -514,6 +538,8 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     r.iterations = iters[i];
     r.objective = obj[i];
     r.max_local_infeasibility = maxinf[i];
+    r.near_ties = ties[2 * i];
+    r.first_near_tie = ties[2 * i + 1];
     r.time_solve = c->last_kernel_s;
     r.time_global = r.time_local = r.time_dual = 0.0;
     if (copy_vectors && any_vec) {
@@ -552,6 +578,13 @@ int dopf_cuda_create(int device, dopf_cuda_ctx** out) {
     int count = 0;
     ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
     if (device < 0 || device >= count) throw std::invalid_argument("no such CUDA device");
+    struct Restore {  // the caller's current device is left as it was
+      int prev = -1;
+      ~Restore() {
+        if (prev >= 0) cudaSetDevice(prev);
+      }
+    } restore;
+    if (cudaGetDevice(&restore.prev) != cudaSuccess) restore.prev = -1;
     ck(cudaSetDevice(device), "cudaSetDevice");
     c->device = device;
     ck(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
@@ -717,6 +750,8 @@ void stream_reset(dopf_cuda_ctx* c) {
 void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, bool copy_vectors) {
   check_settings(s);
   if (!c->uploaded) throw std::invalid_argument("no model uploaded");
+  if (c->partitioned)
+    throw std::invalid_argument("partitioned upload: solve through the dopf_cuda_part_* loop or dopf_cuda_solve_part");
   const StreamLayout& L = c->SL;
   auto& d = c->sd;
   const std::size_t need = r->trace ? static_cast<std::size_t>(s->max_iter) * 6 : 0;
@@ -807,6 +842,8 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   r->iterations = ctl.t;
   r->objective = ctl.objective;
   r->max_local_infeasibility = ctl.maxinf;
+  r->near_ties = ctl.ties;
+  r->first_near_tie = ctl.first_tie;
   r->time_solve = c->last_kernel_s;
   r->time_global = r->time_local = r->time_dual = 0.0;
   if (vectors && !direct) {
@@ -957,7 +994,6 @@ void upload_stream_values(dopf_cuda_ctx* c, const dopf_model_view& m) {
 int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
   if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->uploaded = false;
     const LayoutOptions opt = options_for(c);
     if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
@@ -1001,7 +1037,6 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
 int dopf_cuda_upload_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t count) {
   if (!c || !ms || count < 1) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     c->uploaded = false;
     c->dev_plan = nullptr;
     c->stream_maps = false;
@@ -1044,7 +1079,6 @@ int dopf_cuda_precompute(dopf_cuda_ctx* c, const dopf_model_view* m, double* P, 
                          int32_t* first_singular) {
   if (!c || !m || !P || !v) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     const int S = m->S;
     if (first_singular) *first_singular = -1;
     if (S == 0) return;
@@ -1126,7 +1160,6 @@ extern "C" {
 int dopf_cuda_certify(dopf_cuda_ctx* c, const dopf_lp_view* lp, const double* x, dopf_certificate* out) {
   if (!c || !lp || !x || !out) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     Owned o;
     CertifyParams p{};
     p.rows = lp->rows;
@@ -1165,7 +1198,6 @@ int dopf_cuda_reconstruct(dopf_cuda_ctx* c, const dopf_model_view* m, const doub
                           double* out) {
   if (!c || !m || !x || !z || !out || !m->has_pre) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     Owned o;
     ReconstructParams p{};
     p.n = m->n;
@@ -1194,7 +1226,6 @@ int dopf_cuda_upload_part(dopf_cuda_ctx* c, const dopf_model_view* m, int32_t np
                           const int32_t* part_of_s) {
   if (!c || !m || nparts < 1 || part < 0 || part >= nparts || !part_of_s) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
     c->uploaded = false;
     c->dev_plan = nullptr;
@@ -1303,6 +1334,8 @@ int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask
     r->iterations = h.t;
     r->objective = h.objective;
     r->max_local_infeasibility = h.maxinf;
+    r->near_ties = h.ties;
+    r->first_near_tie = h.first_tie;
     r->time_solve = c->last_kernel_s;
     const std::size_t R = static_cast<std::size_t>(L.rows);
     std::vector<double> z(R), lam(R), x(L.cols);
@@ -1338,7 +1371,6 @@ std::vector<std::pair<const double*, int64_t>> value_ranges(const dopf_model_vie
 int dopf_cuda_pin_model(dopf_cuda_ctx* c, const dopf_model_view* m) {
   if (!c || !m || !m->has_pre) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     for (auto [ptr, n] : value_ranges(*m)) {
       if (!ptr || n <= 0 || std::find(c->pinned.begin(), c->pinned.end(), ptr) != c->pinned.end()) continue;
       const cudaError_t e = cudaHostRegister(const_cast<double*>(ptr), static_cast<std::size_t>(n) * sizeof(double),
@@ -1356,7 +1388,6 @@ int dopf_cuda_pin_model(dopf_cuda_ctx* c, const dopf_model_view* m) {
 int dopf_cuda_pin_host(dopf_cuda_ctx* c, const void* ptr, int64_t bytes) {
   if (!c || !ptr || bytes <= 0) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     if (std::find(c->pinned.begin(), c->pinned.end(), ptr) != c->pinned.end()) return;
     const cudaError_t e =
         cudaHostRegister(const_cast<void*>(ptr), static_cast<std::size_t>(bytes), cudaHostRegisterDefault);
@@ -1410,7 +1441,6 @@ int dopf_cuda_stream_info(const dopf_cuda_ctx* c, int64_t* out) {
 int dopf_cuda_div_rho_check(dopf_cuda_ctx* c, const double* a, int64_t n, double rho, double* out) {
   if (!c || n < 0 || (n > 0 && (!a || !out))) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
     // scratch slots of the context (freed with it), not raw allocations that
     // would leak when a step throws
     double* da = c->scratch<double>(124, static_cast<std::size_t>(std::max<int64_t>(n, 1)));
@@ -1449,6 +1479,8 @@ const char* dopf_cuda_last_error(const dopf_cuda_ctx* c) { return c ? c->err.c_s
 
 void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   if (!c) return;
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
   cudaSetDevice(c->device);
   for (const void* ptr : c->pinned) cudaHostUnregister(const_cast<void*>(ptr));
   c->free_model();
@@ -1457,6 +1489,7 @@ void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (prev >= 0 && prev != c->device) cudaSetDevice(prev);
   delete c;
 }
 

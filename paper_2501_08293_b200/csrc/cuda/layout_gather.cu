@@ -50,7 +50,8 @@ __global__ void k_final_iterates(const double* zring, const double* lring, int64
 // order, plus the scalar results packed for one copy
 __global__ void k_final_single(const double* zring, const double* lring, int64_t rows, const int32_t* ref_of_dev,
                                const int32_t* iters, int ring, const int32_t* status, const double* maxinf,
-                               const double* obj, double* zout, double* lout, double* scalars) {
+                               const double* obj, const int32_t* ties, double* zout, double* lout,
+                               double* scalars) {
   const int64_t base = static_cast<int64_t>(iters[0] % ring) * rows;
   for (int64_t d = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; d < rows;
        d += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -63,6 +64,8 @@ __global__ void k_final_single(const double* zring, const double* lring, int64_t
     scalars[1] = status[0];
     scalars[2] = maxinf[0];
     scalars[3] = obj[0];
+    scalars[4] = ties[0];
+    scalars[5] = ties[1];
   }
 }
 
@@ -70,10 +73,10 @@ __global__ void k_final_single(const double* zring, const double* lring, int64_t
 
 cudaError_t launch_final_single(const double* zring, const double* lring, int64_t rows, const int32_t* ref_of_dev,
                                 const int32_t* iters, int ring, const int32_t* status, const double* maxinf,
-                                const double* obj, double* zout, double* lout, double* scalars, int sm_count,
-                                cudaStream_t s) {
-  k_final_single<<<sm_count, 256, 0, s>>>(zring, lring, rows, ref_of_dev, iters, ring, status, maxinf, obj, zout,
-                                          lout, scalars);
+                                const double* obj, const int32_t* ties, double* zout, double* lout,
+                                double* scalars, int sm_count, cudaStream_t s) {
+  k_final_single<<<sm_count, 256, 0, s>>>(zring, lring, rows, ref_of_dev, iters, ring, status, maxinf, obj, ties,
+                                          zout, lout, scalars);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ cudaError_t launch_final_iterates(const double* zring, const double* lring, int6
 /// lambda permuted to reference order, and {iters, status, maxinf, objective}.
 cudaError_t launch_final_single(const double* zring, const double* lring, int64_t rows, const int32_t* ref_of_dev,
                                 const int32_t* iters, int ring, const int32_t* status, const double* maxinf,
-                                const double* obj, double* zout, double* lout, double* scalars, int sm_count,
-                                cudaStream_t s);
+                                const double* obj, const int32_t* ties, double* zout, double* lout,
+                                double* scalars, int sm_count, cudaStream_t s);
 
 }  // namespace dopf::cuda

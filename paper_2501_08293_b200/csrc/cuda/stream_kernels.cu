@@ -28,6 +28,7 @@
 // exactly the IEEE quotient (div_rho.cuh); only the residual/objective
 // reductions are trees (stop test and trace only).
 #include "stream_kernels.cuh"
+#include "stop_test.cuh"
 
 #include "div_rho.cuh"
 
@@ -84,6 +85,10 @@ __device__ __forceinline__ void finalize_iteration(const StreamParams& p, const 
   ctl->t = t;
   ctl->maxinf = sel_max(ctl->maxinf, v[5]);
   ctl->objective = v[6];
+  if (stop_near_tie(pres, eps_prim, dres, eps_dual)) {
+    ++ctl->ties;
+    if (ctl->first_tie == 0) ctl->first_tie = t;
+  }
   if (p.trace) {
     double* row = p.trace + static_cast<int64_t>(t - 1) * 6;
     row[0] = t;
@@ -594,16 +599,15 @@ using LocalKernel = void (*)(const StreamParams);
 
 LocalKernel local_kernel() { return &k_local; }
 
+// kernel attributes are per device: set on every upload (the caller has made
+// the context's device current)
 cudaError_t stream_prepare() {
-  static cudaError_t e = [] {
-    cudaError_t e2 = cudaSuccess;
-    for (auto k : {&k_staged<2, false>, &k_staged<2, true>})
-      if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    for (auto k : {&k_staged<3, false>, &k_staged<3, true>})
-      if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-    return e2;
-  }();
-  return e;
+  cudaError_t e2 = cudaSuccess;
+  for (auto k : {&k_staged<2, false>, &k_staged<2, true>})
+    if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (auto k : {&k_staged<3, false>, &k_staged<3, true>})
+    if (e2 == cudaSuccess) e2 = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  return e2;
 }
 
 using StagedKernel = void (*)(const StreamParams);

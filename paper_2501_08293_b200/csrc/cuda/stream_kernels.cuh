@@ -16,6 +16,8 @@ struct StreamCtl {      // device-side loop state
   int32_t pad;
   double maxinf;        // running max of ||A_s z_s - b_s||_inf
   double objective;     // c'x of the last iteration
+  int32_t ties;         // near-tie stop tests so far (stop_test.cuh)
+  int32_t first_tie;    // first of them (0: none)
 };
 
 constexpr int kStagedThreads = kStagedRows + 32;  // compute warps + 1 producer warp

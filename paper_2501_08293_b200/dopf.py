@@ -495,6 +495,9 @@ class SolveResult:
     max_local_infeasibility: float
     trace: np.ndarray            # (iterations, 6): t, pres, dres, eps_prim, eps_dual, objective
     timings: dict = field(default_factory=dict)
+    # stop tests within 1e-12 relative of flipping (dopf_result_view.near_ties)
+    near_ties: int = 0
+    first_near_tie: int = 0
 
     @property
     def converged(self) -> bool:
@@ -608,7 +611,8 @@ class CudaSolver:
                            trace[:it].copy(),
                            {"solve": r.time_solve, "upload": r.time_upload,
                             "download": r.time_download, "global": r.time_global,
-                            "local": r.time_local, "dual": r.time_dual})
+                            "local": r.time_local, "dual": r.time_dual},
+                           r.near_ties, r.first_near_tie)
 
 
 def solve(model: DecomposedModel, settings: Settings = Settings(), device: int = 0) -> SolveResult:

@@ -85,8 +85,11 @@ class PartitionedSolver:
         torch = self.torch
         dev = f"cuda:{self.device}"
         key = (info.send, info.recv, info.partials, info.ranks, info.max_export)
+        # a captured graph bakes in the layout's kernel parameters (chunk
+        # counts, boundary columns, export count): any upload invalidates it
+        self._graph_key = None
         if getattr(self, "_buf_key", None) == key:
-            self.info = info  # same-structure re-upload: buffers, stream and captured graph stay valid
+            self.info = info  # same buffers: the tensor views and the stream stay valid
             return
         self.info = info
         self._buf_key = key
@@ -190,7 +193,8 @@ class PartitionedSolver:
                                                   zm.ctypes.data_as(C.POINTER(C.c_uint8))))
         it = r.iterations
         res = dopf.SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
-                               tr[:it].copy() if trace else np.zeros((0, 6)), {"solve": r.time_solve})
+                               tr[:it].copy() if trace else np.zeros((0, 6)), {"solve": r.time_solve},
+                               r.near_ties, r.first_near_tie)
         res.x_mask, res.z_mask = xm.astype(bool), zm.astype(bool)
         return res
 
@@ -207,4 +211,5 @@ class PartitionedSolver:
         if not (np.all(xs == 1) and np.all(zs == 1)):
             raise RuntimeError("partition does not cover every column / copy exactly once")
         return dopf.SolveResult(x, z, lam, res.status, res.iterations, res.objective,
-                                res.max_local_infeasibility, res.trace, res.timings)
+                                res.max_local_infeasibility, res.trace, res.timings, res.near_ties,
+                                res.first_near_tie)

@@ -78,6 +78,16 @@ def test_solve_converges_with_report():
     assert rep["model"] == {"cols": 12, "rows": 11, "subsystems": 2}
     assert rep["settings"]["rho"] == 100.0 and len(rep["solution"]) == 12
     assert rep["max_local_infeasibility"] <= 1e-8
+    # the report prints shortest round-trip doubles: the parsed value is the
+    # solver's exact double, and it equals the restated reference loop's
+    from oracle import oracle_py as O
+    from paper_2501_08293_b200 import dopf
+    _, _, model = dopf.load_model(fixture_path("two_bus"))
+    model.precompute()
+    ref = O.solve(model, dopf.Settings(eps_rel=1e-4))
+    assert rep["max_local_infeasibility"] == ref.max_local_infeasibility
+    assert rep["iterations"] == ref.iterations
+    assert abs(rep["objective"] - ref.objective) <= 1e-12 * abs(ref.objective)  # tree vs sequential c'x
 
 
 @pytest.mark.gpu
@@ -98,3 +108,25 @@ def test_solution_dump_keyed_by_variable(tmp_path):
     assert code == 0
     lines = [l for l in sol.read_text().splitlines() if l]
     assert len(lines) == 12 and any(l.startswith("p_gen:g1:1 ") for l in lines)
+
+
+@pytest.mark.parametrize("args,code,needle", [
+    (["solve", "--input", "f.json", "--rho", "abc"], 104, "--rho"),        # CLI11 ConversionError
+    (["solve", "--input", "f.json", "--max-iter", "1.5"], 104, "--max-iter"),
+    (["solve", "--rho", "1"], 106, "--input"),                             # RequiredError
+    (["solve", "--input"], 106, "--input"),
+    (["bogus"], 109, "bogus"),                                             # ExtrasError
+    (["inspect", "--input", "f.json", "--rho", "1"], 109, "--rho"),
+    ([], 106, "subcommand"),
+])
+def test_command_line_errors_exit_like_cli11(args, code, needle):
+    """Malformed command lines report and exit with CLI11's codes (the
+    reference parses with CLI11_PARSE, tools/main.cpp:297) -- no abort."""
+    got, out = run(*args)
+    assert got == code and needle in out, (got, out)
+
+
+def test_option_equals_value_form_is_accepted(tmp_path):
+    rep = tmp_path / "r.json"
+    code, _ = run("inspect", f"--input={fixture_path('two_bus')}", f"--report={rep}")
+    assert code == 0 and json.loads(rep.read_text())["centralized"] == {"cols": 12, "rows": 11}

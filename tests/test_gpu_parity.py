@@ -34,7 +34,17 @@ def assert_same(gpu, ref, bitwise=False):
     assert abs(gpu.objective - ref.objective) <= OBJ_REL * max(1.0, abs(ref.objective))
     # residual trace: tree vs sequential summation, ulp-level only
     np.testing.assert_allclose(gpu.trace[:, 1:], ref.trace[:, 1:], rtol=1e-9, atol=1e-13)
-    assert gpu.max_local_infeasibility <= max(1e-8, 10 * ref.max_local_infeasibility)
+    # max over iterations of ||A_s z_s - b_s||_inf (admm.cpp:203-205, 219-220):
+    # the same sequential-j row sums on bitwise-equal z, and a max is
+    # order-free -- so the value is bitwise equal, not just small
+    assert_same_maxinf(gpu, ref)
+    # stop tests within 1e-12 of flipping: none on these inputs, on either side
+    assert (gpu.near_ties, gpu.first_near_tie) == (ref.near_ties, ref.first_near_tie)
+
+
+def assert_same_maxinf(gpu, ref):
+    a, b = np.float64(gpu.max_local_infeasibility), np.float64(ref.max_local_infeasibility)
+    assert a.view(np.uint64) == b.view(np.uint64), (float(a), float(b))
 
 
 def model_of_fixture(name):
@@ -370,6 +380,8 @@ def test_stream_direct_and_staged_chunk_mix_bitwise(monkeypatch, stage_kb, ctas,
     assert (info["direct_chunks"] > 0) == direct, info
     if stage_kb > 1:
         assert info["staged_chunks"] > 0, info
+    else:  # every chunk direct: no staged CTAs, partial slots / fold count of the direct kernel only
+        assert info["staged_chunks"] == 0 and info["staged_ctas"] == 0, info
     assert info["stage_bytes"] == stage_kb * 1024
     settings = dopf.Settings(max_iter=150)
     gpu = s.solve(settings)
