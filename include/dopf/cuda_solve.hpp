@@ -55,5 +55,12 @@ class Solver {
 
 SolveResult solve(const DecomposedModel& model, const Settings& settings, int device);
 
+/// One model partitioned over CUDA devices 0..gpus-1 of this process: one
+/// context per device, one NCCL communicator over all of them
+/// (dopf_cuda_comm_init_all), the ranks' device loops on one host thread
+/// each (dopf_cuda_solve_part). Iterates, iteration count and status are
+/// bitwise those of solve(); a missing NCCL throws std::runtime_error.
+SolveResult solve_partitioned(const DecomposedModel& model, const Settings& settings, int gpus);
+
 }  // namespace cuda
 }  // namespace dopf

@@ -132,21 +132,26 @@ int dopf_cuda_div_rho_check(dopf_cuda_ctx* ctx, const double* a, int64_t n, doub
 
 /* ---- Partitioned solve over several ranks (one process per GPU) ----------
  * Subsystem s lives on rank part_of_s[s]. Each rank updates the columns its
- * rows reference; copies held by other ranks arrive through the caller's
- * collective: after step 1 of every iteration, gather every rank's `send`
- * (max_export doubles) into `recv` (nparts * max_export, rank order) and every
- * rank's `partials` (8 doubles) into `ranks` (nparts * 8, rank order), then
- * run step 2 (the identical stop decision on every rank). Before iteration 1,
- * step 3 packs u^0 and the same gather fills `recv`. Loop:
- *   begin; step 3; gather(send); repeat { step 0; step 1; gather(send, partials); step 2 }
- *   until poll says done (kernels after the stop are no-ops, so polling may be lazy); finish.
+ * rows reference; copies held by other ranks arrive through ONE gather per
+ * iteration of every rank's packed record `send` = [u of its exported rows
+ * (max_export doubles, zero padded) | its 8 residual partials] into `recv`
+ * (nparts * xstride doubles, rank order, xstride = max_export + 8); step 2
+ * then combines the ranks' partials in rank order (the identical stop
+ * decision on every rank). Two ways to drive it:
+ *   - dopf_cuda_comm_init + dopf_cuda_solve_part: the library's own NCCL
+ *     communicator, the whole loop (kernels + ncclAllGather) in one CUDA graph
+ *     with a device-side while-node (see below);
+ *   - the caller's collective, step by step:
+ *       begin; step 3; gather(send -> recv);
+ *       repeat { step 0; step 1; gather(send -> recv); step 2 } until poll says done
+ *       (kernels after the stop are no-ops, so polling may be lazy); finish.
  * Iterates are bitwise identical to the single-GPU solve (same summation orders). */
 typedef struct dopf_part_info {
   int32_t nparts, part, rows, cols, n_export, max_export;
-  void* send;      /* device double[max_export]        */
-  void* recv;      /* device double[nparts*max_export] */
-  void* partials;  /* device double[8]                 */
-  void* ranks;     /* device double[nparts*8]          */
+  int32_t xstride;     /* doubles per rank record: max_export + 8 */
+  int32_t reserved;
+  void* send;          /* device double[xstride]          */
+  void* recv;          /* device double[nparts * xstride] */
   double bytes_per_iteration;  /* algorithmic bytes of this rank's share */
 } dopf_part_info;
 int dopf_cuda_upload_part(dopf_cuda_ctx* ctx, const dopf_model_view* model, int32_t nparts,
@@ -161,6 +166,31 @@ int dopf_cuda_part_poll(dopf_cuda_ctx* ctx, int32_t* done, int32_t* iterations);
  * set to 1 there), trace, status, iterations, objective, infeasibility. */
 int dopf_cuda_part_finish(dopf_cuda_ctx* ctx, dopf_result_view* result, uint8_t* x_mask,
                           uint8_t* z_mask);
+
+/* The library's own NCCL path (NCCL bound at run time: an NCCL the process
+ * already holds, else libnccl.so.2 or $DOPF_NCCL_SO; failures are
+ * DOPF_ERR_NCCL). One process per GPU: rank 0 makes the 128-byte id,
+ * the caller broadcasts it out of band, every rank calls comm_init. One
+ * process driving n GPUs (one context each): comm_init_all.
+ * dopf_cuda_solve_part then runs the whole partitioned loop -- reset, u^0
+ * exchange, and the iterations (kernels + one ncclAllGather of the packed
+ * records) as ONE CUDA graph with a device-side while-node; if the
+ * collective cannot be captured into a conditional body on some rank, all
+ * ranks use a graph of 8 iterations relaunched behind a double-buffered,
+ * non-blocking host poll (DOPF_PART_GRAPH=unrolled forces it). Outputs as
+ * dopf_cuda_part_finish. The upload (dopf_cuda_upload_part) must be part
+ * `rank` of `nranks`. Replaces the reference's WorkerPool fork-join
+ * (parallel.cpp:88-120) across GPUs; same iterates as one GPU, bitwise. */
+int dopf_nccl_unique_id(void* out128);
+int dopf_cuda_comm_init(dopf_cuda_ctx* ctx, int32_t nranks, int32_t rank, const void* unique_id);
+int dopf_cuda_comm_init_all(dopf_cuda_ctx** ctxs, int32_t n);
+int dopf_cuda_comm_destroy(dopf_cuda_ctx* ctx);
+int dopf_cuda_solve_part(dopf_cuda_ctx* ctx, const dopf_settings* settings, dopf_result_view* result,
+                         uint8_t* x_mask, uint8_t* z_mask);
+/* 0 no graph yet, 1 device while-node, 2 unrolled graph + lazy poll */
+int dopf_cuda_part_graph_mode(const dopf_cuda_ctx* ctx);
+/* Which NCCL is bound (path and version), or why none is. */
+const char* dopf_nccl_describe(void);
 
 /* Host-only helpers of the partitioned solve: the subsystem -> rank map
  * (contiguous, cost-balanced pieces of the depth-first component walk; every

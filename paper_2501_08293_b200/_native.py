@@ -56,7 +56,7 @@ class LayoutStats_t(C.Structure):
 
 class PartInfo_t(C.Structure):
     _fields_ = [("nparts", i32), ("part", i32), ("rows", i32), ("cols", i32), ("n_export", i32),
-                ("max_export", i32), ("send", vp), ("recv", vp), ("partials", vp), ("ranks", vp),
+                ("max_export", i32), ("xstride", i32), ("reserved", i32), ("send", vp), ("recv", vp),
                 ("bytes_per_iteration", f64)]
 
 
@@ -131,6 +131,7 @@ def cuda() -> C.CDLL:
     path = os.environ.get("DOPF_CUDA_SO", CUDA_SO)  # alternative build, for A/B measurements only
     if not os.path.exists(path):
         raise RuntimeError(f"CUDA solver library missing: {path} (run __graft_entry__.build())")
+    _prefer_python_nccl()
     lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
     _sig(lib, "dopf_cuda_create", C.c_int, C.c_int, P(vp))
     _sig(lib, "dopf_cuda_upload", C.c_int, vp, P(ModelView_t))
@@ -170,8 +171,35 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_part_step", C.c_int, vp, i32)
     _sig(lib, "dopf_cuda_part_poll", C.c_int, vp, P(i32), P(i32))
     _sig(lib, "dopf_cuda_part_finish", C.c_int, vp, P(ResultView_t), P(C.c_uint8), P(C.c_uint8))
+    _sig(lib, "dopf_nccl_unique_id", C.c_int, C.c_char_p)
+    _sig(lib, "dopf_cuda_comm_init", C.c_int, vp, i32, i32, C.c_char_p)
+    _sig(lib, "dopf_cuda_comm_init_all", C.c_int, P(vp), i32)
+    _sig(lib, "dopf_cuda_comm_destroy", C.c_int, vp)
+    _sig(lib, "dopf_cuda_solve_part", C.c_int, vp, P(Settings_t), P(ResultView_t), P(C.c_uint8), P(C.c_uint8))
+    _sig(lib, "dopf_cuda_part_graph_mode", C.c_int, vp)
+    _sig(lib, "dopf_nccl_describe", C.c_char_p)
     _cuda = lib
     return lib
+
+
+def _prefer_python_nccl() -> None:
+    """libdopf_cuda.so binds NCCL at run time (nccl_dyn.cpp): an NCCL already
+    loaded in the process, else $DOPF_NCCL_SO, else libnccl.so.2 from the
+    library path. In Python, PyTorch ships its own (newer) NCCL under the same
+    soname; pointing DOPF_NCCL_SO at it keeps a later `import torch` working
+    when the solver's communicator comes up first."""
+    if os.environ.get("DOPF_NCCL_SO"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for root in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(root, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["DOPF_NCCL_SO"] = cand
+            return
 
 
 def last_error() -> str:

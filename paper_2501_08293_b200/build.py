@@ -104,7 +104,7 @@ def build_cuda(verbose: bool = False) -> str:
     _compile_all(jobs)
     if _newer(CUDA_SO, objs + [HOST_SO]):
         _run([NVCC, "-shared", "-o", CUDA_SO, *objs, "-L", LIB, "-ldopf_host",
-              "-Xlinker", "-rpath,$ORIGIN", "-lcudart"])
+              "-Xlinker", "-rpath,$ORIGIN", "-lcudart", "-ldl"])
     build_dropin_test()
     build_cli()
     return CUDA_SO

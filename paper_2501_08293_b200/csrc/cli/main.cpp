@@ -121,6 +121,7 @@ struct Options {
   unsigned seed = 0;
   int device = 0;  // CUDA device of the solve (this build's addition)
   int gpus = 1;    // GPUs of a partitioned solve (this build's addition)
+  bool gpus_set = false;
   bool oracle = false;
 };
 
@@ -186,7 +187,10 @@ Options parse_args(int argc, char** argv) {
     else if (o.cmd == "solve" && a == "--solution") o.solution_path = value();
     else if (o.cmd == "solve" && a == "--seed") o.seed = convert<unsigned>(a, value());
     else if (o.cmd == "solve" && a == "--device") o.device = convert<int>(a, value());
-    else if (o.cmd == "solve" && a == "--gpus") o.gpus = convert<int>(a, value());
+    else if (o.cmd == "solve" && a == "--gpus") {
+      o.gpus = convert<int>(a, value());
+      o.gpus_set = true;
+    }
     else if (o.cmd == "validate" && a == "--oracle") o.oracle = true;
     else if (o.cmd == "inspect" && a == "--dump-lp") o.dump_lp = value();
     else if (o.cmd == "inspect" && a == "--dump-subsystems") o.dump_subs = value();
@@ -247,7 +251,10 @@ int cmd_solve(const Options& o) {
   settings.workers = o.workers;
   dopf::SolveResult result;
   try {
-    result = dopf::cuda::solve(model, settings, o.device);  // GPU iteration (cuda_solve.hpp)
+    // GPU iteration (cuda_solve.hpp): one device, or the model partitioned
+    // over devices 0..gpus-1 with the NCCL exchange
+    result = o.gpus > 1 || o.gpus_set ? dopf::cuda::solve_partitioned(model, settings, o.gpus)
+                                      : dopf::cuda::solve(model, settings, o.device);
   } catch (const dopf::SingularSubsystemError& e) {
     std::cerr << e.what() << "\n";
     return kExitInfeasibleSubsystem;

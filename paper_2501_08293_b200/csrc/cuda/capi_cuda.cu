@@ -20,6 +20,7 @@
 #include "precompute_kernels.cuh"
 #include "stream_kernels.cuh"
 #include "div_rho.cuh"
+#include "nccl_dyn.hpp"
 
 using namespace dopf::cuda;
 
@@ -100,11 +101,11 @@ struct dopf_cuda_ctx {
     double *cost = nullptr, *inv = nullptr, *lo = nullptr, *hi = nullptr;
     uint8_t* owner = nullptr;
     double *x = nullptr, *z = nullptr, *lam = nullptr, *u = nullptr, *u_remote = nullptr;
-    double *part = nullptr, *objp = nullptr, *partials = nullptr;
+    double *part = nullptr, *objp = nullptr;
     unsigned* final_count = nullptr;
     StreamCtl* ctl = nullptr;
     int32_t* export_rows = nullptr;
-    double *send = nullptr, *ranks = nullptr;
+    double* send = nullptr;
   } sd;
   bool partitioned = false;
   unsigned long long* d_timeline = nullptr;
@@ -136,6 +137,17 @@ struct dopf_cuda_ctx {
   void* h_small = nullptr;
   std::size_t h_stage_cap = 0;
 
+  // NCCL communicator of a partitioned solve (dopf_cuda_comm_init) and the
+  // solve's CUDA graph (kernels + ncclAllGather, dopf_cuda_solve_part)
+  ncclComm_t comm = nullptr;
+  int comm_nranks = 0, comm_rank = -1;
+  int64_t layout_epoch = 0;          // bumped by every structural streaming upload
+  cudaGraphExec_t part_graph = nullptr;
+  int part_graph_mode = 0;           // 1 device while-node, 2 unrolled bodies + lazy host poll
+  double part_key[6] = {0, 0, 0, 0, 0, 0};
+  cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  int32_t* h_flags = nullptr;        // pinned: done flags of the last two unrolled launches
+
   int64_t launches = 0;
   double last_kernel_s = 0;
   bool profiling = false;
@@ -145,6 +157,9 @@ struct dopf_cuda_ctx {
   void drop_graph() {
     if (graph) cudaGraphExecDestroy(graph);
     graph = nullptr;
+    if (part_graph) cudaGraphExecDestroy(part_graph);
+    part_graph = nullptr;
+    part_graph_mode = 0;
   }
 
   void free_model() {
@@ -235,6 +250,8 @@ int guarded(dopf_cuda_ctx* ctx, F&& body) {
                 e.what());
   } catch (const SingularFailure& e) {
     return fail(ctx, DOPF_ERR_SINGULAR, e.what());
+  } catch (const nccl::NcclFailure& e) {
+    return fail(ctx, DOPF_ERR_NCCL, e.what());
   } catch (const std::invalid_argument& e) {
     return fail(ctx, DOPF_ERR_INVALID_ARGUMENT, e.what());
   } catch (const std::bad_alloc&) {
@@ -623,6 +640,7 @@ bool needs_streaming(const dopf_model_view& m, const LayoutOptions& opt) {
 void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, int part = 0,
                    const int32_t* part_of_s = nullptr) {
   c->SL = nparts > 1 ? build_stream_layout_part(m, nparts, part, part_of_s) : build_stream_layout(m);
+  ++c->layout_epoch;  // captured graphs bake in the layout's kernel parameters
   const StreamLayout& L = c->SL;
   if (L.chunks.empty()) throw std::invalid_argument("streaming layout without rows");
   auto& d = c->sd;
@@ -655,13 +673,13 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
                                                    static_cast<int>(L.staged_ids.size())));
   d.part = c->scratch<double>(k++, std::max<std::size_t>(1, c->staged_grid + L.big_ids.size()) * 8);
   d.objp = c->scratch<double>(k++, std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows));
-  d.partials = c->scratch<double>(k++, 8);
+  k++;  // (slot of the former separate partials buffer)
   d.ctl = c->scratch<StreamCtl>(k++, 1);
   k++;  // (slot of the former level-2 partials)
   d.final_count = c->scratch<unsigned>(k++, 1);
   d.export_rows = c->put(k++, L.export_rows);
-  d.send = c->scratch<double>(k++, std::max(1, L.max_export));
-  d.ranks = c->scratch<double>(k++, static_cast<std::size_t>(L.nparts) * 8);
+  d.send = c->scratch<double>(k++, L.xstride());  // [exports | partials] record of this rank
+  k++;  // (slot of the former separate partial gather)
   d.staged_ids = c->put(k++, L.staged_ids);
   d.big_ids = c->put(k++, L.big_ids);
   d.imp_ptr = c->put(k++, L.imp_ptr);
@@ -1258,10 +1276,9 @@ int dopf_cuda_part_info(const dopf_cuda_ctx* c, dopf_part_info* out) {
   out->cols = c->SL.cols;
   out->n_export = static_cast<int32_t>(c->SL.export_rows.size());
   out->max_export = c->SL.max_export;
+  out->xstride = c->SL.xstride();
   out->send = c->sd.send;
   out->recv = c->sd.u_remote;
-  out->partials = c->sd.partials;
-  out->ranks = c->sd.ranks;
   out->bytes_per_iteration = c->SL.bytes_per_iteration;
   return DOPF_OK;
 }
@@ -1279,7 +1296,7 @@ int dopf_cuda_part_begin(dopf_cuda_ctx* c, const dopf_settings* s, int32_t with_
     }
     c->part_trace = with_trace != 0;
     c->part_params = stream_params(c, s, with_trace ? c->d_trace : nullptr);
-    c->part_params.partials_out = c->sd.partials;
+    c->part_params.partials_out = c->sd.send + c->SL.max_export;  // behind the exports
     stream_reset(c);
     // u^0 of the exported rows for the first global update: pack z^0
     ck(cudaEventRecord(c->ev0, c->stream), "event");
@@ -1297,7 +1314,7 @@ int dopf_cuda_part_step(dopf_cuda_ctx* c, int32_t phase) {
       stream_launch_local(p, c->stream);
       c->kernels += (p.n_staged > 0 ? 1 : 0) + (p.n_big > 0 ? 1 : 0) + (p.max_export > 0 ? 1 : 0);
     } else if (phase == 2) {
-      stream_launch_decide(p, c->sd.ranks, c->SL.nparts, c->stream);
+      stream_launch_decide(p, c->sd.u_remote, c->SL.nparts, c->SL.xstride(), c->stream);
       c->kernels += 1;
     } else {
       stream_launch_pack(p, c->stream);  // exports of the current u (u^0 before iteration 1)
@@ -1318,15 +1335,20 @@ int dopf_cuda_part_poll(dopf_cuda_ctx* c, int32_t* done, int32_t* iterations) {
   });
 }
 
-int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask, uint8_t* z_mask) {
-  if (!c || !c->partitioned || !r) return DOPF_ERR_INVALID_ARGUMENT;
-  return guarded(c, [&] {
+}  // extern "C"
+
+namespace {
+
+// results of a partitioned solve (this rank's share): scalars, x at owned
+// columns, z / lambda at this rank's rows, trace; ev0 was recorded before
+// the loop
+void part_results(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask, uint8_t* z_mask) {
+  {
     ck(cudaEventRecord(c->ev1, c->stream), "event");
     ck(cudaEventSynchronize(c->ev1), "solve");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "elapsed");
     c->last_kernel_s = ms * 1e-3;
-    ++c->launches;
     const StreamLayout& L = c->SL;
     StreamCtl h{};
     ck(cudaMemcpy(&h, c->sd.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost), "d2h");
@@ -1357,6 +1379,18 @@ int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask
       ck(cudaMemcpy(r->trace, c->d_trace, static_cast<std::size_t>(h.t) * 6 * sizeof(double),
                     cudaMemcpyDeviceToHost),
          "trace d2h");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dopf_cuda_part_finish(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask, uint8_t* z_mask) {
+  if (!c || !c->partitioned || !r) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    ++c->launches;
+    part_results(c, r, x_mask, z_mask);
   });
 }
 
@@ -1488,6 +1522,15 @@ void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->poll_ev[0]) cudaEventDestroy(c->poll_ev[0]);
+  if (c->poll_ev[1]) cudaEventDestroy(c->poll_ev[1]);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
+  if (c->comm) {
+    try {
+      nccl::api().CommDestroy(c->comm);
+    } catch (...) {
+    }
+  }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (prev >= 0 && prev != c->device) cudaSetDevice(prev);
   delete c;
@@ -1656,6 +1699,7 @@ int dopf_layout_probe_part(const dopf_model_view* m, int32_t nparts, int32_t par
     out->cols = L.cols;
     out->n_export = static_cast<int32_t>(L.export_rows.size());
     out->max_export = L.max_export;
+    out->xstride = L.xstride();
     out->bytes_per_iteration = L.bytes_per_iteration;
     return DOPF_OK;
   } catch (const std::invalid_argument&) {
@@ -1709,6 +1753,269 @@ int dopf_cuda_phase_cycles(const dopf_cuda_ctx* c, int64_t* out, int32_t max_blo
                   cudaMemcpyDeviceToHost),
        "d2h");
   });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Partitioned solve on the library's own NCCL communicator
+// (dopf_cuda_comm_init / dopf_cuda_solve_part). One iteration is
+//   k_global -> chunk kernels (their last CTA writes this rank's partials
+//   behind the exports) -> k_pack -> ncclAllGather(record) -> k_decide
+// and the whole loop is one CUDA graph: a conditional while-node whose body
+// is that iteration (k_decide clears the condition at the stop), or -- when
+// the collective cannot be captured into a conditional body -- a graph of
+// kUnroll iterations relaunched with a lazy, double-buffered host poll
+// (kernels after the stop return at once, so the GPU is never starved and
+// the result is the same). Every rank takes the same form (agreed by an
+// all-reduce), so the collectives always match.
+
+namespace {
+
+constexpr int kPartUnroll = 8;
+
+void require_comm(const dopf_cuda_ctx* c) {
+  if (!c->partitioned || !c->uploaded) throw std::invalid_argument("no partitioned model uploaded");
+  if (!c->comm) throw std::invalid_argument("no communicator: call dopf_cuda_comm_init first");
+  if (c->SL.nparts != c->comm_nranks || c->SL.part != c->comm_rank)
+    throw std::invalid_argument("the uploaded partition (" + std::to_string(c->SL.part) + " of " +
+                                std::to_string(c->SL.nparts) + ") does not match the communicator (rank " +
+                                std::to_string(c->comm_rank) + " of " + std::to_string(c->comm_nranks) + ")");
+}
+
+void enqueue_allgather(dopf_cuda_ctx* c) {
+  const auto& a = nccl::api();
+  nccl::check(a.AllGather(c->sd.send, c->sd.u_remote, static_cast<std::size_t>(c->SL.xstride()), ncclDouble, c->comm,
+                          c->stream),
+              "ncclAllGather");
+}
+
+// one iteration on c->stream (eager or under capture)
+void enqueue_part_iteration(dopf_cuda_ctx* c, const StreamParams& p) {
+  stream_launch_global(p, c->stream);
+  stream_launch_local(p, c->stream);  // chunk kernels + k_pack: this rank's record
+  enqueue_allgather(c);
+  stream_launch_decide(p, c->sd.u_remote, c->SL.nparts, c->SL.xstride(), c->stream);
+}
+
+// conditional while-node graph; false (stream left out of capture) if the
+// runtime or the collective refuses the capture
+bool build_part_graph_cond(dopf_cuda_ctx* c, StreamParams p, cudaGraphExec_t* exec) {
+  cudaGraph_t g = nullptr;
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return false;
+  cudaGraphConditionalHandle h;
+  cudaGraphNodeParams cp = {};
+  cudaGraphNode_t node;
+  bool ok = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+  if (ok) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    ok = cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+  }
+  if (ok) {
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    p.cond = h;
+    p.use_cond = 1;
+    ok = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) ==
+         cudaSuccess;
+    if (ok) {
+      bool enq = true;
+      try {
+        enqueue_part_iteration(c, p);
+      } catch (const std::exception&) {
+        enq = false;
+      }
+      cudaGraph_t out = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(c->stream, &out);
+      ok = enq && e == cudaSuccess && cudaGetLastError() == cudaSuccess;
+    }
+  }
+  if (ok) ok = cudaGraphInstantiate(exec, g, 0) == cudaSuccess;
+  cudaGraphDestroy(g);
+  cudaGetLastError();  // a refused capture leaves no sticky error behind
+  return ok;
+}
+
+void build_part_graph_unrolled(dopf_cuda_ctx* c, StreamParams p, cudaGraphExec_t* exec) {
+  p.use_cond = 0;
+  ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed), "capture");
+  try {
+    for (int i = 0; i < kPartUnroll; ++i) enqueue_part_iteration(c, p);
+  } catch (...) {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t g = nullptr;
+  ck(cudaStreamEndCapture(c->stream, &g), "capture");
+  const cudaError_t e = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  ck(e, "graph instantiate");
+}
+
+// the form every rank can run: min over ranks of this rank's capability
+int agree_mode(dopf_cuda_ctx* c, int mine) {
+  int32_t* d = c->scratch<int32_t>(119, 2);
+  ck(cudaMemcpyAsync(d, &mine, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream), "h2d");
+  nccl::check(nccl::api().AllReduce(d, d + 1, 1, ncclInt32, ncclMax, c->comm, c->stream), "ncclAllReduce");
+  int32_t all = 0;
+  ck(cudaMemcpyAsync(&all, d + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  ck(cudaStreamSynchronize(c->stream), "agree");
+  return all;  // modes: 1 conditional, 2 unrolled -- the max is the common one
+}
+
+void prepare_part_graph(dopf_cuda_ctx* c, const StreamParams& p, const dopf_settings* s, const double* trace) {
+  const double key[6] = {s->rho, s->eps_rel, static_cast<double>(s->max_iter),
+                         static_cast<double>(reinterpret_cast<uintptr_t>(trace)),
+                         static_cast<double>(c->layout_epoch), static_cast<double>(c->comm_nranks)};
+  if (c->part_graph && std::equal(key, key + 6, c->part_key)) return;
+  if (c->part_graph) cudaGraphExecDestroy(c->part_graph);
+  c->part_graph = nullptr;
+  int want = 1;  // DOPF_PART_GRAPH=unrolled forces the unrolled form
+  if (const char* e = std::getenv("DOPF_PART_GRAPH"); e && std::string(e) == "unrolled") want = 2;
+  cudaGraphExec_t exec = nullptr;
+  int mine = 2;
+  if (want == 1 && build_part_graph_cond(c, p, &exec)) mine = 1;
+  const int mode = agree_mode(c, mine);
+  if (mode != mine && exec) {
+    cudaGraphExecDestroy(exec);
+    exec = nullptr;
+  }
+  if (mode == 2) build_part_graph_unrolled(c, p, &exec);
+  c->part_graph = exec;
+  c->part_graph_mode = mode;
+  std::copy(key, key + 6, c->part_key);
+}
+
+void run_part_graph(dopf_cuda_ctx* c, int max_iter) {
+  const int per_it = 4 + (c->SL.staged_ids.empty() ? 0 : 1) + (c->SL.big_ids.empty() ? 0 : 1) - 1;
+  if (c->part_graph_mode == 1) {
+    ck(cudaGraphLaunch(c->part_graph, c->stream), "graph launch");
+    ++c->launches;
+    c->kernels += per_it;  // (per iteration; the count of iterations is known after the stop)
+    return;
+  }
+  if (!c->poll_ev[0]) {
+    ck(cudaEventCreateWithFlags(&c->poll_ev[0], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&c->poll_ev[1], cudaEventDisableTiming), "event");
+  }
+  if (!c->h_flags) ck(cudaMallocHost(&c->h_flags, 2 * sizeof(int32_t)), "cudaMallocHost");
+  const int64_t need = (static_cast<int64_t>(max_iter) + kPartUnroll - 1) / kPartUnroll;  // launches covering max_iter
+  int64_t issued = 0;
+  auto issue = [&] {
+    const int b = static_cast<int>(issued & 1);
+    ck(cudaGraphLaunch(c->part_graph, c->stream), "graph launch");
+    ck(cudaMemcpyAsync(&c->h_flags[b], &c->sd.ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream),
+       "poll");
+    ck(cudaEventRecord(c->poll_ev[b], c->stream), "event");
+    ++issued;
+    ++c->launches;
+    c->kernels += static_cast<int64_t>(per_it) * kPartUnroll;
+  };
+  issue();
+  for (int64_t k = 0;; ++k) {
+    if (issued < need) issue();  // one launch stays queued behind the one being checked
+    ck(cudaEventSynchronize(c->poll_ev[k & 1]), "poll");
+    if (c->h_flags[k & 1]) break;
+    if (k + 1 >= need) throw std::logic_error("partitioned loop ended without a stop decision");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int dopf_nccl_unique_id(void* out) {
+  if (!out) return DOPF_ERR_INVALID_ARGUMENT;
+  try {
+    ncclUniqueId id;
+    nccl::check(nccl::api().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+    return DOPF_OK;
+  } catch (const std::exception&) {
+    return DOPF_ERR_NCCL;
+  }
+}
+
+int dopf_cuda_comm_init(dopf_cuda_ctx* c, int32_t nranks, int32_t rank, const void* unique_id) {
+  if (!c || nranks < 1 || rank < 0 || rank >= nranks || !unique_id) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (c->comm) throw std::invalid_argument("communicator already initialised");
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    nccl::check(nccl::api().CommInitRank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+    c->comm_nranks = nranks;
+    c->comm_rank = rank;
+  });
+}
+
+int dopf_cuda_comm_init_all(dopf_cuda_ctx** ctxs, int32_t n) {
+  if (!ctxs || n < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < n; ++i)
+    if (!ctxs[i] || ctxs[i]->comm) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(ctxs[0], [&] {
+    std::vector<int> devs(n);
+    std::vector<ncclComm_t> comms(n);
+    for (int i = 0; i < n; ++i) devs[i] = ctxs[i]->device;
+    nccl::check(nccl::api().CommInitAll(comms.data(), n, devs.data()), "ncclCommInitAll");
+    for (int i = 0; i < n; ++i) {
+      ctxs[i]->comm = comms[i];
+      ctxs[i]->comm_nranks = n;
+      ctxs[i]->comm_rank = i;
+    }
+  });
+}
+
+int dopf_cuda_comm_destroy(dopf_cuda_ctx* c) {
+  if (!c) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (!c->comm) return;
+    if (c->part_graph) cudaGraphExecDestroy(c->part_graph);
+    c->part_graph = nullptr;
+    nccl::check(nccl::api().CommDestroy(c->comm), "ncclCommDestroy");
+    c->comm = nullptr;
+    c->comm_nranks = 0;
+    c->comm_rank = -1;
+  });
+}
+
+int dopf_cuda_solve_part(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, uint8_t* x_mask,
+                         uint8_t* z_mask) {
+  if (!c || !r) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    check_settings(s);
+    require_comm(c);
+    const std::size_t need = r->trace ? static_cast<std::size_t>(s->max_iter) * 6 : 0;
+    if (need > c->trace_cap) {
+      if (c->d_trace) cudaFree(c->d_trace);
+      c->d_trace = nullptr;
+      ck(cudaMalloc(&c->d_trace, need * sizeof(double)), "trace alloc");
+      c->trace_cap = need;
+    }
+    double* trace = r->trace ? c->d_trace : nullptr;
+    c->part_trace = r->trace != nullptr;
+    StreamParams p = stream_params(c, s, trace);
+    p.partials_out = c->sd.send + c->SL.max_export;  // the record: [exports | partials]
+    prepare_part_graph(c, p, s, trace);
+    // iteration 0: state reset, u^0 exports gathered
+    stream_reset(c);
+    stream_launch_pack(p, c->stream);
+    enqueue_allgather(c);
+    ck(cudaEventRecord(c->ev0, c->stream), "event");
+    run_part_graph(c, s->max_iter);
+    part_results(c, r, x_mask, z_mask);
+  });
+}
+
+int dopf_cuda_part_graph_mode(const dopf_cuda_ctx* c) { return c ? c->part_graph_mode : 0; }
+
+const char* dopf_nccl_describe(void) {
+  static thread_local std::string s;
+  s = nccl::describe();
+  return s.c_str();
 }
 
 }  // extern "C"

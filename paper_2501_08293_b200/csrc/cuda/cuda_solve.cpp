@@ -4,6 +4,7 @@
 #include <chrono>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "../../../include/dopf_cuda.h"
 #include "../host/flat_model.hpp"
@@ -151,6 +152,99 @@ SolveResult solve(const DecomposedModel& model, const Settings& settings, int de
   Solver solver(device);
   solver.upload(model, settings.workers);
   return solver.solve(settings);
+}
+
+SolveResult solve_partitioned(const DecomposedModel& model, const Settings& settings, int gpus) {
+  check_settings(settings);
+  if (gpus < 1) throw std::invalid_argument("gpus must be positive");
+  const auto t0 = std::chrono::steady_clock::now();
+  WorkerPool pool(std::max(1, settings.workers));
+  const Precomputed pre = precompute(model, &pool);  // host restatement (admm.cpp:31-88)
+  const double precompute_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  FlatModel flat;
+  flat.build(model, &pre);
+  const dopf_model_view view = flat.view(model, &pre);
+  std::vector<int32_t> part_of_s(std::max(1, view.S));
+  if (int rc = dopf_partition_subsystems(&view, gpus, part_of_s.data()); rc != DOPF_OK)
+    raise(rc, "partition failed");
+
+  struct Rank {
+    dopf_cuda_ctx* ctx = nullptr;
+    std::vector<double> x, z, lambda, trace;
+    std::vector<uint8_t> xm, zm;
+    dopf_result_view v{};
+    int rc = DOPF_OK;
+    std::string err;
+  };
+  std::vector<Rank> ranks(gpus);
+  struct Cleanup {
+    std::vector<Rank>& r;
+    ~Cleanup() {
+      for (Rank& k : r)
+        if (k.ctx) dopf_cuda_destroy(k.ctx);
+    }
+  } cleanup{ranks};
+  const int n = model.global_cols, Nz = model.total_local_vars();
+  for (int k = 0; k < gpus; ++k) {
+    Rank& rk = ranks[k];
+    if (int rc = dopf_cuda_create(k, &rk.ctx); rc != DOPF_OK)
+      raise(rc, "dopf_cuda_create failed (no usable CUDA device " + std::to_string(k) + ")");
+    if (int rc = dopf_cuda_upload_part(rk.ctx, &view, gpus, k, part_of_s.data()); rc != DOPF_OK)
+      raise(rc, dopf_cuda_last_error(rk.ctx));
+    rk.x.assign(n, 0.0);
+    rk.z.assign(Nz, 0.0);
+    rk.lambda.assign(Nz, 0.0);
+    rk.trace.assign(static_cast<std::size_t>(settings.max_iter) * DOPF_TRACE_WIDTH, 0.0);
+    rk.xm.assign(n, 0);
+    rk.zm.assign(Nz, 0);
+    rk.v.x = rk.x.data();
+    rk.v.z = rk.z.data();
+    rk.v.lambda = rk.lambda.data();
+    rk.v.trace = rk.trace.data();
+  }
+  std::vector<dopf_cuda_ctx*> ctxs;
+  for (Rank& rk : ranks) ctxs.push_back(rk.ctx);
+  if (int rc = dopf_cuda_comm_init_all(ctxs.data(), gpus); rc != DOPF_OK) raise(rc, dopf_cuda_last_error(ctxs[0]));
+  const dopf_settings cs = to_c(settings);
+  std::vector<std::thread> threads;
+  for (Rank& rk : ranks)
+    threads.emplace_back([&rk, &cs] {
+      rk.rc = dopf_cuda_solve_part(rk.ctx, &cs, &rk.v, rk.xm.data(), rk.zm.data());
+      if (rk.rc != DOPF_OK) rk.err = dopf_cuda_last_error(rk.ctx);
+    });
+  for (std::thread& t : threads) t.join();
+  for (const Rank& rk : ranks)
+    if (rk.rc != DOPF_OK) raise(rk.rc, rk.err);
+
+  // each column from the rank that owns it, each copy from the rank holding it
+  SolveResult r;
+  r.x.assign(n, 0.0);
+  r.z.assign(Nz, 0.0);
+  r.lambda.assign(Nz, 0.0);
+  for (const Rank& rk : ranks) {
+    for (int i = 0; i < n; ++i)
+      if (rk.xm[i]) r.x[i] = rk.x[i];
+    for (int q = 0; q < Nz; ++q)
+      if (rk.zm[q]) {
+        r.z[q] = rk.z[q];
+        r.lambda[q] = rk.lambda[q];
+      }
+  }
+  const dopf_result_view& v = ranks[0].v;  // scalars and trace agree on every rank
+  r.status = v.status == DOPF_CONVERGED ? SolveStatus::converged : SolveStatus::iteration_limit;
+  r.iterations = v.iterations;
+  r.objective = v.objective;
+  r.max_local_infeasibility = v.max_local_infeasibility;
+  r.trace.resize(v.iterations);
+  for (int t = 0; t < v.iterations; ++t) {
+    const double* row = ranks[0].trace.data() + static_cast<std::size_t>(t) * DOPF_TRACE_WIDTH;
+    r.trace[t] = TraceRow{static_cast<int>(row[0]), row[1], row[2], row[3], row[4], row[5]};
+  }
+  r.timings.precompute = precompute_s;
+  r.timings.global = v.time_global;
+  r.timings.local = v.time_local;
+  r.timings.dual = v.time_dual;
+  return r;
 }
 
 }  // namespace dopf::cuda

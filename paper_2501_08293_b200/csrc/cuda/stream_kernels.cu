@@ -519,20 +519,24 @@ __global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const Str
 }
 
 __global__ void k_pack(const StreamParams p) {
-  // this rank's exported u values -> its send slots (zero padded)
+  // this rank's exported u values -> the head of its send record (zero
+  // padded); the chunk kernels' last CTA already wrote the partials behind them
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < p.max_export) p.send[e] = e < p.n_export ? p.u[p.export_rows[e]] : 0.0;
 }
 
-__global__ void k_decide(const StreamParams p, const double* ranks, int nranks) {
+__global__ void k_decide(const StreamParams p, const double* recv, int nranks, int stride) {
   if (p.ctl->done) return;
-  // rank partials combined in rank order: identical decision on every rank
+  // every rank's partials (at r * stride + max_export of the gathered
+  // records) combined in rank order: identical decision on every rank
+  const double* ranks = recv + p.max_export;
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   for (int r = 0; r < nranks; ++r) {
+    const double* rp = ranks + static_cast<int64_t>(r) * stride;
 #pragma unroll
-    for (int q = 0; q < 5; ++q) v[q] = v[q] + ranks[r * 8 + q];
-    v[5] = sel_max(v[5], ranks[r * 8 + 5]);
-    v[6] = v[6] + ranks[r * 8 + 6];
+    for (int q = 0; q < 5; ++q) v[q] = v[q] + rp[q];
+    v[5] = sel_max(v[5], rp[5]);
+    v[6] = v[6] + rp[6];
   }
   finalize_iteration(p, v);
 }
@@ -637,8 +641,8 @@ void stream_launch_local(const StreamParams& p, cudaStream_t s) {
 void stream_launch_pack(const StreamParams& p, cudaStream_t s) {
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
 }
-void stream_launch_decide(const StreamParams& p, const double* ranks, int nranks, cudaStream_t s) {
-  k_decide<<<1, 1, 0, s>>>(p, ranks, nranks);
+void stream_launch_decide(const StreamParams& p, const double* recv, int nranks, int stride, cudaStream_t s) {
+  k_decide<<<1, 1, 0, s>>>(p, recv, nranks, stride);
 }
 
 int stream_graph_unroll() {

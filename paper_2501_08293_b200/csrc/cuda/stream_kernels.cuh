@@ -110,6 +110,6 @@ void stream_launch_iteration(const StreamParams& p, cudaStream_t s);
 void stream_launch_global(const StreamParams& p, cudaStream_t s);
 void stream_launch_local(const StreamParams& p, cudaStream_t s);
 void stream_launch_pack(const StreamParams& p, cudaStream_t s);
-void stream_launch_decide(const StreamParams& p, const double* ranks, int nranks, cudaStream_t s);
+void stream_launch_decide(const StreamParams& p, const double* recv, int nranks, int stride, cudaStream_t s);
 
 }  // namespace dopf::cuda

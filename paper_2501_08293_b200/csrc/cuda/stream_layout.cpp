@@ -239,10 +239,10 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     for (const auto& e : exports) L.max_export = std::max<int32_t>(L.max_export, static_cast<int32_t>(e.size()));
     for (int q = 0; q < nparts; ++q)
       for (std::size_t e = 0; e < exports[q].size(); ++e)
-        slot_of_ref[exports[q][e]] = q * L.max_export + static_cast<int32_t>(e);
+        slot_of_ref[exports[q][e]] = q * L.xstride() + static_cast<int32_t>(e);
     for (int32_t ref : exports[part]) L.export_rows.push_back(dev_of_ref[ref]);
-    L.remote_slots = nparts * L.max_export;
   }
+  L.remote_slots = nparts * L.xstride();  // gathered records (exports + partials) of every part
 
   // ---- boundary columns: CSR over copies in ascending s (local copies ->
   // device rows, other parts' copies -> remote slots) and their data

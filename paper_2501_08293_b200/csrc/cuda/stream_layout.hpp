@@ -119,6 +119,8 @@ DOPF_HD inline void stage_plan(const StreamChunk& ch, StagePlan& sp) {
   sp.total = cur;
 }
 
+constexpr int32_t kExchangePartials = 8;  // gap, step, bx2, z2, lam2, maxinf, c'x, spare
+
 struct StreamLayout {
   int32_t S = 0, n = 0, N_z = 0;       // whole model
   int32_t rows = 0;                    // device rows (this rank)
@@ -140,10 +142,13 @@ struct StreamLayout {
   std::vector<int32_t> imp_ptr, imp_slot;  // boundary column -> its import slots (CSR)
   int32_t remote_slots = 0;            // partitioned: size of the gathered remote u array
   double bytes_per_iteration = 0;      // algorithmic bytes of this rank's share
-  // partitioned exchange: this rank's exported rows (u packed into slot
-  // part * max_export + e of every rank's remote array, in this order)
+  // partitioned exchange: ONE gather per iteration of every rank's packed
+  // record [u of its exported rows (max_export, zero padded) | its 8
+  // residual partials]; rank q's exports land in slots q * xstride() + e of
+  // every rank's remote array, its partials at q * xstride() + max_export
   int32_t nparts = 1, part = 0, max_export = 0;
   std::vector<int32_t> export_rows;
+  int32_t xstride() const { return max_export + kExchangePartials; }
   // re-upload fast path: every model value the layout holds, as an index
   // into the concatenation raw = [P | A | b | v | z0 | c | inv_copy | x_lo | x_hi]
   // of the model view (blob_src: -1 zero padding, -2 metadata to keep)

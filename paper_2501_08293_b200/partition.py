@@ -4,8 +4,9 @@ GPU; BASELINE config 4: the tiled feeder split by subtree).
 Each rank holds a contiguous, cost-balanced piece of the depth-first
 component walk (for the tiled feeder: runs of whole tiles). Per iteration
 (reference admm.cpp:190-235) every rank runs the HBM-streaming kernels on its
-piece. The only exchange is one gather of the boundary copies' u = z -
-lambda/rho (a few KB) plus 8 residual partials per rank. Every rank then sums
+piece. The only exchange is ONE gather per iteration of every rank's packed
+record: the boundary copies' u = z - lambda/rho (a few KB) followed by its 8
+residual partials. Every rank then sums
 each boundary column's copies in ascending s, and combines the partials in
 rank order, so iterates and the stop decision are bitwise identical on every
 rank and equal to the single-GPU solve.
@@ -84,7 +85,7 @@ class PartitionedSolver:
         self._err(self._lib.dopf_cuda_part_info(self._h, C.byref(info)))
         torch = self.torch
         dev = f"cuda:{self.device}"
-        key = (info.send, info.recv, info.partials, info.ranks, info.max_export)
+        key = (info.send, info.recv, info.xstride)
         # a captured graph bakes in the layout's kernel parameters (chunk
         # counts, boundary columns, export count): any upload invalidates it
         self._graph_key = None
@@ -93,12 +94,9 @@ class PartitionedSolver:
             return
         self.info = info
         self._buf_key = key
-        mx = max(1, info.max_export)
-        self.send = torch.as_tensor(_DevArray(info.send, mx), device=dev)[:info.max_export]
-        self.recv = torch.as_tensor(_DevArray(info.recv, max(1, self.world * info.max_export)),
-                                    device=dev)[:self.world * info.max_export]
-        self.partials = torch.as_tensor(_DevArray(info.partials, 8), device=dev)
-        self.ranks = torch.as_tensor(_DevArray(info.ranks, 8 * self.world), device=dev)
+        # [exports | 8 partials] per rank, gathered in rank order
+        self.send = torch.as_tensor(_DevArray(info.send, info.xstride), device=dev)
+        self.recv = torch.as_tensor(_DevArray(info.recv, self.world * info.xstride), device=dev)
         # one dedicated stream for the kernels AND the collectives (made current
         # around the loop), so they are ordered (a NULL handle would mean "own stream")
         if getattr(self, "stream", None) is None:
@@ -107,7 +105,7 @@ class PartitionedSolver:
         self._graph_key = None
         # eager collective: communicator set-up must not happen inside a graph capture
         with torch.cuda.stream(self.stream):
-            self._gather(self.ranks, self.partials)
+            self._gather(self.recv, self.send)
         self.stream.synchronize()
 
     def bytes_per_iteration(self) -> float:
@@ -139,9 +137,8 @@ class PartitionedSolver:
     def _iteration(self):
         lib, h = self._lib, self._h
         self._err(lib.dopf_cuda_part_step(h, 0))   # global update (x^t)
-        self._err(lib.dopf_cuda_part_step(h, 1))   # local, dual, exports, partials
-        self._gather(self.recv, self.send)
-        self._gather(self.ranks, self.partials)
+        self._err(lib.dopf_cuda_part_step(h, 1))   # local, dual, exports + partials record
+        self._gather(self.recv, self.send)          # the one exchange of the iteration
         self._err(lib.dopf_cuda_part_step(h, 2))   # identical stop decision everywhere
 
     def _solve(self, settings, poll_every, trace, graph):
@@ -213,3 +210,144 @@ class PartitionedSolver:
         return dopf.SolveResult(x, z, lam, res.status, res.iterations, res.objective,
                                 res.max_local_infeasibility, res.trace, res.timings, res.near_ties,
                                 res.first_near_tie)
+
+
+# --------------------------------------------------------------------------
+# The library's own NCCL path (C ABI dopf_cuda_comm_init / dopf_cuda_solve_part):
+# the whole partitioned loop -- kernels and one ncclAllGather of the packed
+# records per iteration -- is one CUDA graph on the device; Python only sets
+# it up. torch.distributed (any backend) carries the 128-byte NCCL id.
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = N.cuda().dopf_nccl_unique_id(buf)
+    if rc != 0:
+        raise RuntimeError("ncclGetUniqueId failed: " + (N.cuda().dopf_nccl_describe() or b"").decode())
+    return buf.raw
+
+
+def _share_of(solver: "dopf.CudaSolver", model, settings, trace):
+    n, Nz = model.global_cols, model.total_local_vars
+    x, z, lam = np.zeros(n), np.zeros(Nz), np.zeros(Nz)
+    xm, zm = np.zeros(n, dtype=np.uint8), np.zeros(Nz, dtype=np.uint8)
+    tr = np.zeros((settings.max_iter, 6)) if trace else None
+    r = N.ResultView_t()
+    r.x = x.ctypes.data_as(C.POINTER(C.c_double))
+    r.z = z.ctypes.data_as(C.POINTER(C.c_double))
+    r.lambda_ = lam.ctypes.data_as(C.POINTER(C.c_double))
+    if trace:
+        r.trace = tr.ctypes.data_as(C.POINTER(C.c_double))
+    st = settings.to_c()
+    rc = solver._lib.dopf_cuda_solve_part(solver._h, C.byref(st), C.byref(r),
+                                          xm.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                          zm.ctypes.data_as(C.POINTER(C.c_uint8)))
+    return rc, r, (x, z, lam, xm, zm, tr)
+
+
+def _result(r, bufs):
+    x, z, lam, xm, zm, tr = bufs
+    it = r.iterations
+    res = dopf.SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
+                           tr[:it].copy() if tr is not None else np.zeros((0, 6)), {"solve": r.time_solve},
+                           r.near_ties, r.first_near_tie)
+    res.x_mask, res.z_mask = xm.astype(bool), zm.astype(bool)
+    return res
+
+
+def merge_shares(shares) -> "dopf.SolveResult":
+    """Whole-model x, z, lambda from every rank's share (each entry from its
+    owner); scalars and trace are identical on every rank."""
+    first = shares[0]
+    x, z, lam = np.zeros_like(first.x), np.zeros_like(first.z), np.zeros_like(first.lam)
+    xs, zs = np.zeros(len(x), dtype=int), np.zeros(len(z), dtype=int)
+    for s in shares:
+        x[s.x_mask], z[s.z_mask], lam[s.z_mask] = s.x[s.x_mask], s.z[s.z_mask], s.lam[s.z_mask]
+        xs += s.x_mask
+        zs += s.z_mask
+    if not (np.all(xs == 1) and np.all(zs == 1)):
+        raise RuntimeError("partition does not cover every column / copy exactly once")
+    return dopf.SolveResult(x, z, lam, first.status, first.iterations, first.objective,
+                            first.max_local_infeasibility, first.trace, first.timings, first.near_ties,
+                            first.first_near_tie)
+
+
+class NcclPartitionedSolver:
+    """One rank (one process, one GPU) of a partitioned solve on the
+    library's NCCL communicator. `unique_id` comes from nccl_unique_id() on
+    rank 0, shared by the caller (see from_torch_distributed)."""
+
+    def __init__(self, device: int, nranks: int, rank: int, unique_id: bytes):
+        self.solver = dopf.CudaSolver(device)
+        self.nranks, self.rank = nranks, rank
+        self.solver._err(self.solver._lib.dopf_cuda_comm_init(self.solver._h, nranks, rank, unique_id))
+
+    @classmethod
+    def from_torch_distributed(cls, device: int, group=None) -> "NcclPartitionedSolver":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        return cls(device, world, rank, box[0])
+
+    def upload(self, model: "dopf.DecomposedModel", part_of_s: Optional[np.ndarray] = None):
+        if not model.has_precompute:
+            model.precompute()
+        self.model = model
+        self.part_of_s = np.ascontiguousarray(
+            partition_subsystems(model, self.nranks) if part_of_s is None else part_of_s, dtype=np.int32)
+        s = self.solver
+        s._err(s._lib.dopf_cuda_upload_part(s._h, C.byref(model.view()), self.nranks, self.rank,
+                                            self.part_of_s.ctypes.data_as(C.POINTER(N.i32))))
+        s.model = model
+
+    def solve(self, settings: "dopf.Settings", trace: bool = True) -> "dopf.SolveResult":
+        dopf._check_settings(settings)
+        rc, r, bufs = _share_of(self.solver, self.model, settings, trace)
+        self.solver._err(rc)
+        return _result(r, bufs)
+
+    def graph_mode(self) -> str:
+        return {0: "none", 1: "while-node", 2: "unrolled"}[self.solver._lib.dopf_cuda_part_graph_mode(self.solver._h)]
+
+    def bytes_per_iteration(self) -> float:
+        return self.solver.bytes_per_iteration()
+
+    def last_kernel_seconds(self) -> float:
+        return float(self.solver._lib.dopf_cuda_last_kernel_seconds(self.solver._h))
+
+
+class MultiGpuSolver:
+    """One process driving n GPUs (one context each, ncclCommInitAll): the
+    partitioned solve of one model, the ranks' loops on threads (the C ABI
+    releases the GIL)."""
+
+    def __init__(self, devices):
+        self.devices = list(devices)
+        self.solvers = [dopf.CudaSolver(d) for d in self.devices]
+        arr = (C.c_void_p * len(self.solvers))(*[s._h.value for s in self.solvers])
+        self.solvers[0]._err(self.solvers[0]._lib.dopf_cuda_comm_init_all(arr, len(self.solvers)))
+
+    def upload(self, model: "dopf.DecomposedModel", part_of_s: Optional[np.ndarray] = None):
+        if not model.has_precompute:
+            model.precompute()
+        n = len(self.solvers)
+        self.model = model
+        self.part_of_s = np.ascontiguousarray(
+            partition_subsystems(model, n) if part_of_s is None else part_of_s, dtype=np.int32)
+        for k, s in enumerate(self.solvers):
+            s._err(s._lib.dopf_cuda_upload_part(s._h, C.byref(model.view()), n, k,
+                                                self.part_of_s.ctypes.data_as(C.POINTER(N.i32))))
+            s.model = model
+
+    def solve(self, settings: "dopf.Settings", trace: bool = True) -> "dopf.SolveResult":
+        import concurrent.futures as cf
+        dopf._check_settings(settings)
+        with cf.ThreadPoolExecutor(max_workers=len(self.solvers)) as ex:
+            outs = list(ex.map(lambda s: _share_of(s, self.model, settings, trace), self.solvers))
+        shares = []
+        for s, (rc, r, bufs) in zip(self.solvers, outs):
+            s._err(rc)
+            shares.append(_result(r, bufs))
+        return merge_shares(shares)

@@ -130,3 +130,18 @@ def test_option_equals_value_form_is_accepted(tmp_path):
     rep = tmp_path / "r.json"
     code, _ = run("inspect", f"--input={fixture_path('two_bus')}", f"--report={rep}")
     assert code == 0 and json.loads(rep.read_text())["centralized"] == {"cols": 12, "rows": 11}
+
+
+@pytest.mark.gpu
+def test_solve_partitioned_gpus_flag_matches_single_gpu(tmp_path):
+    """`--gpus N` partitions the model over N devices with the NCCL exchange
+    (dopf::cuda::solve_partitioned); this run has one GPU, so N = 1 -- the
+    same report, bit for bit, as the single-device solve."""
+    args = ["solve", "--input", fixture_path("four_bus_delta"), "--eps-rel", "1e-4"]
+    code1, out1 = run(*args)
+    code2, out2 = run(*args, "--gpus", "1")
+    assert code1 == code2 == 0
+    a, b = json.loads(out1), json.loads(out2)
+    for k in ("timings_sec",):
+        a.pop(k), b.pop(k)
+    assert a == b
