@@ -266,26 +266,44 @@ def upload_bytes(models) -> int:
 
 def run_partitioned(args, rank, world, local):
     """Tiled feeder split by subtree over `world` GPUs (strong scaling): one
-    instance, boundary copies exchanged with NCCL every iteration."""
+    instance, one gather of the packed boundary records per iteration. On
+    GPUs (NCCL) the library drives it itself: dopf_cuda_comm_init +
+    dopf_cuda_solve_part, the whole loop -- kernels and ncclAllGather -- one
+    CUDA graph per solve. Ranks sharing one GPU (tests, gloo) step the same
+    kernels through torch.distributed (partition.PartitionedSolver)."""
     import numpy as np
     import torch
     import torch.distributed as td
 
     from paper_2501_08293_b200 import dopf
-    from paper_2501_08293_b200.partition import PartitionedSolver
+    from paper_2501_08293_b200.partition import NcclPartitionedSolver, PartitionedSolver
     torch.cuda.set_device(local)
     workers = max(1, (os.cpu_count() or 1) // max(1, world))
     f = dopf.tiled_feeder("ieee8500", args.tiles, args.seed)
     _, _, model = dopf.load_model(f, workers=workers)
     model.precompute(workers)
-    ps = PartitionedSolver(local)
+    capi = td.get_backend() == "nccl" and os.environ.get("DOPF_PART_IMPL", "capi") == "capi"
+    ps = NcclPartitionedSolver.from_torch_distributed(local) if capi else PartitionedSolver(local)
     if os.environ.get("DOPF_BENCH_PAGEABLE") != "1":
         ps.solver.pin(model)  # e2e inputs from pinned host memory (setup)
     ps.upload(model)
     settings = dopf.Settings(rho=100.0, eps_rel=1e-3, max_iter=50000)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    lib = ps.solver._lib
+
+    def timed_solve(trace=False):
+        if capi:  # CUDA events around the graph on the solver's stream (inside the library)
+            r = ps.solve(settings, trace=trace)
+            return r, float(lib.dopf_cuda_last_kernel_seconds(ps.solver._h))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ps.stream)
+        r = ps.solve(settings, trace=trace)
+        e1.record(ps.stream)
+        e1.synchronize()
+        return r, e0.elapsed_time(e1) * 1e-3
+
     for _ in range(max(3, args.warmup)):
-        ps.solve(settings, trace=False)
+        timed_solve()
     times, its = [], []
     k0 = ps.solver.kernels_executed()
     with ClockSampler(local) as clocks:
@@ -294,12 +312,8 @@ def run_partitioned(args, rank, world, local):
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(ps.stream)
-            r = ps.solve(settings, trace=False)
-            e1.record(ps.stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1) * 1e-3)
+            r, dt = timed_solve()
+            times.append(dt)
             its.append(r.iterations)
         td.barrier()
         torch.cuda.synchronize()
@@ -310,13 +324,14 @@ def run_partitioned(args, rank, world, local):
     max_t = max(float(a[0]) for a in allt)
     bytes_job = sum(float(a[1]) for a in allt)
     value = sum(its) / max_t
-    # e2e: upload (host layout + H2D) + solve + assembled host results, per step
+    # e2e per rank: upload of the whole model (host layout + H2D of its share)
+    # + solve + its share of x / z / lambda and the trace back in host memory
     e2e_t, e2e_it = 0.0, 0
     for step in range(args.steps + 1):
         td.barrier()
         t0 = time.perf_counter()
         ps.upload(model)
-        r = ps.assemble(ps.solve(settings, trace=True))
+        r = ps.solve(settings, trace=True)
         dt = time.perf_counter() - t0
         if step > 0:
             e2e_t += dt
@@ -325,6 +340,7 @@ def run_partitioned(args, rank, world, local):
     td.all_reduce(tt, op=td.ReduceOp.MAX)
     peak, peak_kind = read_peaks()
     achieved = bytes_job * (sum(its) / args.steps) / (max_t / args.steps) / 1e9
+    mode = ps.graph_mode() if capi else "torch.distributed steps"
     if rank == 0:
         st = model.stats()
         line = {
@@ -333,19 +349,23 @@ def run_partitioned(args, rank, world, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {**config_of(args, world), "parallelism": f"subtree-partitioned over {world} GPUs "
-                       "(NCCL all-gather of boundary copies + residual partials per iteration)"},
+                       "(one NCCL all-gather of the packed [boundary u | residual partials] records per "
+                       f"iteration; loop: {mode})"},
             "time_to_converge_ms": 1e3 * max_t / args.steps, "iterations_to_converge": int(its[-1]),
             "status": "converged" if r.status == 0 else "iteration_limit", "objective": r.objective,
             "e2e": {"value": e2e_it / float(tt[0]), "unit": "iter/s",
                     "h2d_bytes_per_step": int(8 * (st["sum_n2"] + st["sum_mn"]) + 40 * st["N_z"]),
                     "d2h_bytes_per_step": int(8 * (st["n"] + 2 * st["N_z"])),
-                    "time_to_converge_ms": 1e3 * float(tt[0]) / args.steps},
+                    "time_to_converge_ms": 1e3 * float(tt[0]) / args.steps,
+                    "note": "per rank: upload + solve + its share of the results to host memory; "
+                            "max over ranks"},
             "gpu_launches": int(kernels),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
                          "frac": achieved / (peak * world), "traffic": None, "peak_kind": peak_kind,
                          "bytes_per_iteration": bytes_job,
                          "note": "whole job: algorithmic bytes of all ranks / max rank time vs world x HBM peak"},
-            "kernel": {"name": "k_global+k_staged(+k_local)+k_pack+k_decide per iteration", "ranks": world},
+            "kernel": {"name": "k_global+k_staged(+k_local)+k_pack+ncclAllGather+k_decide per iteration",
+                       "ranks": world, "driver": "C ABI dopf_cuda_solve_part" if capi else "python"},
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -355,7 +375,10 @@ def main():
     args = parse_args()
     rank, world, local = dist_env()
     import torch
-    if world > 1:
+    # DOPF_BENCH_PARTITIONED=1: the partitioned tiled path even at one rank
+    # (under torchrun; exercises the NCCL loop on a one-GPU box)
+    part_one = args.config == "tiled" and os.environ.get("DOPF_BENCH_PARTITIONED") == "1"
+    if world > 1 or part_one:
         import torch.distributed as td
         shared = os.environ.get("DOPF_SHARE_GPU") == "1"  # NCCL refuses two ranks on one GPU
         backend = os.environ.get("DOPF_DIST_BACKEND") or (
@@ -367,7 +390,7 @@ def main():
             import torch.distributed as td
             td.destroy_process_group()
         return
-    if args.config == "tiled" and world > 1:
+    if args.config == "tiled" and (world > 1 or part_one):
         run_partitioned(args, rank, world, local)
         import torch.distributed as td
         td.destroy_process_group()

@@ -146,6 +146,9 @@ struct dopf_cuda_ctx {
   int part_graph_mode = 0;           // 1 device while-node, 2 unrolled bodies + lazy host poll
   double part_key[6] = {0, 0, 0, 0, 0, 0};
   cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  // second stream: the direct-load chunk kernel beside the staged one (fork / join)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int32_t* h_flags = nullptr;        // pinned: done flags of the last two unrolled launches
 
   int64_t launches = 0;
@@ -611,6 +614,9 @@ int dopf_cuda_create(int device, dopf_cuda_ctx** out) {
     c->stream = c->own_stream;
     ck(cudaEventCreate(&c->ev0), "event");
     ck(cudaEventCreate(&c->ev1), "event");
+    ck(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming), "event");
   });
   if (rc != DOPF_OK) {
     // keep the message reachable for the caller through a leaked-free path
@@ -763,6 +769,24 @@ void stream_reset(dopf_cuda_ctx* c) {
   ck(cudaMemsetAsync(d.lam, 0, L.rows * sizeof(double), c->stream), "lambda0");
   ck(cudaMemsetAsync(d.ctl, 0, sizeof(StreamCtl), c->stream), "ctl");
   ck(cudaMemsetAsync(d.final_count, 0, sizeof(unsigned), c->stream), "counter");
+}
+
+// The chunk kernels of one iteration on c->stream, the direct-load kernel on
+// the auxiliary stream beside the staged one (a fork / join: under stream
+// capture these become parallel graph branches), then the export pack.
+void launch_chunks(dopf_cuda_ctx* c, const StreamParams& p) {
+  if (p.n_big > 0 && p.n_staged > 0) {
+    ck(cudaEventRecord(c->fork_ev, c->stream), "fork");
+    ck(cudaStreamWaitEvent(c->aux, c->fork_ev, 0), "fork");
+    stream_launch_direct(p, c->aux);
+    ck(cudaEventRecord(c->join_ev, c->aux), "join");
+    stream_launch_staged(p, c->stream);
+    ck(cudaStreamWaitEvent(c->stream, c->join_ev, 0), "join");
+  } else {
+    stream_launch_direct(p, c->stream);
+    stream_launch_staged(p, c->stream);
+  }
+  stream_launch_pack(p, c->stream);
 }
 
 void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, bool copy_vectors) {
@@ -1311,7 +1335,7 @@ int dopf_cuda_part_step(dopf_cuda_ctx* c, int32_t phase) {
       stream_launch_global(p, c->stream);
       c->kernels += 1;
     } else if (phase == 1) {
-      stream_launch_local(p, c->stream);
+      launch_chunks(c, p);
       c->kernels += (p.n_staged > 0 ? 1 : 0) + (p.n_big > 0 ? 1 : 0) + (p.max_export > 0 ? 1 : 0);
     } else if (phase == 2) {
       stream_launch_decide(p, c->sd.u_remote, c->SL.nparts, c->SL.xstride(), c->stream);
@@ -1351,7 +1375,8 @@ void part_results(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask, uint8_
     c->last_kernel_s = ms * 1e-3;
     const StreamLayout& L = c->SL;
     StreamCtl h{};
-    ck(cudaMemcpy(&h, c->sd.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost), "d2h");
+    ck(cudaMemcpyAsync(&h, c->sd.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "d2h");
     r->status = h.status;
     r->iterations = h.t;
     r->objective = h.objective;
@@ -1360,10 +1385,15 @@ void part_results(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask, uint8_
     r->first_near_tie = h.first_tie;
     r->time_solve = c->last_kernel_s;
     const std::size_t R = static_cast<std::size_t>(L.rows);
-    std::vector<double> z(R), lam(R), x(L.cols);
-    ck(cudaMemcpy(z.data(), c->sd.z, R * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
-    ck(cudaMemcpy(lam.data(), c->sd.lam, R * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
-    ck(cudaMemcpy(x.data(), c->sd.x, L.cols * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    // through the context's page-locked staging buffer (DMA speed), then
+    // scattered to reference order on the host
+    double* z = static_cast<double*>(c->stage((2 * R + L.cols) * sizeof(double)));
+    double* lam = z + R;
+    double* x = z + 2 * R;
+    ck(cudaMemcpyAsync(z, c->sd.z, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(lam, c->sd.lam, R * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(x, c->sd.x, L.cols * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "d2h");
     for (int32_t q = 0; q < L.cols; ++q) {
       if (!L.owner[q]) continue;
       if (r->x) r->x[L.gcol[q]] = x[q];
@@ -1522,6 +1552,9 @@ void dopf_cuda_destroy(dopf_cuda_ctx* c) {
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
+  if (c->aux) cudaStreamDestroy(c->aux);
   if (c->poll_ev[0]) cudaEventDestroy(c->poll_ev[0]);
   if (c->poll_ev[1]) cudaEventDestroy(c->poll_ev[1]);
   if (c->h_flags) cudaFreeHost(c->h_flags);
@@ -1793,7 +1826,7 @@ void enqueue_allgather(dopf_cuda_ctx* c) {
 // one iteration on c->stream (eager or under capture)
 void enqueue_part_iteration(dopf_cuda_ctx* c, const StreamParams& p) {
   stream_launch_global(p, c->stream);
-  stream_launch_local(p, c->stream);  // chunk kernels + k_pack: this rank's record
+  launch_chunks(c, p);  // chunk kernels side by side + k_pack: this rank's record
   enqueue_allgather(c);
   stream_launch_decide(p, c->sd.u_remote, c->SL.nparts, c->SL.xstride(), c->stream);
 }
@@ -1890,13 +1923,17 @@ void prepare_part_graph(dopf_cuda_ctx* c, const StreamParams& p, const dopf_sett
   std::copy(key, key + 6, c->part_key);
 }
 
+// our kernels per partitioned iteration: k_global, chunk kernels, k_pack, k_decide
+int part_kernels_per_iteration(const dopf_cuda_ctx* c) {
+  return 2 + (c->SL.staged_ids.empty() ? 0 : 1) + (c->SL.big_ids.empty() ? 0 : 1) + (c->SL.max_export > 0 ? 1 : 0);
+}
+
 void run_part_graph(dopf_cuda_ctx* c, int max_iter) {
-  const int per_it = 4 + (c->SL.staged_ids.empty() ? 0 : 1) + (c->SL.big_ids.empty() ? 0 : 1) - 1;
+  const int per_it = part_kernels_per_iteration(c);
   if (c->part_graph_mode == 1) {
     ck(cudaGraphLaunch(c->part_graph, c->stream), "graph launch");
     ++c->launches;
-    c->kernels += per_it;  // (per iteration; the count of iterations is known after the stop)
-    return;
+    return;  // kernels counted from the iteration count (dopf_cuda_solve_part)
   }
   if (!c->poll_ev[0]) {
     ck(cudaEventCreateWithFlags(&c->poll_ev[0], cudaEventDisableTiming), "event");
@@ -2007,6 +2044,7 @@ int dopf_cuda_solve_part(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_v
     ck(cudaEventRecord(c->ev0, c->stream), "event");
     run_part_graph(c, s->max_iter);
     part_results(c, r, x_mask, z_mask);
+    if (c->part_graph_mode == 1) c->kernels += part_kernels_per_iteration(c) * r->iterations;
   });
 }
 

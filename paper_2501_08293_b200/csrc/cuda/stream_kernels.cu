@@ -638,6 +638,13 @@ void stream_launch_local(const StreamParams& p, cudaStream_t s) {
   launch_local_all(p, s);  // the last chunk CTA writes this rank's partials
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
 }
+void stream_launch_direct(const StreamParams& p, cudaStream_t s) {
+  if (p.n_big > 0) local_kernel()<<<p.n_big, kStreamRows, 0, s>>>(p);
+}
+void stream_launch_staged(const StreamParams& p, cudaStream_t s) {
+  if (p.n_staged > 0)
+    staged_kernel(p.staged_ctas, p.prof != nullptr)<<<p.staged_grid, kStagedThreads, p.stages * p.stage_bytes, s>>>(p);
+}
 void stream_launch_pack(const StreamParams& p, cudaStream_t s) {
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
 }

@@ -110,6 +110,11 @@ void stream_launch_iteration(const StreamParams& p, cudaStream_t s);
 void stream_launch_global(const StreamParams& p, cudaStream_t s);
 void stream_launch_local(const StreamParams& p, cudaStream_t s);
 void stream_launch_pack(const StreamParams& p, cudaStream_t s);
+/// The chunk kernels one at a time: direct-load chunks (image from HBM), and
+/// the staged (bulk-copy pipelined) kernel -- to run side by side on two
+/// streams (they occupy disjoint SMs).
+void stream_launch_direct(const StreamParams& p, cudaStream_t s);
+void stream_launch_staged(const StreamParams& p, cudaStream_t s);
 void stream_launch_decide(const StreamParams& p, const double* recv, int nranks, int stride, cudaStream_t s);
 
 }  // namespace dopf::cuda

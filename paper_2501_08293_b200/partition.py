@@ -54,6 +54,16 @@ def probe_part(model, nparts: int, part: int, part_of_s: np.ndarray) -> dict:
             "max_export": info.max_export, "bytes_per_iteration": info.bytes_per_iteration}
 
 
+def _partition_for(owner, model, nparts: int, part_of_s) -> np.ndarray:
+    """The given map, else the cost-balanced walk partition -- computed once
+    per model (a same-model re-upload, e.g. every e2e step, reuses it)."""
+    if part_of_s is not None:
+        return np.ascontiguousarray(part_of_s, dtype=np.int32)
+    if getattr(owner, "model", None) is model and getattr(owner, "part_of_s", None) is not None:
+        return owner.part_of_s
+    return np.ascontiguousarray(partition_subsystems(model, nparts), dtype=np.int32)
+
+
 class PartitionedSolver:
     """One rank's share of a partitioned solve (torch.distributed must be up)."""
 
@@ -76,9 +86,8 @@ class PartitionedSolver:
     def upload(self, model: "dopf.DecomposedModel", part_of_s: Optional[np.ndarray] = None):
         if not model.has_precompute:
             model.precompute()
+        self.part_of_s = _partition_for(self, model, self.world, part_of_s)
         self.model = model
-        self.part_of_s = np.ascontiguousarray(
-            partition_subsystems(model, self.world) if part_of_s is None else part_of_s, dtype=np.int32)
         self._err(self._lib.dopf_cuda_upload_part(self._h, C.byref(model.view()), self.world, self.rank,
                                                   self.part_of_s.ctypes.data_as(C.POINTER(N.i32))))
         info = N.PartInfo_t()
@@ -294,9 +303,8 @@ class NcclPartitionedSolver:
     def upload(self, model: "dopf.DecomposedModel", part_of_s: Optional[np.ndarray] = None):
         if not model.has_precompute:
             model.precompute()
+        self.part_of_s = _partition_for(self, model, self.nranks, part_of_s)
         self.model = model
-        self.part_of_s = np.ascontiguousarray(
-            partition_subsystems(model, self.nranks) if part_of_s is None else part_of_s, dtype=np.int32)
         s = self.solver
         s._err(s._lib.dopf_cuda_upload_part(s._h, C.byref(model.view()), self.nranks, self.rank,
                                             self.part_of_s.ctypes.data_as(C.POINTER(N.i32))))

@@ -138,10 +138,11 @@ def test_solve_partitioned_gpus_flag_matches_single_gpu(tmp_path):
     (dopf::cuda::solve_partitioned); this run has one GPU, so N = 1 -- the
     same report, bit for bit, as the single-device solve."""
     args = ["solve", "--input", fixture_path("four_bus_delta"), "--eps-rel", "1e-4"]
-    code1, out1 = run(*args)
-    code2, out2 = run(*args, "--gpus", "1")
+    r1, r2 = tmp_path / "one.json", tmp_path / "part.json"   # (NCCL may log to stdout)
+    code1, _ = run(*args, "--report", str(r1))
+    code2, _ = run(*args, "--gpus", "1", "--report", str(r2))
     assert code1 == code2 == 0
-    a, b = json.loads(out1), json.loads(out2)
+    a, b = json.loads(r1.read_text()), json.loads(r2.read_text())
     for k in ("timings_sec",):
         a.pop(k), b.pop(k)
     assert a == b
