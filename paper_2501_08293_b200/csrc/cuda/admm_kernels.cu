@@ -67,13 +67,16 @@ namespace {
 
 constexpr int kWarps = kThreads / 32;
 constexpr int kHoist = kThreads > 512 ? 4 : 8;  // operator loads in flight per row (register budget)
-constexpr int kCW = kThreads - 32;  // compute threads (warps 1..)
+constexpr int kCW = kComputeThreads;  // compute threads (warps 2..)
+constexpr int kSyncThreads = kCW + 32;  // service + compute warps (the check warp runs decoupled)
 constexpr int kSlots = kSlotRing;  // partial-slot ring (see header)
 constexpr int kDec = 8;             // decision ring (shared memory), > kLag
 static_assert(kDec > kLag, "decision ring too small");
 constexpr int kDecG = 8;            // decision ring (global, written by the leader CTA)
 constexpr int kLine = 16;           // u64 words per 128-byte line: flags are one per line
-enum : int { kBarCompute = 1, kBarExchanged = 3, kBarPartials = 4 };
+enum : int { kBarCompute = 1, kBarExchanged = 3, kBarPartials = 4,
+             kBarZReady = 5,   // 5, 6 by iteration parity: z^t written (compute arrive, check warp syncs)
+             kBarZFree = 7 };  // 7, 8 by iteration parity: z^t checked (check warp arrives, compute syncs)
 // phase clock slots (per CTA): compute warp 1 lane 0, service lane 0
 enum : int { kPhTarget = 0, kPhGemv, kPhDual, kPhEqRed, kPhWait, kPhGlobal, kPhSvcNbr, kPhSvcAll };
 
@@ -207,8 +210,8 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
   // tu: GEMV target during (L), then the exchange value u from (D) to (G)
   double* tu = smem + off;
   off += bd.rows;
-  double* zs = smem + off;
-  off += bd.rows;
+  double* zbuf = smem + off;  // [2][rows]: z^t in buffer t & 1 (the service warp checks A z^t
+  off += 2 * static_cast<std::size_t>(bd.rows);  // while the compute warps write z^{t+1})
   double* vs = smem + off;
   off += bd.rows;
   double* xring = smem + off;  // [kXRing][cols]: x^s in slot s % kXRing
@@ -229,8 +232,10 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
   off += kDec * 4;
   long long* ph = reinterpret_cast<long long*>(smem + off);  // [8] phase clock
   off += 8;
-  double* emax = smem + off;  // [kLag + 1][kWarps] per-warp infeasibility of the last iterations
-  off += (kLag + 1) * kWarps;
+  double* emax = smem + off;  // [kLag + 1] block infeasibility of the last iterations (check warp)
+  off += kLag + 1;
+  double* adone = smem + off;  // t_last + 1 once the compute warps left their loop (ends the check warp)
+  off += 1;
   double* a_rhs = smem + off;  // equality-row rhs b_r
   off += bd.arows;
   AMeta* a_meta = reinterpret_cast<AMeta*>(smem + off);  // 16 B each
@@ -257,7 +262,9 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
     c_hi[c] = p.chi[bd.col_off + c];
   }
   if (tid < kDec * 4) dec[tid] = 0.0;
-  if (tid < (kLag + 1) * kWarps) emax[tid] = 0.0;
+  if (tid < kLag + 1) emax[tid] = 0.0;
+  if (tid == 0) adone[0] = 0.0;
+  for (int i = tid; i < 2 * kWarps * kPartials; i += kThreads) red[i] = 0.0;  // the check warp adds zeros
   if (tid < 8) ph[tid] = 0;
 
   const int G = id.blocks;
@@ -273,8 +280,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
   __syncthreads();
 
   int stop_at = 0;  // set by the branch that detects the stop; broadcast below
-  double m_old = 0.0;   // compute warps (lane 0): warp infeasibility max over iterations <= t - kLag - 1
-  int thread_last = 0;  // compute threads: last iteration executed
+  double m_old = 0.0;  // check warp (lane 0): infeasibility max over iterations <= s - kLag - 1
   if (warp == 0) {
     // ======================= service warp =======================
     const bool leader_cta = bd.inst_block == 0;  // writes the trace and the scalar results
@@ -348,10 +354,10 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
     int t = 1;
     for (;; ++t) {
       const long long c0 = tick ? clock64() : 0;
-      named_sync(kBarPartials, kThreads);  // warp partials of t in red[t & 1]
+      named_sync(kBarPartials, kSyncThreads);  // warp partials of t in red[t & 1]
       const long long c1 = tick ? clock_after_barrier(ph) : 0;
       const bool cw_stop = (t > kLag && dec[((t - kLag) % kDec) * 4] != 0.0) || t == p.max_iter;
-      named_arrive(kBarExchanged, kThreads);
+      named_arrive(kBarExchanged, kSyncThreads);
       // residuals / stop test of t-1 (read by the compute warps at t+1) --
       // BEFORE counting slot(t): a block's count for t then also certifies it
       // finished reading every slot of t-1, so the slot ring cannot be
@@ -398,9 +404,60 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
         p.ties[2 * bd.instance + 1] = first_tie;
       }
     }
+  } else if (warp == 1) {
+    // ======================= equality-check warp =======================
+    // Decoupled from the exchange: it waits only for z^t (barrier
+    // kBarZReady + t % 2) and releases its buffer (kBarZFree + t % 2) for
+    // the compute warps' GEMV of t + 2; barriers alternate by parity so no
+    // side can arrive twice on one barrier before the other has passed it.
+    // (A) local equality residual ||A_s z_s - b_s||_inf of iteration s
+    // (admm.cpp:203-205) over the block's equality rows, from z^s in shared
+    // memory -- off the compute warps' critical path. Lane l takes rows l,
+    // l + 32, ... (the rows of one sliced-ELL lane: conflict-free); four rows
+    // in flight per lane. The infeasibility is a max over iterations
+    // (admm.cpp:219-220): m_old holds iterations <= s - kLag - 1, emax the last
+    // kLag + 1, folded once the stopping iteration is known.
+    auto acheck = [&](int s) {
+      const double* zsrc = zbuf + static_cast<std::size_t>(s & 1) * bd.rows;
+      double e = 0.0;
+      for (int a0 = lane; a0 < bd.arows; a0 += 4 * 32) {
+        double acc[4];
+        AMeta am[4];
+        int nmax = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i] = 0.0;
+          const int a = a0 + 32 * i;
+          am[i] = a < bd.arows ? a_meta[a] : AMeta{0, 0, 0, 0};
+          nmax = am[i].n > nmax ? am[i].n : nmax;
+        }
+        for (int j = 0; j < nmax; ++j) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (j < am[i].n) acc[i] = acc[i] + Aop[am[i].aofs + 32 * j] * zsrc[am[i].base + j];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (a0 + 32 * i < bd.arows) e = sel_max(e, fabs(acc[i] - a_rhs[a0 + 32 * i]));
+      }
+      e = warp_max(e);
+      if (lane == 0) {
+        double* slot = emax + s % (kLag + 1);
+        m_old = sel_max(m_old, *slot);
+        *slot = e;
+      }
+      __syncwarp();
+    };
+
+    for (int s = 1;; ++s) {
+      named_sync(kBarZReady + (s & 1), kCW + 32);
+      if (static_cast<int>(*reinterpret_cast<volatile double*>(adone)) == s) break;
+      acheck(s);
+      named_arrive(kBarZFree + (s & 1), kCW + 32);
+    }
   } else {
     // ======================= compute warps =======================
-    const int ctid = tid - 32;
+    const int ctid = tid - 64;
     const bool tick = clock_on && ctid == 0;
     // per-thread metadata, packed to keep the K-way state in registers:
     //  row: pofs, and n (bits 0-6) | exported (7) | base (8-19) | xloc (20-31)
@@ -546,6 +603,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
       unsigned long long* u_out = p.ux + static_cast<int64_t>(t & 1) * 2 * p.rows_total;
       double* z_res = p.z_out + static_cast<int64_t>(t % kZRing) * p.rows_total;
       double* l_res = p.lam_out + static_cast<int64_t>(t % kZRing) * p.rows_total;
+      double* zs = zbuf + static_cast<std::size_t>(t & 1) * bd.rows;
 
       // (L1) consensus target
 #pragma unroll
@@ -562,7 +620,9 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
 
       // (L2) z = P t + v, one row per thread and slot k; P in sliced-ELL order
       // (entry j of a warp's 32 rows is 256 contiguous bytes). Each row's
-      // loads are issued 8 at a time ahead of its sequential-j sum.
+      // loads are issued 8 at a time ahead of its sequential-j sum. z^t goes
+      // to buffer t % 2, once the check warp is done with z^{t-2} there.
+      if (t >= 3) named_sync(kBarZFree + (t & 1), kCW + 32);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int r = ctid + k * kCW;
@@ -589,6 +649,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
           zs[r] = acc + vs[r];
         }
       }
+      named_arrive(kBarZReady + (t & 1), kCW + 32);  // z^t for the check warp
       // every row's target read before (D) overwrites tu; z visible to (A)
       named_sync(kBarCompute, kCW);
       if (tick) {
@@ -637,38 +698,8 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
       // the exchange; x^{t+1} goes to slot (t+1) % 4, so x^{t-2} (a possible
       // stopping iterate) survives
       double obj_next = global_interior(xnext);
-      // (A) local equality residual ||A_s z_s - b_s||_inf, result copies,
-      // partial reductions -- overlapping the exchange. The infeasibility is
-      // a max over iterations (admm.cpp:219-220): each thread keeps its own
-      // running max (m_old: iterations <= t-3) plus the last three
-      // iterations, folded once the stopping iteration is known.
-      double e_t = 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int a = ctid + k * kCW;
-        if (a < bd.arows) {
-          const AMeta am = a_meta[a];
-          const double* ar = Aop + am.aofs;
-          const double* zb = zs + am.base;
-          double acc = 0.0;
-          for (int j0 = 0; j0 < am.n; j0 += kHoist) {
-            double av[kHoist], zv[kHoist];
-#pragma unroll
-            for (int e = 0; e < kHoist; ++e) {
-              av[e] = 0.0;
-              zv[e] = 0.0;
-              if (j0 + e < am.n) {
-                av[e] = ar[(j0 + e) * 32];
-                zv[e] = zb[j0 + e];
-              }
-            }
-#pragma unroll
-            for (int e = 0; e < kHoist; ++e)
-              if (j0 + e < am.n) acc = acc + av[e] * zv[e];
-          }
-          e_t = sel_max(e_t, fabs(acc - a_rhs[a]));
-        }
-      }
+      // result copies and partial reductions -- overlapping the exchange
+      // (the equality check of z^t runs on the service warp)
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int r = ctid + k * kCW;
@@ -678,20 +709,10 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
         }
       }
       {
-        // warp max of this iteration into the ring; lane 0 folds the value
-        // leaving the ring (iteration t - kLag - 1) into its running max
-        const double we = warp_max(e_t);
-        if (lane == 0) {
-          double* slot = emax + (t % (kLag + 1)) * kWarps + warp;
-          m_old = sel_max(m_old, *slot);
-          *slot = we;
-        }
-      }
-      {
         const double mine = sum8(v8, lane);
         if ((lane & 3) == 0) red[(t & 1) * kWarps * kPartials + warp * kPartials + sum8_index(lane)] = mine;
       }
-      named_arrive(kBarPartials, kThreads);
+      named_arrive(kBarPartials, kSyncThreads);
       if (tick) {
         c1 = clock_after_barrier(ph);
         ph[kPhEqRed] += c1 - c0;
@@ -706,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
         ph[kPhGlobal] += c1 - c0;
         c0 = c1;
       }
-      named_sync(kBarExchanged, kThreads);  // decision of t-2 in dec[]; x^{t+1} complete
+      named_sync(kBarExchanged, kSyncThreads);  // decision of t-2 in dec[]; x^{t+1} complete
       if (tl) {
         (void)clock_after_barrier(ph);
         tl[2] = globaltimer();  // every boundary column of the block done
@@ -718,26 +739,27 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
       }
       if ((t > kLag && dec[((t - kLag) % kDec) * 4] != 0.0) || t == p.max_iter) break;
     }
-    thread_last = t;
+    // release the check warp from its wait for z^{t+1}
+    if (ctid == 0) *reinterpret_cast<volatile double*>(adone) = t + 1;
+    named_arrive(kBarZReady + ((t + 1) & 1), kCW + 32);
   }
   __syncthreads();
   stop_at = static_cast<int>(red[0]);
   if (clock_on && tid < 8) p.prof[blockIdx.x * 8 + tid] += ph[tid];
-  if (warp != 0) {
-    // max_local_infeasibility over iterations 1..stop_at: the loop ended at
-    // t = last, stop_at >= last - kLag; the ring holds iterations last-kLag..last
-    const int last = thread_last;
+  if (warp == 1 && lane == 0) {
+    // max_local_infeasibility over iterations 1..stop_at: the check warp saw
+    // iterations up to the compute warps' last one, last - kLag <= stop_at <= last
+    const int last = static_cast<int>(adone[0]) - 1;
     double mx = m_old;
     for (int q = last - kLag; q <= stop_at; ++q)
-      if (q >= 1) mx = sel_max(mx, emax[(q % (kLag + 1)) * kWarps + warp]);
-    if (lane == 0)
-      atomicMax(reinterpret_cast<unsigned long long*>(p.maxinf + bd.instance),
-                static_cast<unsigned long long>(__double_as_longlong(mx)));  // mx >= 0: bit order = value order
+      if (q >= 1) mx = sel_max(mx, emax[q % (kLag + 1)]);
+    atomicMax(reinterpret_cast<unsigned long long*>(p.maxinf + bd.instance),
+              static_cast<unsigned long long>(__double_as_longlong(mx)));  // mx >= 0: bit order = value order
   }
-  if (warp != 0) {
+  if (warp >= 2) {
     // owners write x^stop_at (still in the ring); (z, lambda)^stop_at are in
     // result buffer stop_at % kZRing, which the host reads
-    const int ctid = tid - 32;
+    const int ctid = tid - 64;
     const double* xfinal = xring + static_cast<std::size_t>(stop_at % kXRing) * bd.cols;
     for (int c = ctid; c < bd.cols; c += kCW) {
       const ColMeta cmc = p.cmeta[bd.col_off + c];

@@ -633,7 +633,7 @@ namespace {
 
 bool needs_streaming(const dopf_model_view& m, const LayoutOptions& opt) {
   // resident kernel: <= 148 CTAs x 480 threads x kMaxK rows, operators in smem
-  const int64_t cap_rows = static_cast<int64_t>(opt.max_blocks) * (opt.threads - 32) * kMaxK;
+  const int64_t cap_rows = static_cast<int64_t>(opt.max_blocks) * (opt.threads - 64) * kMaxK;
   if (m.N_z > cap_rows) return true;
   double bytes = 0;
   for (int s = 0; s < m.S; ++s) {

@@ -37,6 +37,9 @@
 namespace dopf::cuda {
 
 constexpr int kThreads = 512;   // CTA size of the iteration kernels
+// warp 0: service (exchange flags, residual combine, stop test); warp 1: the
+// equality check ||A z - b||_inf; warps 2..: compute (rows, columns)
+constexpr int kComputeThreads = kThreads - 64;
 constexpr int kMaxK = 4;        // max rows (and cols, A-rows) per thread
 constexpr int kPartials = 8;    // gap, step, bx2, z2, lam2, objective, maxinf, pad
 

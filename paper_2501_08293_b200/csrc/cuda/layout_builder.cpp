@@ -84,10 +84,10 @@ std::size_t block_smem_bytes(const BlockDesc& b, bool ops_in_smem) {
   // must match the carve-up at the top of admm_persistent
   std::size_t doubles = 0;
   if (ops_in_smem) doubles += static_cast<std::size_t>(b.p_len) + b.a_len;
-  doubles += 3ull * b.rows;                     // target, z, v
+  doubles += 4ull * b.rows;                     // target, z (two buffers), v
   doubles += (kXRing + 5ull) * b.cols;          // x ring, c/rho, inv, lo, hi, c
   doubles += 2 * (kThreads / 32ull) * kPartials + 8 * 4 + 8;  // warp partials x2, decision ring, phase clock
-  doubles += (kLag + 1ull) * (kThreads / 32);   // per-warp infeasibility ring
+  doubles += kLag + 2ull;                       // block infeasibility ring + end flag (check warp)
   doubles += 3ull * b.arows;                    // equality rows: rhs + AMeta (16 B)
   return 8 * doubles + 4ull * b.copy_len + 64;
 }
@@ -125,7 +125,7 @@ int choose_blocks(const dopf_model_view& m, const LayoutOptions& opt) {
     bytes += 8.0 * (n * n + m.m_s[s] * n) + 16.0 * n + 4.0 * n;
   }
   bytes += 56.0 * m.n;
-  const int rows_cap = (opt.threads - 32) * 2;
+  const int rows_cap = (opt.threads - 64) * 2;
   int g0 = static_cast<int>(bytes / (0.92 * static_cast<double>(opt.smem_limit))) + 1;
   g0 = std::max(g0, (m.N_z + rows_cap - 1) / rows_cap);
   g0 = std::max(1, std::min(g0, std::max(1, m.S)));
@@ -164,7 +164,7 @@ InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions&
   const std::vector<std::vector<int>> parts =
       split_blocks(m, locality_order_impl(m), std::max(1, std::min(G, std::max(1, m.S))));
   const int nb = static_cast<int>(parts.size());
-  const int cw = opt.threads - 32;
+  const int cw = opt.threads - 64;  // compute threads (kComputeThreads)
 
   // Pass 1: device rows (subsystems by n_s descending inside each block).
   std::vector<int32_t> dev_of_ref(m.N_z, -1);
@@ -180,7 +180,7 @@ InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions&
     // widest row of every slot; reversing the subsystem order inside odd
     // slots pairs wide rows of one slot with narrow rows of the next.
     {
-      const int cwb = opt.threads - 32;
+      const int cwb = opt.threads - 64;
       std::vector<int> out;
       std::vector<int> seg;
       int rows_done = 0, k = 0;
@@ -333,7 +333,7 @@ InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions&
     bd.ops_in_smem = block_smem_bytes(bd, true) <= opt.smem_limit ? 1 : 0;
     if (!bd.ops_in_smem) P.all_ops_in_smem = false;
     P.smem_bytes = std::max(P.smem_bytes, block_smem_bytes(bd, bd.ops_in_smem));
-    // warps 1.. (cw threads) own rows, interior columns and equality rows
+    // warps 2.. (cw threads) own rows, interior columns and equality-row slots
     const int k_need = (std::max(bd.rows, std::max(bd.cols_int, bd.arows)) + cw - 1) / cw;
     P.K = std::max(P.K, std::max(1, k_need));
     P.blocks.push_back(bd);
