@@ -63,6 +63,7 @@ class BatchSolver:
             out.append(dopf.SolveResult(x, z, lam, rs[i].status, it, rs[i].objective,
                                         rs[i].max_local_infeasibility,
                                         tr[:it].copy() if tr is not None else np.zeros((0, 6)),
-                                        {"solve": rs[i].time_solve}, rs[i].near_ties,
+                                        {"solve": rs[i].time_solve, "global": rs[i].time_global,
+                                         "local": rs[i].time_local, "dual": rs[i].time_dual}, rs[i].near_ties,
                                         rs[i].first_near_tie))
         return out

@@ -458,7 +458,9 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
   } else {
     // ======================= compute warps =======================
     const int ctid = tid - 64;
-    const bool tick = clock_on && ctid == 0;
+    // phase clock: every iteration when profiling, else every kSampleEvery-th
+    // iteration of block 0 of instance 0 (the solve's PhaseTimings split)
+    const bool sampler = ctid == 0 && (clock_on || (bd.instance == 0 && bd.inst_block == 0));
     // per-thread metadata, packed to keep the K-way state in registers:
     //  row: pofs, and n (bits 0-6) | exported (7) | base (8-19) | xloc (20-31)
     //  col: copy_start (bits 0-22) | copy_count (23-30) | owner (31)
@@ -595,9 +597,10 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
     double obj = global_interior(xring + bd.cols);
     obj = obj + global_boundary(0, xring + bd.cols);
     named_sync(kBarCompute, kCW);
-    long long c0 = tick ? clock64() : 0, c1 = 0;
+    long long c0 = sampler ? clock64() : 0, c1 = 0;
     int t = 1;
     for (;; ++t) {
+      const bool tick = sampler && (clock_on || t % kSampleEvery == 1);
       const double* xt = xring + static_cast<std::size_t>(t % kXRing) * bd.cols;  // x^t
       double* xnext = xring + static_cast<std::size_t>((t + 1) % kXRing) * bd.cols;
       unsigned long long* u_out = p.ux + static_cast<int64_t>(t & 1) * 2 * p.rows_total;
@@ -736,6 +739,8 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
         c1 = clock_after_barrier(ph);
         ph[kPhWait] += c1 - c0;
         c0 = c1;
+      } else if (sampler && (t + 1) % kSampleEvery == 1) {
+        c0 = clock_after_barrier(ph);  // start of the next sampled iteration
       }
       if ((t > kLag && dec[((t - kLag) % kDec) * 4] != 0.0) || t == p.max_iter) break;
     }
@@ -746,6 +751,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
   __syncthreads();
   stop_at = static_cast<int>(red[0]);
   if (clock_on && tid < 8) p.prof[blockIdx.x * 8 + tid] += ph[tid];
+  if (p.phase_sample && bd.instance == 0 && bd.inst_block == 0 && tid < 8) p.phase_sample[tid] = ph[tid];
   if (warp == 1 && lane == 0) {
     // max_local_infeasibility over iterations 1..stop_at: the check warp saw
     // iterations up to the compute warps' last one, last - kLag <= stop_at <= last

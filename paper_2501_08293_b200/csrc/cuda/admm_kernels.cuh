@@ -10,6 +10,7 @@
 namespace dopf::cuda {
 
 constexpr int kCtlWords = 64;
+constexpr int kSampleEvery = 32;  // phase-timing sample period (iterations)
 constexpr int kTimelineT0 = 100, kTimelineIters = 64;  // iterations stamped by the timeline
 constexpr int kSlotRing = 4;   // residual-slot ring depth (admm_kernels.cu)
 // Decision lag: the compute warps act on the stop test of t - kLag at
@@ -47,6 +48,8 @@ struct KernelParams {
   unsigned long long* ctl;    // [instances][kCtlWords]: slot counter, decision seq, decision ring
   double* trace;        // [instances][trace_stride][6] (may be null)
   long long* prof;      // [blocks][8] phase cycle counters (null: off)
+  long long* phase_sample;  // [8] phase cycles of block 0 of instance 0, every kSampleEvery-th iteration
+                            // (always on; the solve's PhaseTimings split)
   unsigned long long* timeline;  // [blocks][kTimelineIters][3] globaltimer stamps (null: off)
   int32_t* iters;       // [instances]
   int32_t* status;      // [instances] 0 converged, 1 iteration limit

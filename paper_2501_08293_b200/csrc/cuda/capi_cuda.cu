@@ -81,6 +81,7 @@ struct dopf_cuda_ctx {
   int32_t *d_iters = nullptr, *d_status = nullptr;
   double *d_maxinf = nullptr, *d_obj = nullptr;
   int32_t* d_ties = nullptr;  // [instances][2] near-tie count, first near tie
+  long long* d_phase = nullptr;  // [8] sampled phase cycles of block 0 (PhaseTimings)
   double* d_trace = nullptr;
   std::size_t trace_cap = 0;  // doubles
   // cached layout plans (structure only), reused while the structure repeats
@@ -203,8 +204,8 @@ struct dopf_cuda_ctx {
     return static_cast<T*>(ensure(slot, count * sizeof(T)));
   }
 
-  void* small_stage() {  // 64 pinned bytes for packed scalar results
-    if (!h_small) ck(cudaMallocHost(&h_small, 64), "cudaMallocHost");
+  void* small_stage() {  // 256 pinned bytes for packed scalar results
+    if (!h_small) ck(cudaMallocHost(&h_small, 256), "cudaMallocHost");
     return h_small;
   }
 
@@ -304,6 +305,7 @@ void upload_layout(dopf_cuda_ctx* c) {
   c->d_maxinf = c->scratch<double>(k++, I);
   c->d_obj = c->scratch<double>(k++, I);
   c->d_ties = c->scratch<int32_t>(k++, 2 * I);
+  c->d_phase = c->scratch<long long>(k++, 8);
   ck(cudaStreamSynchronize(c->stream), "upload sync");
 }
 
@@ -354,6 +356,24 @@ void finish_upload(dopf_cuda_ctx* c) {
   c->uploaded = true;
 }
 
+// PhaseTimings (reference admm.hpp:104-106, measured at admm.cpp:182-217) of
+// a resident solve: the loop's device time split by the phase clock that
+// block 0 samples every kSampleEvery-th iteration -- local = consensus target
+// + GEMV (admm.cpp:131-138), dual = dual update + exchange value
+// (admm.cpp:140-143), global = column updates incl. the neighbour wait
+// (admm.cpp:118-129). The equality check runs on its own warp, beside them.
+void resident_timings(dopf_result_view& r, const long long* ph, double total_s) {
+  double sum = 0;
+  for (int q = 0; q < 6; ++q) sum += static_cast<double>(ph[q]);
+  if (!(sum > 0)) {
+    r.time_global = r.time_local = r.time_dual = 0.0;
+    return;
+  }
+  r.time_local = total_s * static_cast<double>(ph[0] + ph[1]) / sum;
+  r.time_dual = total_s * static_cast<double>(ph[2]) / sum;
+  r.time_global = total_s * static_cast<double>(ph[3] + ph[4] + ph[5]) / sum;
+}
+
 // Runs the kernel; copies scalars (and optionally vectors/trace) back.
 // Results of a single-instance solve (the resident path's common case).
 void finish_single(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view& r, bool copy_vectors,
@@ -368,6 +388,8 @@ void finish_single(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view& r
   ++c->kernels;
   double* scal = static_cast<double*>(c->small_stage());
   ck(cudaMemcpyAsync(scal, d_res + 2 * R, 6 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  long long* ph = reinterpret_cast<long long*>(scal + 8);
+  ck(cudaMemcpyAsync(ph, c->d_phase, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream), "d2h");
   if (copy_vectors) {
     const InstDesc& id = L.inst[0];
     if (r.x)
@@ -389,7 +411,7 @@ void finish_single(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view& r
   r.near_ties = static_cast<int32_t>(scal[4]);
   r.first_near_tie = static_cast<int32_t>(scal[5]);
   r.time_solve = c->last_kernel_s;
-  r.time_global = r.time_local = r.time_dual = 0.0;
+  resident_timings(r, ph, c->last_kernel_s);
   if (r.trace && r.iterations > 0) {
     ck(cudaMemcpyAsync(r.trace, c->d_trace, static_cast<std::size_t>(r.iterations) * 6 * sizeof(double),
                        cudaMemcpyDeviceToHost, c->stream),
@@ -476,6 +498,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.maxinf = c->d_maxinf;
   p.objective = c->d_obj;
   p.ties = c->d_ties;
+  p.phase_sample = c->d_phase;
   p.rho = s->rho;
   p.rho_inv = rho_reciprocal(s->rho);
   p.eps_rel = s->eps_rel;
@@ -513,6 +536,8 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   ck(cudaMemcpy(maxinf.data(), c->d_maxinf, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
   ck(cudaMemcpy(obj.data(), c->d_obj, I * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
   ck(cudaMemcpy(ties.data(), c->d_ties, 2 * I * sizeof(int32_t), cudaMemcpyDeviceToHost), "d2h");
+  long long ph[8];
+  ck(cudaMemcpy(ph, c->d_phase, sizeof ph, cudaMemcpyDeviceToHost), "d2h");
   bool any_vec = false;
   for (int i = 0; i < count; ++i)
     any_vec = any_vec || results[i].x || results[i].z || results[i].lambda;
@@ -561,7 +586,7 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
     r.near_ties = ties[2 * i];
     r.first_near_tie = ties[2 * i + 1];
     r.time_solve = c->last_kernel_s;
-    r.time_global = r.time_local = r.time_dual = 0.0;
+    resident_timings(r, ph, c->last_kernel_s);  // instance 0's split (same kernel for all)
     if (copy_vectors && any_vec) {
       if (r.x) std::memcpy(r.x, xall + id.x_off, sizeof(double) * id.n);
       const std::size_t base = 0;
@@ -641,6 +666,23 @@ bool needs_streaming(const dopf_model_view& m, const LayoutOptions& opt) {
     bytes += 8.0 * (n * n + m.m_s[s] * n);
   }
   return bytes > 0.8 * static_cast<double>(opt.max_blocks) * static_cast<double>(opt.smem_limit);
+}
+
+// PhaseTimings of a streaming solve: the loop's device time split by the
+// %globaltimer stamps of the kernels -- global = the boundary-column kernel
+// (admm.cpp:118-129, interior columns run inside the chunk kernels), local =
+// the chunk kernels, whose local update and dual update (admm.cpp:131-143)
+// are one fused pass per row, so the dual share is reported inside local.
+// (Partitioned: the exchange sits between them and counts in neither.)
+void stream_timings(dopf_result_view& r, const StreamCtl& h, double total_s) {
+  const double g = static_cast<double>(h.t_global), l = static_cast<double>(h.t_local);
+  r.time_dual = 0.0;
+  if (!(g + l > 0)) {
+    r.time_global = r.time_local = 0.0;
+    return;
+  }
+  r.time_global = total_s * g / (g + l);
+  r.time_local = total_s * l / (g + l);
 }
 
 void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, int part = 0,
@@ -887,7 +929,7 @@ void run_stream(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r, b
   r->near_ties = ctl.ties;
   r->first_near_tie = ctl.first_tie;
   r->time_solve = c->last_kernel_s;
-  r->time_global = r->time_local = r->time_dual = 0.0;
+  stream_timings(*r, ctl, c->last_kernel_s);
   if (vectors && !direct) {
     const std::size_t R = static_cast<std::size_t>(L.rows);
     double* st = static_cast<double*>(c->stage((2 * R + L.cols) * sizeof(double)));
@@ -1384,6 +1426,7 @@ void part_results(dopf_cuda_ctx* c, dopf_result_view* r, uint8_t* x_mask, uint8_
     r->near_ties = h.ties;
     r->first_near_tie = h.first_tie;
     r->time_solve = c->last_kernel_s;
+    stream_timings(*r, h, c->last_kernel_s);
     const std::size_t R = static_cast<std::size_t>(L.rows);
     // through the context's page-locked staging buffer (DMA speed), then
     // scattered to reference order on the host

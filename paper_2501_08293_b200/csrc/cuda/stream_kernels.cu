@@ -105,9 +105,23 @@ __device__ __forceinline__ void finalize_iteration(const StreamParams& p, const 
   }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// PhaseTimings stamps: one thread of the first CTA of each kernel
+__device__ __forceinline__ void stamp_chunks_start(StreamCtl* ctl) {
+  const unsigned long long now = gtimer();
+  ctl->t_global += static_cast<long long>(now - ctl->g0);
+  ctl->c0 = now;
+}
+
 __global__ void __launch_bounds__(kStreamRows, 4) k_global(const StreamParams p) {
   __shared__ double sh[8];
   if (p.ctl->done) return;  // partitioned loops may run past the stop (lazy host check)
+  if (blockIdx.x == 0 && threadIdx.x == 0) p.ctl->g0 = gtimer();
   const int c = blockIdx.x * kStreamRows + threadIdx.x;
   double o[1] = {0.0};
   if (c < p.bcols) {
@@ -322,6 +336,7 @@ __device__ void arrive_and_finish(const StreamParams& p, double* red, bool* last
       for (int k = 1; k < W; ++k) w[q] = q == 5 ? sel_max(w[q], red[q * W + k]) : w[q] + red[q * W + k];
     }
     *p.final_count = 0;  // ready for the next iteration (kernel boundary orders it)
+    p.ctl->t_local += static_cast<long long>(gtimer() - p.ctl->c0);
     if (p.partials_out) {  // partitioned: the host combines ranks, then calls k_decide
 #pragma unroll
       for (int q = 0; q < 7; ++q) p.partials_out[q] = w[q];
@@ -339,6 +354,7 @@ __global__ void __launch_bounds__(kStreamRows, 2) k_local(const StreamParams p) 
   __shared__ ChunkHead hsh;
   __shared__ bool lastflag;
   if (p.ctl->done) return;
+  if (p.n_staged == 0 && blockIdx.x == 0 && threadIdx.x == 0) stamp_chunks_start(p.ctl);
   const StreamChunk ch = p.chunks[p.big_ids[blockIdx.x]];
   const unsigned char* img = p.blob + ch.image_off;
   if (threadIdx.x < sizeof(ChunkHead) / 4)
@@ -424,6 +440,7 @@ __global__ void __launch_bounds__(kStagedThreads, kCtasPerSm) k_staged(const Str
   __shared__ bool lastflag;
   if (p.ctl->done) return;
   const int tid = threadIdx.x;
+  if (tid == 0 && blockIdx.x == 0) stamp_chunks_start(p.ctl);
   if (tid == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);

@@ -18,6 +18,11 @@ struct StreamCtl {      // device-side loop state
   double objective;     // c'x of the last iteration
   int32_t ties;         // near-tie stop tests so far (stop_test.cuh)
   int32_t first_tie;    // first of them (0: none)
+  // PhaseTimings stamps (%globaltimer, ns): start of this iteration's column
+  // kernel and chunk kernels; accumulated global (boundary columns) and local
+  // (chunk kernels: target, GEMV, dual, interior columns) time
+  unsigned long long g0, c0;
+  long long t_global, t_local;
 };
 
 constexpr int kStagedThreads = kStagedRows + 32;  // compute warps + 1 producer warp

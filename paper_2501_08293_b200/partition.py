@@ -199,7 +199,8 @@ class PartitionedSolver:
                                                   zm.ctypes.data_as(C.POINTER(C.c_uint8))))
         it = r.iterations
         res = dopf.SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
-                               tr[:it].copy() if trace else np.zeros((0, 6)), {"solve": r.time_solve},
+                               tr[:it].copy() if trace else np.zeros((0, 6)), {"solve": r.time_solve, "global": r.time_global, "local": r.time_local,
+                            "dual": r.time_dual},
                                r.near_ties, r.first_near_tie)
         res.x_mask, res.z_mask = xm.astype(bool), zm.astype(bool)
         return res
@@ -258,7 +259,8 @@ def _result(r, bufs):
     x, z, lam, xm, zm, tr = bufs
     it = r.iterations
     res = dopf.SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
-                           tr[:it].copy() if tr is not None else np.zeros((0, 6)), {"solve": r.time_solve},
+                           tr[:it].copy() if tr is not None else np.zeros((0, 6)), {"solve": r.time_solve, "global": r.time_global, "local": r.time_local,
+                            "dual": r.time_dual},
                            r.near_ties, r.first_near_tie)
     res.x_mask, res.z_mask = xm.astype(bool), zm.astype(bool)
     return res
