@@ -205,6 +205,52 @@ def auto_cpu_iters(models, workers, settings_kw, target_s=12.0):
     return max(20, min(50000, int(per_scen * target_s)))
 
 
+def cpu_model() -> str:
+    """Host CPU model name (/proc/cpuinfo, as lscpu prints it)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+NCU_TARGETS = {"ieee8500": ("ieee8500", 8500), "ieee123": ("ieee123", 123), "ieee13": ("ieee13", 13)}
+
+
+def ncu_traffic(config: str):
+    """DRAM bytes (read + write) of one launch of the resident kernel,
+    measured now: ncu on tools/ncu_target.py (the same model, one warm-up
+    launch skipped). None when ncu is missing or the capture fails."""
+    if config not in NCU_TARGETS or os.environ.get("DOPF_BENCH_NO_NCU"):
+        return None, "skipped"
+    ncu = "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    shape, seed = NCU_TARGETS[config]
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+           "-k", "regex:admm_persistent", "-s", "1", "-c", "1", "--csv", "--print-units", "base",
+           sys.executable, os.path.join(ROOT, "tools", "ncu_target.py"), shape, str(seed), "2"]
+    try:
+        out = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                             timeout=240).stdout
+    except Exception as e:  # noqa: BLE001
+        return None, f"ncu failed: {type(e).__name__}"
+    import csv
+    tot, seen = 0.0, 0
+    for row in csv.reader(line for line in out.splitlines() if "dram__bytes_" in line):
+        if len(row) >= 2 and row[-3 if len(row) >= 3 else 0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            try:
+                tot += float(row[-1].replace(",", ""))
+                seen += 1
+            except ValueError:
+                pass
+    return (tot if seen == 2 else None), ("ncu live capture (dram__bytes_read.sum + dram__bytes_write.sum, "
+                                          "one launch)" if seen == 2 else "ncu output unparsed")
+
+
 def read_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -234,8 +280,13 @@ def run_reference(args, rank, world):
         tot_it += it
         tot_t += dt
     value = tot_it / tot_t
-    what = (f"{iters} ADMM iterations of each of {n} scenarios (one thread per scenario)"
-            if n > 1 else f"{iters} ADMM iterations of the {args.config} solve (WorkerPool of {workers} threads)")
+    per_step = tot_it / max(1, args.steps)
+    if n > 1:
+        what = (f"{per_step:.0f} ADMM iterations over {n} scenarios (one thread per scenario, each "
+                f"capped at {iters} iterations)")
+    else:
+        what = (f"{per_step:.0f} ADMM iterations of the {args.config} solve (WorkerPool of {workers} "
+                f"threads; cap {iters}" + (", the solve stops at convergence first)" if per_step < iters else ")"))
     line = {
         "impl": "reference",
         "metric": metric_name(args),
@@ -244,6 +295,7 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_of(args, world),
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": workers, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": what + " per step; C++ oracle restating admm.cpp:172-244"},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -526,14 +578,19 @@ def main():
     peak, peak_kind = read_peaks()
     kernel_avg = tot_t / args.steps
     achieved = b_iter * (sum(iters) / args.steps) / kernel_avg / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as fh:
-                traffic = json.load(fh).get(args.config)
-        except Exception:
-            traffic = None
+    traffic, traffic_src = (None, "not measured (N > 1)")
+    if rank == 0 and world == 1:
+        traffic, traffic_src = ncu_traffic(args.config)
+    if traffic is None:
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            try:
+                with open(tp) as fh:
+                    traffic = json.load(fh).get(args.config)
+                if traffic is not None:
+                    traffic_src += "; committed profiles/ncu_traffic.json (ncu --set full of the same command)"
+            except Exception:
+                traffic = None
     last_its, last_status = per_step[-1][0], per_step[-1][1]
 
     if rank == 0:
@@ -555,8 +612,8 @@ def main():
             "gpu_launches": int(kernels),
             "graph_or_kernel_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "bytes_per_iteration": b_iter,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_kind": peak_kind, "bytes_per_iteration": b_iter,
                          "traffic_per": "launch" if info["sync"] != "stream-graph" else "iteration",
                          "note": "algorithmic bytes (DESIGN.md s4) x iterations / kernel time; " +
                                  ("operators are staged in shared memory once per launch, so "
@@ -580,8 +637,14 @@ def main():
             cps, cit, cdt, n = cpu_sample(models, kw, it_n, cores)
             what = (f"{it_n} ADMM iterations of each of {n} scenarios, one thread per scenario"
                     if n > 1 else f"{cit} ADMM iterations of the {args.config} solve, {cores} threads")
+            # the same sample on ONE thread (workers = 1 figure), bounded to ~4 s
+            one_n = max(5, int(it_n * min(1.0, 4.0 / max(cdt * cores, 1e-9)))) if n == 1 else it_n
+            c1, c1it, c1dt, _ = cpu_sample(models[:1], kw, one_n, 1)
             line["cpu_baseline"] = {"value": cps, "unit": "iter/s", "cores": cores, "kind": "port",
-                                    "sample": f"{what} ({cdt:.1f} s, C++ oracle)"}
+                                    "cpu_model": cpu_model(),
+                                    "value_1_thread": c1,
+                                    "sample": f"{what} ({cdt:.1f} s, C++ oracle); 1-thread figure: {c1it} "
+                                              f"iterations of one instance ({c1dt:.1f} s)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as td

@@ -70,6 +70,34 @@ int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
 int dopf_cuda_precompute(dopf_cuda_ctx* ctx, const dopf_model_view* model, double* P, double* v,
                          int32_t* first_singular);
 
+/* Decomposition finish + one-time operators of MANY models on the GPU
+ * (SURVEY row f2): row_reduce of every subsystem's equality rows (reference
+ * decompose.cpp:48-98, reduce_subsystems :175-199) and then P_s, v_s of the
+ * reduced rows (admm.cpp:31-88), one launch per stage over every subsystem of
+ * every model -- bitwise identical to dopf_model_reduce + dopf_model_precompute
+ * on the host. models[k] are UNREDUCED views (a partitioned model, has_pre 0).
+ * Outputs are the concatenation over k (caller-allocated, in model order):
+ *   A  sum_k a_offsets_k[S_k] doubles: the reduced m'_s x n_s rows of s at
+ *      the start of its unreduced slot a_offsets_k[s]
+ *   b  sum_k b_offsets_k[S_k]: the reduced rhs at the start of its slot
+ *   m  sum_k S_k: reduced row counts m'_s
+ *   P  sum_k sum_s n_s^2 (row-major n_s x n_s, as p_offsets)
+ *   v  sum_k N_z_k
+ * Feed them to dopf_model_set_reduced then dopf_model_set_operators.
+ * Errors as the host: 7 (infeasible) naming the first failing model /
+ * subsystem after the whole reduction, else 2 (singular). seconds[3]
+ * (optional): pack + upload, kernels (CUDA events), download + unpack. */
+typedef struct dopf_prepare_out {
+  double* A;
+  double* b;
+  int32_t* m;
+  double* P;
+  double* v;
+} dopf_prepare_out;
+int dopf_cuda_prepare(dopf_cuda_ctx* ctx, const dopf_model_view* models, int32_t count, double tol,
+                      dopf_prepare_out* out, int32_t* fail_model, int32_t* fail_subsystem,
+                      double* seconds);
+
 /* Post-solve certification on the GPU (reference oracle.cpp:10-43,
  * check_feasibility): ||A x - b||_inf over the centralized LP, bound
  * violation, worst row / column (first maximum, -1 if none) and c'x. */

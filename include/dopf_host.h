@@ -87,6 +87,19 @@ int dopf_model_precompute(dopf_model* m, int32_t workers);
  * n_s x n_s per subsystem, p_offsets order) and v (N_z); copy counts and the
  * CSR scatter are built here exactly as dopf_model_precompute does. */
 int dopf_model_set_operators(dopf_model* m, const double* P, const double* v);
+/* Feeder helpers the reference exposes (feeder.hpp:104-110, lp_builder.hpp:49):
+ * load coefficients {a, b, alpha, beta} of a canonical load kind
+ * (0 constant power, 1 constant current, 2 constant impedance), and a line's
+ * voltage-drop sensitivities M^p, M^q (np x np row-major; r, x likewise;
+ * phases ascending, a subset of {1, 2, 3}). */
+int dopf_derive_load_coefficients(double p_ref, double q_ref, int32_t kind, double* out);
+int dopf_line_m_matrices(int32_t np, const int32_t* phases, const double* r, const double* x,
+                         double* mp, double* mq);
+/* Replaces every subsystem's rows by reduced ones laid out in the model's
+ * CURRENT (unreduced) slots: the first m_s[s] x n_s of A's slot s, the first
+ * m_s[s] of b's (the output of dopf_cuda_prepare); the GPU-side equivalent
+ * of dopf_model_reduce. Drops precomputed operators. */
+int dopf_model_set_reduced(dopf_model* m, const double* A, const double* b, const int32_t* m_s);
 int dopf_model_view_get(const dopf_model* m, dopf_model_view* out);
 int dopf_model_component_id(const dopf_model* m, int32_t s, char* buf, size_t cap);
 int dopf_model_rows_before_reduction(const dopf_model* m, int32_t* out /* S */);

@@ -33,6 +33,10 @@ class ModelView_t(C.Structure):
                 ("x_hi", P(f64)), ("x0", P(f64)), ("z0", P(f64))]
 
 
+class PrepareOut_t(C.Structure):
+    _fields_ = [("A", P(f64)), ("b", P(f64)), ("m", P(i32)), ("P", P(f64)), ("v", P(f64))]
+
+
 class ResultView_t(C.Structure):
     _fields_ = [("x", P(f64)), ("z", P(f64)), ("lambda_", P(f64)), ("trace", P(f64)),
                 ("status", i32), ("iterations", i32), ("objective", f64),
@@ -111,6 +115,9 @@ def host() -> C.CDLL:
          P(f64), P(f64), P(f64), P(f64), P(i32), P(vp))
     _sig(lib, "dopf_model_precompute", C.c_int, vp, i32)
     _sig(lib, "dopf_model_set_operators", C.c_int, vp, P(f64), P(f64))
+    _sig(lib, "dopf_model_set_reduced", C.c_int, vp, P(f64), P(f64), P(i32))
+    _sig(lib, "dopf_derive_load_coefficients", C.c_int, f64, f64, i32, P(f64))
+    _sig(lib, "dopf_line_m_matrices", C.c_int, i32, P(i32), P(f64), P(f64), P(f64), P(f64))
     _sig(lib, "dopf_model_view_get", C.c_int, vp, P(ModelView_t))
     _sig(lib, "dopf_model_component_id", C.c_int, vp, i32, C.c_char_p, sz)
     _sig(lib, "dopf_model_rows_before_reduction", C.c_int, vp, P(i32))
@@ -146,6 +153,8 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_kernels_executed", i64, vp)
     _sig(lib, "dopf_cuda_set_path", C.c_int, vp, i32)
     _sig(lib, "dopf_cuda_precompute", C.c_int, vp, P(ModelView_t), P(f64), P(f64), P(i32))
+    _sig(lib, "dopf_cuda_prepare", C.c_int, vp, P(ModelView_t), i32, f64, P(PrepareOut_t), P(i32), P(i32),
+         P(f64))
     _sig(lib, "dopf_cuda_certify", C.c_int, vp, P(LpView_t), P(f64), P(Certificate_t))
     _sig(lib, "dopf_cuda_reconstruct", C.c_int, vp, P(ModelView_t), P(f64), P(f64), P(f64))
     _sig(lib, "dopf_cuda_timeline", C.c_int, vp, P(u64), i64)

@@ -612,6 +612,11 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
 
 }  // namespace
 
+namespace {
+int prepare_models(dopf_cuda_ctx* c, const dopf_model_view* ms, int count, double tol, bool reduce,
+                   dopf_prepare_out* out, int32_t* fail_model, int32_t* fail_subsystem, double* seconds);
+}  // namespace
+
 extern "C" {
 
 int dopf_cuda_create(int device, dopf_cuda_ctx** out) {
@@ -1162,59 +1167,21 @@ int dopf_cuda_solve_device(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result
 int dopf_cuda_precompute(dopf_cuda_ctx* c, const dopf_model_view* m, double* P, double* v,
                          int32_t* first_singular) {
   if (!c || !m || !P || !v) return DOPF_ERR_INVALID_ARGUMENT;
-  return guarded(c, [&] {
-    const int S = m->S;
-    if (first_singular) *first_singular = -1;
-    if (S == 0) return;
-    std::vector<int64_t> so(S);
-    int64_t scratch = 0;
-    for (int s = 0; s < S; ++s) {
-      const int64_t n = m->z_offsets[s + 1] - m->z_offsets[s], mm = m->m_s[s];
-      so[s] = scratch;
-      scratch += 2 * mm * mm + mm * n + mm;
-    }
-    auto dev = [&](const void* h, std::size_t bytes) {
-      void* d = nullptr;
-      ck(cudaMalloc(&d, std::max<std::size_t>(bytes, 16)), "cudaMalloc");
-      if (h && bytes) ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream), "h2d");
-      return d;
-    };
-    std::vector<void*> owned;
-    auto keep = [&](void* d) { owned.push_back(d); return d; };
-    try {
-      PrecomputeParams p{};
-      p.S = S;
-      p.z_offsets = static_cast<int32_t*>(keep(dev(m->z_offsets, (S + 1) * sizeof(int32_t))));
-      p.m_s = static_cast<int32_t*>(keep(dev(m->m_s, S * sizeof(int32_t))));
-      p.a_offsets = static_cast<int64_t*>(keep(dev(m->a_offsets, (S + 1) * sizeof(int64_t))));
-      p.A = static_cast<double*>(keep(dev(m->A, m->a_offsets[S] * sizeof(double))));
-      p.b_offsets = static_cast<int32_t*>(keep(dev(m->b_offsets, (S + 1) * sizeof(int32_t))));
-      p.b = static_cast<double*>(keep(dev(m->b, m->b_offsets[S] * sizeof(double))));
-      p.p_offsets = static_cast<int64_t*>(keep(dev(m->p_offsets, (S + 1) * sizeof(int64_t))));
-      p.scratch_offsets = static_cast<int64_t*>(keep(dev(so.data(), S * sizeof(int64_t))));
-      p.scratch = static_cast<double*>(keep(dev(nullptr, scratch * sizeof(double))));
-      p.P = static_cast<double*>(keep(dev(nullptr, m->p_offsets[S] * sizeof(double))));
-      p.v = static_cast<double*>(keep(dev(nullptr, m->N_z * sizeof(double))));
-      p.singular = static_cast<int32_t*>(keep(dev(nullptr, S * sizeof(int32_t))));
-      ck(launch_precompute(p, c->stream), "precompute launch");
-      std::vector<int32_t> sing(S);
-      ck(cudaMemcpyAsync(P, p.P, m->p_offsets[S] * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
-      ck(cudaMemcpyAsync(v, p.v, m->N_z * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
-      ck(cudaMemcpyAsync(sing.data(), p.singular, S * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream), "d2h");
-      ck(cudaStreamSynchronize(c->stream), "precompute");
-      ++c->kernels;
-      for (void* d : owned) cudaFree(d);
-      owned.clear();
-      for (int s = 0; s < S; ++s)
-        if (sing[s]) {
-          if (first_singular) *first_singular = s;
-          throw SingularFailure("numerically singular subsystem #" + std::to_string(s));
-        }
-    } catch (...) {
-      for (void* d : owned) cudaFree(d);
-      throw;
-    }
-  });
+  if (first_singular) *first_singular = -1;
+  dopf_prepare_out out{nullptr, nullptr, nullptr, P, v};
+  int32_t fm = -1, fs = -1;
+  const int rc = prepare_models(c, m, 1, 0.0, false, &out, &fm, &fs, nullptr);
+  if (rc == DOPF_ERR_SINGULAR && first_singular) *first_singular = fs;
+  return rc;
+}
+
+int dopf_cuda_prepare(dopf_cuda_ctx* c, const dopf_model_view* models, int32_t count, double tol,
+                      dopf_prepare_out* out, int32_t* fail_model, int32_t* fail_subsystem,
+                      double* seconds) {
+  if (!c || !models || count < 1 || !out || !out->A || !out->b || !out->m || !out->P || !out->v ||
+      !(tol >= 0))
+    return DOPF_ERR_INVALID_ARGUMENT;
+  return prepare_models(c, models, count, tol, true, out, fail_model, fail_subsystem, seconds);
 }
 
 }  // extern "C"
@@ -1236,6 +1203,177 @@ struct Owned {
     for (void* d : p) cudaFree(d);
   }
 };
+
+// Batched row reduction + operators over every subsystem of `count` models
+// (precompute_kernels.cu): inputs packed into one pinned staging buffer and
+// copied once, two launches, outputs copied once into the caller's
+// concatenated arrays. Errors as the host: the first infeasible subsystem
+// (model order, then subsystem order) after the whole reduction, else the
+// first singular one.
+int prepare_models(dopf_cuda_ctx* c, const dopf_model_view* ms, int count, double tol, bool reduce,
+                   dopf_prepare_out* out, int32_t* fail_model, int32_t* fail_subsystem, double* seconds) {
+  if (fail_model) *fail_model = -1;
+  if (fail_subsystem) *fail_subsystem = -1;
+  int32_t code_model = -1, code_sub = -1, code = 0;
+  const int rc = guarded(c, [&] {
+    using clock = std::chrono::steady_clock;
+    const auto t0 = clock::now();
+    std::vector<PrepSub> subs;
+    std::vector<int32_t> sub_model, sub_index;
+    int64_t na = 0, nb = 0, np = 0, nz = 0, red_words = 0, prj_words = 0, big_words = 0;
+    const int64_t smem_cap = c->smem_optin / static_cast<int64_t>(sizeof(double)) - 16;
+    for (int k = 0; k < count; ++k) {
+      const dopf_model_view& m = ms[k];
+      if (m.S < 0 || (m.S > 0 && (!m.z_offsets || !m.m_s || !m.a_offsets || !m.b_offsets)))
+        throw std::invalid_argument("bad model view");
+      for (int s = 0; s < m.S; ++s) {
+        PrepSub d{};
+        d.m = m.m_s[s];
+        d.n = m.z_offsets[s + 1] - m.z_offsets[s];
+        if (d.m < 0 || d.n < 0 || m.a_offsets[s + 1] - m.a_offsets[s] != static_cast<int64_t>(d.m) * d.n)
+          throw std::invalid_argument("inconsistent subsystem sizes");
+        d.a_off = na + m.a_offsets[s];
+        d.b_off = nb + m.b_offsets[s];
+        d.p_off = np;
+        d.v_off = nz + m.z_offsets[s];
+        np += static_cast<int64_t>(d.n) * d.n;
+        const int64_t rw = reduce ? reduce_words(d.m, d.n) : 0, pw = project_words(d.m, d.n);
+        red_words = std::max(red_words, rw);
+        prj_words = std::max(prj_words, pw);
+        subs.push_back(d);
+        sub_model.push_back(k);
+        sub_index.push_back(s);
+      }
+      na += m.S ? m.a_offsets[m.S] : 0;
+      nb += m.S ? m.b_offsets[m.S] : 0;
+      nz += m.N_z;
+    }
+    const int64_t S = static_cast<int64_t>(subs.size());
+    if (S == 0) return;
+    if (S > 0x7fffffff) throw std::invalid_argument("too many subsystems");
+    // subsystems beyond shared memory: every subsystem on global scratch
+    const bool global_work = std::max(red_words, prj_words) > smem_cap;
+    std::vector<int64_t> woff;
+    if (global_work) {
+      woff.resize(S);
+      for (int64_t q = 0; q < S; ++q) {
+        woff[q] = big_words;
+        big_words += std::max(reduce ? reduce_words(subs[q].m, subs[q].n) : 0,
+                              project_words(subs[q].m, subs[q].n));
+      }
+    }
+    // pinned staging: [A | b] in, [A | b | rank | status | P | v] out
+    const std::size_t in_bytes = (na + nb) * sizeof(double);
+    const std::size_t out_bytes = (na + nb + np + nz) * sizeof(double) + 2 * S * sizeof(int32_t);
+    auto* st = static_cast<unsigned char*>(c->stage(std::max(in_bytes, out_bytes)));
+    {
+      double* hA = reinterpret_cast<double*>(st);
+      double* hb = hA + na;
+      for (int k = 0; k < count; ++k) {
+        const dopf_model_view& m = ms[k];
+        if (!m.S) continue;
+        const int64_t a = m.a_offsets[m.S], b = m.b_offsets[m.S];
+        if ((a && !m.A) || (b && !m.b)) throw std::invalid_argument("model view without A / b");
+        std::memcpy(hA, m.A, a * sizeof(double));
+        std::memcpy(hb, m.b, b * sizeof(double));
+        hA += a;
+        hb += b;
+      }
+    }
+    Owned o;
+    auto dalloc = [&](std::size_t bytes) {
+      void* d = nullptr;
+      ck(cudaMalloc(&d, std::max<std::size_t>(bytes, 16)), "cudaMalloc");
+      o.p.push_back(d);
+      return d;
+    };
+    PrepParams p{};
+    p.count = S;
+    p.tol = tol;
+    p.reduce = reduce ? 1 : 0;
+    auto* dsubs = static_cast<PrepSub*>(dalloc(S * sizeof(PrepSub)));
+    p.subs = dsubs;
+    p.A = static_cast<double*>(dalloc((na + nb) * sizeof(double)));
+    p.b = p.A + na;
+    p.rank = static_cast<int32_t*>(dalloc(2 * S * sizeof(int32_t)));
+    p.status = p.rank + S;
+    p.P = static_cast<double*>(dalloc((np + nz) * sizeof(double)));
+    p.v = p.P + np;
+    if (global_work) {
+      p.scratch = static_cast<double*>(dalloc(big_words * sizeof(double)));
+      auto* d = static_cast<int64_t*>(dalloc(S * sizeof(int64_t)));
+      ck(cudaMemcpyAsync(d, woff.data(), S * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream), "h2d");
+      p.scratch_off = d;
+    }
+    ck(cudaMemcpyAsync(dsubs, subs.data(), S * sizeof(PrepSub), cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaMemcpyAsync(p.A, st, in_bytes, cudaMemcpyHostToDevice, c->stream), "h2d");
+    if (!reduce) {
+      std::vector<int32_t> r(2 * S, 0);
+      for (int64_t q = 0; q < S; ++q) r[q] = subs[q].m;
+      ck(cudaMemcpyAsync(p.rank, r.data(), 2 * S * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream), "h2d");
+    }
+    ck(cudaEventRecord(c->ev0, c->stream), "event");
+    const auto t1 = clock::now();
+    if (reduce) {
+      ck(launch_row_reduce(p, global_work ? 0 : red_words, c->stream), "row_reduce launch");
+      ++c->kernels;
+      // the host reports infeasibility before computing any operator
+      std::vector<int32_t> stat(S);
+      ck(cudaMemcpyAsync(stat.data(), p.status, S * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      ck(cudaStreamSynchronize(c->stream), "row_reduce");
+      for (int64_t q = 0; q < S; ++q)
+        if (stat[q] == kPrepInfeasible) {
+          code = DOPF_ERR_INFEASIBLE;
+          code_model = sub_model[q];
+          code_sub = sub_index[q];
+          return;
+        }
+    }
+    ck(launch_project(p, global_work ? 0 : prj_words, c->stream), "project launch");
+    ++c->kernels;
+    ck(cudaEventRecord(c->ev1, c->stream), "event");
+    // one copy back: [A | b] (reduced in place), [P | v], [rank | status]
+    double* hA = reinterpret_cast<double*>(st);
+    double* hP = hA + na + nb;
+    auto* hr = reinterpret_cast<int32_t*>(hP + np + nz);
+    if (reduce) ck(cudaMemcpyAsync(hA, p.A, (na + nb) * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(hP, p.P, (np + nz) * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(hr, p.rank, 2 * S * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "prepare");
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, c->ev0, c->ev1);
+    const auto t2 = clock::now();
+    for (int64_t q = 0; q < S; ++q)
+      if (hr[S + q] == kPrepSingular) {
+        code = DOPF_ERR_SINGULAR;
+        code_model = sub_model[q];
+        code_sub = sub_index[q];
+        return;
+      }
+    if (reduce) {
+      std::memcpy(out->A, hA, na * sizeof(double));
+      std::memcpy(out->b, hA + na, nb * sizeof(double));
+      std::memcpy(out->m, hr, S * sizeof(int32_t));
+    }
+    std::memcpy(out->P, hP, np * sizeof(double));
+    std::memcpy(out->v, hP + np, nz * sizeof(double));
+    if (seconds) {
+      seconds[0] = std::chrono::duration<double>(t1 - t0).count();  // pack + upload issue
+      seconds[1] = kms * 1e-3;                                       // both kernels (events)
+      seconds[2] = std::chrono::duration<double>(clock::now() - t2).count() +
+                   std::max(0.0, std::chrono::duration<double>(t2 - t1).count() - kms * 1e-3);
+    }
+  });
+  if (rc != DOPF_OK) return rc;
+  if (code) {
+    if (fail_model) *fail_model = code_model;
+    if (fail_subsystem) *fail_subsystem = code_sub;
+    return fail(c, code, std::string(code == DOPF_ERR_INFEASIBLE ? "infeasible" : "numerically singular") +
+                             " subsystem #" + std::to_string(code_sub) + " of model " +
+                             std::to_string(code_model));
+  }
+  return DOPF_OK;
+}
 
 }  // namespace
 

@@ -304,6 +304,62 @@ int dopf_model_precompute(dopf_model* m, int32_t workers) {
   });
 }
 
+int dopf_derive_load_coefficients(double p_ref, double q_ref, int32_t kind, double* out) {
+  if (!out || kind < 0 || kind > 2) return fail(DOPF_ERR_INVALID_ARGUMENT, "bad load kind");
+  return guarded([&] {
+    const dopf::LoadCoefficients lc =
+        dopf::derive_load_coefficients(p_ref, q_ref, static_cast<dopf::LoadKind>(kind));
+    out[0] = lc.a;
+    out[1] = lc.b;
+    out[2] = lc.alpha;
+    out[3] = lc.beta;
+  });
+}
+
+int dopf_line_m_matrices(int32_t np, const int32_t* phases, const double* r, const double* x,
+                         double* mp, double* mq) {
+  if (np < 1 || np > 3 || !phases || !r || !x || !mp || !mq)
+    return fail(DOPF_ERR_INVALID_ARGUMENT, "bad line");
+  return guarded([&] {
+    dopf::LineSegment line;
+    line.phases = dopf::PhaseSet(std::vector<int>(phases, phases + np));
+    line.r.assign(np, std::vector<double>(np));
+    line.x.assign(np, std::vector<double>(np));
+    for (int i = 0; i < np; ++i)
+      for (int j = 0; j < np; ++j) {
+        line.r[i][j] = r[i * np + j];
+        line.x[i][j] = x[i * np + j];
+      }
+    std::vector<double> p, q;
+    dopf::build_m_matrices(line, p, q);
+    std::copy(p.begin(), p.end(), mp);
+    std::copy(q.begin(), q.end(), mq);
+  });
+}
+
+int dopf_model_set_reduced(dopf_model* m, const double* A, const double* b, const int32_t* m_s) {
+  if (!m || !m_s || (!A && m->model.subsystem_count() > 0)) return fail(DOPF_ERR_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    auto& subs = m->model.subsystems;
+    for (std::size_t s = 0; s < subs.size(); ++s)
+      if (m_s[s] < 0 || m_s[s] > subs[s].row_count())
+        throw std::invalid_argument("reduced row count of subsystem " + std::to_string(s) + " out of range");
+    std::size_t a_at = 0, b_at = 0;  // slots of the current (unreduced) rows
+    for (std::size_t s = 0; s < subs.size(); ++s) {
+      dopf::Subsystem& sub = subs[s];
+      const int rows = sub.row_count(), n = sub.col_count(), r = m_s[s];
+      dopf::Dense red(r, n);
+      for (int k = 0; k < r * n; ++k) red.a[k] = A[a_at + k];
+      sub.b.assign(b + b_at, b + b_at + r);
+      sub.A = std::move(red);
+      a_at += static_cast<std::size_t>(rows) * n;
+      b_at += rows;
+    }
+    m->flat_ready = false;
+    m->has_pre = false;
+  });
+}
+
 int dopf_model_set_operators(dopf_model* m, const double* P, const double* v) {
   if (!m || !P || !v) return fail(DOPF_ERR_INVALID_ARGUMENT, "null argument");
   return guarded([&] {

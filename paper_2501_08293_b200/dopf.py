@@ -65,6 +65,19 @@ def _raise(code: int, msg: str):
     raise RuntimeError(msg)
 
 
+def _release(obj, free_name: str) -> None:
+    """Frees a native handle once. Safe during interpreter shutdown, when
+    module globals (the native library bindings) may already be gone."""
+    h = getattr(obj, "_h", None)
+    obj._h = None
+    if h is None or not h.value:
+        return
+    try:
+        getattr(N.host(), free_name)(h)
+    except Exception:  # shutdown: the process is exiting, the OS reclaims it
+        pass
+
+
 def _check(code: int):
     if code != 0:
         _raise(code, N.last_error())
@@ -87,10 +100,7 @@ class Feeder:
         self._h = C.c_void_p(handle)
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value and N is not None:  # N is None at interpreter shutdown
-            N.host().dopf_feeder_free(h)
-            self._h = None
+        _release(self, "dopf_feeder_free")
 
     @property
     def handle(self):
@@ -176,10 +186,7 @@ class LinearSystem:
         self.rows, self.cols, self.nnz = v.rows, v.cols, v.nnz
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value and N is not None:
-            N.host().dopf_lp_free(h)
-            self._h = None
+        _release(self, "dopf_lp_free")
 
     @property
     def handle(self):
@@ -256,6 +263,29 @@ class LinearSystem:
         return text
 
 
+LOAD_KINDS = {"constant_power": 0, "constant_current": 1, "constant_impedance": 2}
+
+
+def derive_load_coefficients(p_ref: float, q_ref: float, kind: str) -> dict:
+    """Reference derive_load_coefficients (feeder.hpp:104-110)."""
+    out = (C.c_double * 4)()
+    _check(N.host().dopf_derive_load_coefficients(p_ref, q_ref, LOAD_KINDS[kind], out))
+    return {"a": out[0], "b": out[1], "alpha": out[2], "beta": out[3]}
+
+
+def line_m_matrices(phases, r, x):
+    """Reference build_m_matrices (lp_builder.cpp:275-296) of one line."""
+    ph = np.ascontiguousarray(phases, dtype=np.int32)
+    n = len(ph)
+    r = np.ascontiguousarray(r, dtype=np.float64).reshape(n, n)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(n, n)
+    mp, mq = np.zeros((n, n)), np.zeros((n, n))
+    dp = C.POINTER(C.c_double)
+    _check(N.host().dopf_line_m_matrices(n, ph.ctypes.data_as(C.POINTER(N.i32)), r.ctypes.data_as(dp),
+                                         x.ctypes.data_as(dp), mp.ctypes.data_as(dp), mq.ctypes.data_as(dp)))
+    return mp, mq
+
+
 def assemble_centralized(f: Feeder) -> LinearSystem:
     h = C.c_void_p()
     _check(N.host().dopf_lp_assemble(f.handle, C.byref(h)))
@@ -286,10 +316,7 @@ class DecomposedModel:
         self._view: Optional[N.ModelView_t] = None
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value and N is not None:
-            N.host().dopf_model_free(h)
-            self._h = None
+        _release(self, "dopf_model_free")
 
     @property
     def handle(self):
@@ -317,8 +344,11 @@ class DecomposedModel:
         P = np.zeros(int((ns * ns).sum()))
         vv = np.zeros(int(v.N_z))
         first = N.i32(-1)
-        solver._err(solver._lib.dopf_cuda_precompute(solver._h, C.byref(v), P.ctypes.data_as(C.POINTER(C.c_double)),
-                                                     vv.ctypes.data_as(C.POINTER(C.c_double)), C.byref(first)))
+        rc = solver._lib.dopf_cuda_precompute(solver._h, C.byref(v), P.ctypes.data_as(C.POINTER(C.c_double)),
+                                              vv.ctypes.data_as(C.POINTER(C.c_double)), C.byref(first))
+        if rc == 2 and first.value >= 0:
+            raise SingularSubsystemError(f"numerically singular subsystem '{self.component_id(first.value)}'")
+        solver._err(rc)
         _check(N.host().dopf_model_set_operators(self._h, P.ctypes.data_as(C.POINTER(C.c_double)),
                                                  vv.ctypes.data_as(C.POINTER(C.c_double))))
         self._view = None
@@ -432,6 +462,62 @@ def partition(ls: LinearSystem, f: Feeder) -> DecomposedModel:
     return DecomposedModel(h.value)
 
 
+def prepare_gpu(models: List["DecomposedModel"], solver: "CudaSolver", tol: float = 1e-9,
+                chunk: int = 512) -> dict:
+    """GPU equivalent of ``m.reduce(tol); m.precompute()`` for every model
+    (SURVEY row f2): row_reduce (reference decompose.cpp:48-98) and the
+    operators (admm.cpp:31-88) of all subsystems of `chunk` models per pair of
+    launches (dopf_cuda_prepare), bitwise equal to the host. `models` are
+    partitioned, unreduced models. Raises InfeasibleSubsystemError /
+    SingularSubsystemError naming the component like the host does. Returns
+    the summed {pack, kernels, unpack} seconds of the device calls."""
+    tot = {"pack_s": 0.0, "kernels_s": 0.0, "unpack_s": 0.0}
+    for c0 in range(0, len(models), chunk):
+        part = models[c0:c0 + chunk]
+        views = (N.ModelView_t * len(part))(*[m.view() for m in part])
+        na = nb = ns = npp = nz = 0
+        sizes = []
+        for v in views:
+            S = v.S
+            a = int(v.a_offsets[S]) if S else 0
+            b = int(v.b_offsets[S]) if S else 0
+            zo = np.ctypeslib.as_array(v.z_offsets, shape=(S + 1,)) if S else np.zeros(1, np.int32)
+            p2 = int((np.diff(zo).astype(np.int64) ** 2).sum())
+            sizes.append((a, b, S, p2, int(v.N_z)))
+            na, nb, ns, npp, nz = na + a, nb + b, ns + S, npp + p2, nz + int(v.N_z)
+        A, B = np.zeros(max(na, 1)), np.zeros(max(nb, 1))
+        Ms = np.zeros(max(ns, 1), dtype=np.int32)
+        Pp, V = np.zeros(max(npp, 1)), np.zeros(max(nz, 1))
+        out = N.PrepareOut_t(A.ctypes.data_as(C.POINTER(C.c_double)), B.ctypes.data_as(C.POINTER(C.c_double)),
+                             Ms.ctypes.data_as(C.POINTER(N.i32)), Pp.ctypes.data_as(C.POINTER(C.c_double)),
+                             V.ctypes.data_as(C.POINTER(C.c_double)))
+        fm, fs = N.i32(-1), N.i32(-1)
+        secs = (C.c_double * 3)()
+        rc = solver._lib.dopf_cuda_prepare(solver._h, views, len(part), tol, C.byref(out), C.byref(fm),
+                                           C.byref(fs), secs)
+        if rc == 7:
+            raise InfeasibleSubsystemError(
+                f"infeasible subsystem '{part[fm.value].component_id(fs.value)}': contradictory rows")
+        if rc == 2:
+            raise SingularSubsystemError(
+                f"numerically singular subsystem '{part[fm.value].component_id(fs.value)}'")
+        solver._err(rc)
+        tot["pack_s"] += secs[0]
+        tot["kernels_s"] += secs[1]
+        tot["unpack_s"] += secs[2]
+        a0 = b0 = s0 = p0 = z0 = 0
+        for m, (a, b, S, p2, n_z) in zip(part, sizes):
+            _check(N.host().dopf_model_set_reduced(
+                m.handle, A[a0:].ctypes.data_as(C.POINTER(C.c_double)),
+                B[b0:].ctypes.data_as(C.POINTER(C.c_double)), Ms[s0:].ctypes.data_as(C.POINTER(N.i32))))
+            _check(N.host().dopf_model_set_operators(
+                m.handle, Pp[p0:].ctypes.data_as(C.POINTER(C.c_double)),
+                V[z0:].ctypes.data_as(C.POINTER(C.c_double))))
+            m._view = None
+            a0, b0, s0, p0, z0 = a0 + a, b0 + b, s0 + S, p0 + p2, z0 + n_z
+    return tot
+
+
 def model_from_arrays(subsystems, c, x_lo, x_hi, is_w=None) -> DecomposedModel:
     """Build a model from dense subsystem data.
 
@@ -531,10 +617,13 @@ class CudaSolver:
         self.model: Optional[DecomposedModel] = None
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            self._lib.dopf_cuda_destroy(h)
-            self._h = None
+        h, self._h = getattr(self, "_h", None), None
+        lib = getattr(self, "_lib", None)
+        if h is not None and h.value and lib is not None:
+            try:
+                lib.dopf_cuda_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
 
     def _err(self, rc):
         if rc != 0:

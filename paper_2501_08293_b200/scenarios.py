@@ -31,16 +31,25 @@ def scenario_seed(seed: int, k: int) -> int:
     return seed * 1_000_003 + k
 
 
-def build_scenarios(shape: str, seed: int, indices, workers: int = 0) -> List["dopf.DecomposedModel"]:
-    """Decomposed + precomputed models of scenarios `indices` (host C++, threads)."""
+def build_scenarios(shape: str, seed: int, indices, workers: int = 0,
+                    gpu: "dopf.CudaSolver" = None) -> List["dopf.DecomposedModel"]:
+    """Decomposed + precomputed models of scenarios `indices`. Host C++ on
+    `workers` threads; with `gpu` (a CudaSolver) the threads only assemble and
+    partition, and the row reduction + operators of every scenario run in
+    batched launches on the device (dopf.prepare_gpu, bitwise equal)."""
     base = dopf.synthetic_feeder(shape, seed)
     workers = workers or (os.cpu_count() or 1)
 
     def one(k):
         f = dopf.scale_loads(base, scenario_seed(seed, k))
+        if gpu is not None:
+            return dopf.partition(dopf.assemble_centralized(f), f)
         _, _, m = dopf.load_model(f)
         m.precompute()
         return m
 
     with cf.ThreadPoolExecutor(max_workers=workers) as ex:
-        return list(ex.map(one, list(indices)))
+        models = list(ex.map(one, list(indices)))
+    if gpu is not None:
+        dopf.prepare_gpu(models, gpu)
+    return models
