@@ -66,7 +66,7 @@ namespace dopf::cuda {
 namespace {
 
 constexpr int kWarps = kThreads / 32;
-constexpr int kGemvH = kThreads > 512 ? 2 : 4;  // entries per row per GEMV step (K rows x kGemvH x 2 loads in flight)
+constexpr int kHoist = kThreads > 512 ? 4 : 8;  // operator loads in flight per row (register budget)
 constexpr int kCW = kComputeThreads;  // compute threads (warps 2..)
 constexpr int kSyncThreads = kCW + 32;  // service + compute warps (the check warp runs decoupled)
 constexpr int kSlots = kSlotRing;  // partial-slot ring (see header)
@@ -622,48 +622,34 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
       }
 
       // (L2) z = P t + v, one row per thread and slot k; P in sliced-ELL order
-      // (entry j of a warp's 32 rows is 256 contiguous bytes). The K rows of
-      // a thread advance together, kGemvH entries per step with every load of
-      // the step issued first: K independent sequential-j chains in flight, so
-      // a thread costs its longest row's chain (8-cycle DADD latency per
-      // entry), not the sum of its rows'. z^t goes to buffer t % 2, once the
-      // check warp is done with z^{t-2} there.
+      // (entry j of a warp's 32 rows is 256 contiguous bytes). Each row's
+      // loads are issued 8 at a time ahead of its sequential-j sum. z^t goes
+      // to buffer t % 2, once the check warp is done with z^{t-2} there.
       if (t >= 3) named_sync(kBarZFree + (t & 1), kCW + 32);
-      {
-        int nk[K], nmax = 0;
-        double acc[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          nk[k] = (ctid + k * kCW < bd.rows) ? row_n(rpk[k]) : 0;
-          nmax = nk[k] > nmax ? nk[k] : nmax;
-          acc[k] = 0.0;
-        }
-        for (int j0 = 0; j0 < nmax; j0 += kGemvH) {
-          double pv[K][kGemvH], tv[K][kGemvH];
+      for (int k = 0; k < K; ++k) {
+        const int r = ctid + k * kCW;
+        if (r < bd.rows) {
+          const int n = row_n(rpk[k]);
+          const double* pr = Pop + pofs[k];
+          const double* tb = tu + row_base(rpk[k]);
+          double acc = 0.0;
+          for (int j0 = 0; j0 < n; j0 += kHoist) {
+            double pv[kHoist], tv[kHoist];
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const double* pr = Pop + pofs[k];
-            const double* tb = tu + row_base(rpk[k]);
-#pragma unroll
-            for (int e = 0; e < kGemvH; ++e) {
-              pv[k][e] = 0.0;
-              tv[k][e] = 0.0;
-              if (j0 + e < nk[k]) {
-                pv[k][e] = pr[(j0 + e) * 32];
-                tv[k][e] = tb[j0 + e];
+            for (int e = 0; e < kHoist; ++e) {
+              pv[e] = 0.0;
+              tv[e] = 0.0;
+              if (j0 + e < n) {
+                pv[e] = pr[(j0 + e) * 32];
+                tv[e] = tb[j0 + e];
               }
             }
+#pragma unroll
+            for (int e = 0; e < kHoist; ++e)
+              if (j0 + e < n) acc = acc + pv[e] * tv[e];
           }
-#pragma unroll
-          for (int e = 0; e < kGemvH; ++e)
-#pragma unroll
-            for (int k = 0; k < K; ++k)
-              if (j0 + e < nk[k]) acc[k] = acc[k] + pv[k][e] * tv[k][e];
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int r = ctid + k * kCW;
-          if (r < bd.rows) zs[r] = acc[k] + vs[r];
+          zs[r] = acc + vs[r];
         }
       }
       named_arrive(kBarZReady + (t & 1), kCW + 32);  // z^t for the check warp

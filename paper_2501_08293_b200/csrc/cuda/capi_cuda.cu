@@ -344,6 +344,15 @@ LayoutOptions options_for(const dopf_cuda_ctx* c) {
   return o;
 }
 
+// Limits of the resident kernel a single-instance plan must meet (the same
+// ones finish_upload / choose_sync enforce), checked before any upload.
+void check_resident(const dopf_cuda_ctx* c, const InstancePlan& P) {
+  if (P.K > kMaxK) throw std::invalid_argument("model too large for the resident kernel");
+  if (P.max_neighbours > 32) throw std::invalid_argument("a block shares columns with more than 32 other blocks");
+  if (static_cast<int>(P.blocks.size()) > c->sm_count * ctas_per_sm())
+    throw std::invalid_argument("instance needs more CTAs than fit the GPU");
+}
+
 void finish_upload(dopf_cuda_ctx* c) {
   if (c->L.K > kMaxK)
     throw std::invalid_argument("model too large for the resident kernel (" +
@@ -1092,7 +1101,8 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
     const bool was_partitioned = c->partitioned;
     c->partitioned = false;
     if (was_partitioned) c->stream_maps = false;
-    if (c->streaming) {
+    auto stream_upload = [&] {
+      c->streaming = true;
       c->dev_plan = nullptr;
       c->L.reset();
       if (c->stream_maps && !c->partitioned && c->SL.same_structure(*m)) {
@@ -1104,9 +1114,11 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
       }
       c->L.bytes_per_iteration = c->SL.bytes_per_iteration;
       c->uploaded = true;
+    };
+    if (c->streaming) {
+      stream_upload();
       return;
     }
-    c->stream_maps = false;  // the map pointers are about to hold the resident plan's
     const bool same = c->plan && c->plan->same_structure(*m, opt);
     if (same && c->dev_plan == c->plan.get() && c->L.inst.size() == 1) {
       // fast path: structure and index maps already on the device; copy the
@@ -1115,7 +1127,22 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
       c->uploaded = true;
       return;
     }
-    if (!same) c->plan = std::make_shared<InstancePlan>(plan_instance(*m, choose_blocks(*m, opt), opt));
+    // the resident plan, checked against every limit of the resident kernel
+    // before any device state changes; the automatic path falls back to the
+    // streaming path when the model exceeds one (a forced resident path
+    // reports it as std::invalid_argument)
+    std::shared_ptr<InstancePlan> plan = same ? c->plan : nullptr;
+    try {
+      if (!plan) plan = std::make_shared<InstancePlan>(plan_instance(*m, choose_blocks(*m, opt), opt));
+      check_resident(c, *plan);
+    } catch (const std::invalid_argument& e) {
+      if (c->path_request != 0) throw;
+      if (std::getenv("DOPF_VERBOSE")) std::fprintf(stderr, "dopf: resident path unavailable (%s): streaming\n", e.what());
+      stream_upload();
+      return;
+    }
+    c->stream_maps = false;  // the map pointers are about to hold the resident plan's
+    c->plan = plan;
     c->L.reset();
     append_instance(c->L, *c->plan, *m);
     finish_upload(c);

@@ -167,3 +167,29 @@ def test_near_tie_flag_on_a_constructed_tie(solver):
     assert ref.first_near_tie == t0 and ref.near_ties >= 1, (t0, ref.first_near_tie, ref.iterations)
     assert gpu.first_near_tie == t0 and gpu.near_ties >= 1, (t0, gpu.first_near_tie, gpu.iterations)
     assert min(gpu.iterations, ref.iterations) >= t0
+
+
+def wide_subsystem_model(n=150, m=100, seed=5):
+    """One subsystem with n_s = 150 >= 128 columns: beyond the resident
+    kernel's packed row metadata, within a streaming chunk."""
+    rng = np.random.default_rng(seed)
+    a = rng.normal(size=(m, n))
+    b = a @ rng.normal(size=n)
+    lo = np.where(rng.random(n) < 0.5, -1.0, -INF)
+    hi = np.where(rng.random(n) < 0.5, 1.0, INF)
+    mdl = dopf.single_sub_model(a, b, rng.normal(size=n), lo, hi)
+    mdl.precompute()
+    return mdl
+
+
+def test_auto_path_falls_back_to_streaming_beyond_resident_limits():
+    m = wide_subsystem_model()
+    s = dopf.CudaSolver(0)
+    s.upload(m)  # auto: the resident plan is rejected, the streaming path takes it
+    assert s.info()["sync"] == "stream-graph"
+    st = dopf.Settings(max_iter=400)
+    assert_same(s.solve(st), O.solve(m, st), bitwise=True)
+    forced = dopf.CudaSolver(0)
+    forced.set_path("resident")
+    with pytest.raises(ValueError):
+        forced.upload(m)
