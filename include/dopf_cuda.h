@@ -61,6 +61,14 @@ int dopf_cuda_solve_batch(dopf_cuda_ctx* ctx, const dopf_settings* settings,
                           dopf_result_view* results, int32_t count);
 
 int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
+/* Parity mode (reference Settings::record_iterates, admm.cpp:228-229): the
+ * same solve, with the state after every iteration t = 1 .. min(T, stop)
+ * written by the device loop itself (one pass, not a re-run per t) and
+ * returned in reference order, n + 3 N_z doubles per iteration:
+ * [x | z | z_prev | lambda] (IterateSnapshot, admm.hpp:108-114). Single
+ * model on the resident path; code 1 otherwise. */
+int dopf_cuda_solve_snapshots(dopf_cuda_ctx* ctx, const dopf_settings* settings,
+                              dopf_result_view* result, double* snapshots, int32_t T);
 /* One-time operators on the GPU (reference admm.cpp:31-88, batched over all
  * subsystems): P (row-major n_s x n_s at p_offsets) and v (N_z) of the model
  * view's A, b -- bitwise identical to the host precompute (same sequential

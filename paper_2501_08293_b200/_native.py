@@ -153,6 +153,7 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_kernels_executed", i64, vp)
     _sig(lib, "dopf_cuda_set_path", C.c_int, vp, i32)
     _sig(lib, "dopf_cuda_precompute", C.c_int, vp, P(ModelView_t), P(f64), P(f64), P(i32))
+    _sig(lib, "dopf_cuda_solve_snapshots", C.c_int, vp, P(Settings_t), P(ResultView_t), P(f64), i32)
     _sig(lib, "dopf_cuda_prepare", C.c_int, vp, P(ModelView_t), i32, f64, P(PrepareOut_t), P(i32), P(i32),
          P(f64))
     _sig(lib, "dopf_cuda_certify", C.c_int, vp, P(LpView_t), P(f64), P(Certificate_t))

@@ -686,6 +686,24 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
           zp[k] = z;
         }
       }
+      if (p.snap != nullptr && t <= p.snap_iters) {
+        // parity mode (reference record_iterates, admm.cpp:228-229): the
+        // state after iteration t -- z^t, lambda^t by device row, x^t by
+        // column (owners)
+        double* sn = p.snap + static_cast<int64_t>(t - 1) * p.snap_stride;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int r = ctid + k * kCW;
+          if (r < bd.rows) {
+            sn[bd.row0 + r] = zp[k];
+            sn[p.rows_total + bd.row0 + r] = lam[k];
+          }
+        }
+        for (int c = ctid; c < bd.cols; c += kCW) {
+          const ColMeta cmc = p.cmeta[bd.col_off + c];
+          if (cmc.owner) sn[2 * p.rows_total + id.x_off + cmc.gcol] = xt[c];
+        }
+      }
       named_sync(kBarCompute, kCW);  // every u(t) in shared memory
       unsigned long long* tl = nullptr;
       if (p.timeline && ctid == 0 && t >= kTimelineT0 && t < kTimelineT0 + kTimelineIters) {

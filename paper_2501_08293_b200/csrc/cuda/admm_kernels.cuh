@@ -56,6 +56,11 @@ struct KernelParams {
   double* maxinf;       // [instances]
   double* objective;    // [instances]
   int32_t* ties;        // [instances][2] near-tie stop tests up to the stop, first one (stop_test.cuh)
+  double* snap;         // parity mode (null: off): per iteration t <= snap_iters, [z | lambda | x]
+                        // at snap + (t-1) * (2 rows_total + x_total): z, lambda by device row, x by column
+  int64_t snap_stride;
+  int32_t snap_iters;
+  int32_t snap_pad;
   double rho;
   double rho_inv;  // RN(1 / rho) for div_rho (div_rho.cuh)
   double eps_rel;

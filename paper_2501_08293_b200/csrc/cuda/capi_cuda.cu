@@ -88,6 +88,8 @@ struct dopf_cuda_ctx {
   std::shared_ptr<InstancePlan> plan, batch_plan;
   // HBM-streaming path (instances too large for shared-memory residency)
   int path_request = 0;      // 0 auto, 1 resident persistent kernel, 2 streaming graph
+  double* snap_dev = nullptr;  // parity mode: per-iteration snapshots of the next resident run (slot 118)
+  int snap_iters = 0;
   bool streaming = false;    // path of the uploaded model
   StreamLayout SL;
   struct StreamDev {
@@ -516,6 +518,9 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.max_iter = s->max_iter;
   p.blocks_per_instance = L.blocks_per_instance;
   p.sync_mode = static_cast<int32_t>(c->mode);
+  p.snap = c->snap_dev;
+  p.snap_stride = 2 * L.rows_total + L.x_total;
+  p.snap_iters = c->snap_dev ? c->snap_iters : 0;
 
   ck(cudaEventRecord(c->ev0, c->stream), "event");
   ck(launch_admm(p, c->num_blocks, L.K, L.smem_bytes, c->mode, c->cluster, L.all_ops_in_smem, c->stream),
@@ -742,7 +747,44 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.export_rows = c->put(k++, L.export_rows);
   d.send = c->scratch<double>(k++, L.xstride());  // [exports | partials] record of this rank
   k++;  // (slot of the former separate partial gather)
-  d.staged_ids = c->put(k++, L.staged_ids);
+  // chunk -> CTA assignment of the persistent staged kernel (CTA b takes
+  // positions b, b + G, b + 2G, ...): cost-aware, deterministic. Chunks are
+  // dealt in rounds of G, heaviest first, each round's heaviest chunk to the
+  // CTA with the least accumulated cost (cost = stage bytes + a per-chunk
+  // constant for the fixed phases). DOPF_STREAM_RR=1 keeps the walk order.
+  {
+    const int G = std::max(1, c->staged_grid);
+    std::vector<int32_t> ids = L.staged_ids;
+    if (!std::getenv("DOPF_STREAM_RR") && G > 1 && ids.size() > static_cast<std::size_t>(G)) {
+      std::vector<double> cost(ids.size());
+      for (std::size_t i = 0; i < ids.size(); ++i) {
+        StagePlan sp;
+        stage_plan(L.chunks[ids[i]], sp);
+        cost[i] = static_cast<double>(sp.total) + 8192.0;
+      }
+      std::vector<std::size_t> by_cost(ids.size());
+      for (std::size_t i = 0; i < ids.size(); ++i) by_cost[i] = i;
+      std::stable_sort(by_cost.begin(), by_cost.end(), [&](std::size_t a, std::size_t b) { return cost[a] > cost[b]; });
+      std::vector<double> load(G, 0.0);
+      std::vector<int> cta(G);
+      std::vector<int32_t> out(ids.size());
+      for (std::size_t r0 = 0, round = 0; r0 < ids.size(); r0 += G, ++round) {
+        const std::size_t cnt = std::min<std::size_t>(G, ids.size() - r0);
+        for (int b = 0; b < G; ++b) cta[b] = b;
+        // the last, partial round may only use CTAs whose position exists
+        std::stable_sort(cta.begin(), cta.end(), [&](int a, int b) { return load[a] < load[b]; });
+        if (cnt < static_cast<std::size_t>(G)) std::sort(cta.begin(), cta.begin() + cnt);
+        for (std::size_t j = 0; j < cnt; ++j) {
+          const int b = cnt < static_cast<std::size_t>(G) ? static_cast<int>(j) : cta[j];
+          const std::size_t i = by_cost[r0 + j];
+          out[round * G + b] = ids[i];
+          load[b] += cost[i];
+        }
+      }
+      ids.swap(out);
+    }
+    d.staged_ids = c->put(k++, ids);
+  }
   d.big_ids = c->put(k++, L.big_ids);
   d.imp_ptr = c->put(k++, L.imp_ptr);
   d.imp_slot = c->put(k++, L.imp_slot);
@@ -1188,6 +1230,45 @@ int dopf_cuda_solve_device(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result
   return guarded(c, [&] {
     if (c->streaming) run_stream(c, s, r, false);
     else run(c, s, r, 1, false);
+  });
+}
+
+int dopf_cuda_solve_snapshots(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* r,
+                              double* snaps, int32_t T) {
+  if (!c || !r || !snaps || T < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (c->streaming || c->partitioned || !c->dev_plan || c->L.inst.size() != 1)
+      throw std::invalid_argument("iterate snapshots need a single model on the resident path");
+    const InstancePlan& P = *c->dev_plan;
+    const int64_t R = c->L.rows_total, X = c->L.x_total;
+    const int64_t stride = 2 * R + X;
+    c->snap_dev = c->scratch<double>(118, static_cast<std::size_t>(T) * stride);
+    c->snap_iters = T;
+    struct Off {
+      dopf_cuda_ctx* c;
+      ~Off() { c->snap_dev = nullptr; }
+    } off{c};
+    run(c, s, r, 1, true);
+    const int rec = std::min<int>(T, r->iterations);
+    std::vector<double> dev(static_cast<std::size_t>(rec) * stride), z0(R);
+    ck(cudaMemcpy(dev.data(), c->snap_dev, dev.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    ck(cudaMemcpy(z0.data(), c->d_z0, R * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    // reference order: [x (n) | z (N_z) | z_prev (N_z) | lambda (N_z)] per iteration
+    const int64_t n = X, out = n + 3 * R;
+    std::vector<double> prev(R);
+    for (int64_t d = 0; d < R; ++d) prev[P.ref_of_dev[d]] = z0[d];
+    for (int t = 0; t < rec; ++t) {
+      const double* sn = dev.data() + static_cast<int64_t>(t) * stride;
+      double* o = snaps + static_cast<int64_t>(t) * out;
+      std::copy(sn + 2 * R, sn + 2 * R + n, o);
+      for (int64_t d = 0; d < R; ++d) {
+        const int32_t ref = P.ref_of_dev[d];
+        o[n + ref] = sn[d];
+        o[n + 2 * R + ref] = sn[R + d];
+      }
+      std::copy(prev.begin(), prev.end(), o + n + R);
+      std::copy(o + n, o + n + R, prev.begin());
+    }
   });
 }
 

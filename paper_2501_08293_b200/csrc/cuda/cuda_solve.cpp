@@ -2,6 +2,8 @@
 #include "../../../include/dopf/cuda_solve.hpp"
 
 #include <chrono>
+#include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -123,25 +125,46 @@ SolveResult Solver::solve(const Settings& settings) {
   impl_->run(settings, result, true);
   if (settings.record_iterates) {
     // IterateSnapshot{x, z, z_prev, lambda} after every iteration t
-    // (admm.cpp:228-229): the device loop is deterministic, so the state
-    // after t iterations is the result of a run capped at max_iter = t.
+    // (admm.cpp:228-229), written by the device loop itself in parity mode
+    // (dopf_cuda_solve_snapshots, resident path: one run). The streaming
+    // path has no parity mode: the loop is deterministic, so the state after
+    // t iterations is the result of a run capped at max_iter = t.
+    const int n = impl_->model->global_cols, Nz = impl_->model->total_local_vars();
+    const int T = std::max(1, result.iterations);
+    std::vector<double> snaps(static_cast<std::size_t>(T) * (n + 3 * static_cast<std::size_t>(Nz)));
+    std::vector<double> x(n), z(Nz), lam(Nz);
+    dopf_result_view v{};
+    v.x = x.data();
+    v.z = z.data();
+    v.lambda = lam.data();
+    const dopf_settings cs = to_c(settings);
+    const int rc = dopf_cuda_solve_snapshots(impl_->ctx, &cs, &v, snaps.data(), T);
     result.snapshots.resize(result.iterations);
-    std::vector<double> z_prev;
-    {
-      FlatModel& f = impl_->flat;
-      z_prev = f.z0;
-    }
-    for (int t = 1; t <= result.iterations; ++t) {
-      Settings capped = settings;
-      capped.max_iter = t;
-      SolveResult r;
-      impl_->run(capped, r, false);
-      IterateSnapshot& snap = result.snapshots[t - 1];
-      snap.x = std::move(r.x);
-      snap.z = r.z;
-      snap.z_prev = z_prev;
-      snap.lambda = std::move(r.lambda);
-      z_prev = std::move(r.z);
+    if (rc == DOPF_OK) {
+      for (int t = 0; t < result.iterations; ++t) {
+        const double* o = snaps.data() + static_cast<std::size_t>(t) * (n + 3 * static_cast<std::size_t>(Nz));
+        IterateSnapshot& snap = result.snapshots[t];
+        snap.x.assign(o, o + n);
+        snap.z.assign(o + n, o + n + Nz);
+        snap.z_prev.assign(o + n + Nz, o + n + 2 * Nz);
+        snap.lambda.assign(o + n + 2 * Nz, o + n + 3 * Nz);
+      }
+    } else if (rc == DOPF_ERR_INVALID_ARGUMENT) {
+      std::vector<double> z_prev = impl_->flat.z0;
+      for (int t = 1; t <= result.iterations; ++t) {
+        Settings capped = settings;
+        capped.max_iter = t;
+        SolveResult r;
+        impl_->run(capped, r, false);
+        IterateSnapshot& snap = result.snapshots[t - 1];
+        snap.x = std::move(r.x);
+        snap.z = r.z;
+        snap.z_prev = z_prev;
+        snap.lambda = std::move(r.lambda);
+        z_prev = std::move(r.z);
+      }
+    } else {
+      impl_->check(rc);
     }
   }
   return result;
@@ -149,9 +172,20 @@ SolveResult Solver::solve(const Settings& settings) {
 
 SolveResult solve(const DecomposedModel& model, const Settings& settings, int device) {
   check_settings(settings);
-  Solver solver(device);
-  solver.upload(model, settings.workers);
-  return solver.solve(settings);
+  // One context per (thread, device), kept across calls: the reference's
+  // solve() is called in loops (scenarios, rho sweeps), and a context owns
+  // streams, device buffers and the cached layout -- a same-structure model
+  // re-uploads through the values-only fast path. A failed call drops it.
+  thread_local std::map<int, std::unique_ptr<Solver>> contexts;
+  auto& slot = contexts[device];
+  if (!slot) slot = std::make_unique<Solver>(device);
+  try {
+    slot->upload(model, settings.workers);
+    return slot->solve(settings);
+  } catch (...) {
+    slot.reset();
+    throw;
+  }
 }
 
 SolveResult solve_partitioned(const DecomposedModel& model, const Settings& settings, int gpus) {

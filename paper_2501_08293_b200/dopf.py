@@ -584,6 +584,8 @@ class SolveResult:
     # stop tests within 1e-12 relative of flipping (dopf_result_view.near_ties)
     near_ties: int = 0
     first_near_tie: int = 0
+    # parity mode: t -> {x, z, z_prev, lambda} after iteration t (CudaSolver.solve(snapshots=T))
+    snapshots: dict = field(default_factory=dict)
 
     @property
     def converged(self) -> bool:
@@ -679,7 +681,11 @@ class CudaSolver:
     def bytes_per_iteration(self) -> float:
         return float(self._lib.dopf_cuda_bytes_per_iteration(self._h))
 
-    def solve(self, settings: Settings, outputs: bool = True) -> SolveResult:
+    def solve(self, settings: Settings, outputs: bool = True, snapshots: int = 0) -> SolveResult:
+        """One device solve. `snapshots` = T > 0 (parity mode, resident path)
+        also records the state after every iteration t <= min(T, stop) on the
+        device: result.snapshots[t] = {x, z, z_prev, lambda} (reference order,
+        IterateSnapshot of admm.cpp:228-229)."""
         _check_settings(settings)
         v = self.model.view()
         n, Nz = v.n, v.N_z
@@ -694,14 +700,26 @@ class CudaSolver:
             r.lambda_ = lam.ctypes.data_as(C.POINTER(C.c_double))
         r.trace = trace.ctypes.data_as(C.POINTER(C.c_double))
         st = settings.to_c()
-        self._err(self._lib.dopf_cuda_solve(self._h, C.byref(st), C.byref(r)))
+        snaps = None
+        if snapshots > 0:
+            T = min(int(snapshots), settings.max_iter)
+            snaps = np.zeros((T, n + 3 * Nz))
+            self._err(self._lib.dopf_cuda_solve_snapshots(self._h, C.byref(st), C.byref(r),
+                                                          snaps.ctypes.data_as(C.POINTER(C.c_double)), T))
+        else:
+            self._err(self._lib.dopf_cuda_solve(self._h, C.byref(st), C.byref(r)))
         it = r.iterations
-        return SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
-                           trace[:it].copy(),
-                           {"solve": r.time_solve, "upload": r.time_upload,
-                            "download": r.time_download, "global": r.time_global,
-                            "local": r.time_local, "dual": r.time_dual},
-                           r.near_ties, r.first_near_tie)
+        res = SolveResult(x, z, lam, r.status, it, r.objective, r.max_local_infeasibility,
+                          trace[:it].copy(),
+                          {"solve": r.time_solve, "upload": r.time_upload,
+                           "download": r.time_download, "global": r.time_global,
+                           "local": r.time_local, "dual": r.time_dual},
+                          r.near_ties, r.first_near_tie)
+        if snaps is not None:
+            res.snapshots = {t + 1: {"x": snaps[t, :n], "z": snaps[t, n:n + Nz],
+                                     "z_prev": snaps[t, n + Nz:n + 2 * Nz], "lambda": snaps[t, n + 2 * Nz:]}
+                             for t in range(min(it, snaps.shape[0]))}
+        return res
 
 
 def solve(model: DecomposedModel, settings: Settings = Settings(), device: int = 0) -> SolveResult:

@@ -70,27 +70,53 @@ def test_fixture_solve_matches_oracle_bitwise(solver, name, eps):
     assert_same(gpu, ref, bitwise=True)
 
 
-@pytest.mark.parametrize("name", ["two_bus", "four_bus_delta"])
-def test_per_iterate_parity(solver, name):
-    """Every sampled iterate t: run the device loop with max_iter = t."""
+def assert_snapshots_bitwise(gpu, ref, ts):
+    for t in ts:
+        g, r = gpu.snapshots[t], ref.snapshots[t]
+        for k in ("x", "z", "z_prev", "lambda"):
+            assert np.array_equal(g[k].view(np.uint64), r[k].view(np.uint64)), (t, k)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_per_iterate_parity(name):
+    """Every iterate t of the solve (parity mode: the device loop records the
+    state after each iteration itself, reference record_iterates,
+    admm.cpp:228-229): x, z, z_prev, lambda bitwise equal to the oracle's."""
     _, model = model_of_fixture(name)
-    samples = [1, 2, 3, 5, 10, 50, 100, 300]
-    ref = O.solve(model, dopf.Settings(eps_rel=1e-12, max_iter=max(samples)), snap_iters=samples)
-    solver.upload(model)
-    # two_bus reaches exact consensus (pres = dres = 0) at t = 203 even at 1e-12
-    samples = [t for t in samples if t < ref.iterations] + [ref.iterations]
-    for t in samples:
-        gpu = solver.solve(dopf.Settings(eps_rel=1e-12, max_iter=t))
-        assert gpu.iterations == t
-        assert gpu.status == (ref.status if t == ref.iterations else dopf.ITERATION_LIMIT)
-        if t == ref.iterations:
-            snap = {"x": ref.x, "z": ref.z, "lambda": ref.lam}
-            assert np.array_equal(gpu.x, snap["x"]) and np.array_equal(gpu.z, snap["z"])
-            continue
-        snap = ref.snapshots[t]
-        assert np.array_equal(gpu.x, snap["x"]), t
-        assert np.array_equal(gpu.z, snap["z"]), t
-        assert np.array_equal(gpu.lam, snap["lambda"]), t
+    st = dopf.Settings(eps_rel=1e-12, max_iter=300)
+    s = dopf.CudaSolver(0)
+    s.set_path("resident")
+    s.upload(model)
+    gpu = s.solve(st, snapshots=st.max_iter)
+    ts = list(range(1, gpu.iterations + 1))
+    ref = O.solve(model, st, snap_iters=ts)
+    assert (gpu.iterations, gpu.status) == (ref.iterations, ref.status)
+    assert sorted(gpu.snapshots) == ts
+    assert_snapshots_bitwise(gpu, ref, ts)
+
+
+@pytest.mark.parametrize("shape,seed,T,every", [("ieee123", 123, 1000, 1), ("ieee8500", 8500, 200, 7)])
+def test_per_iterate_parity_synthetic(shape, seed, T, every):
+    f = dopf.synthetic_feeder(shape, seed)
+    _, _, model = dopf.load_model(f, workers=4)
+    model.precompute(4)
+    st = dopf.Settings(max_iter=T)
+    s = dopf.CudaSolver(0)
+    s.upload(model)
+    gpu = s.solve(st, snapshots=T)
+    ts = list(range(1, gpu.iterations + 1, every)) + [gpu.iterations]
+    ref = O.solve(model, dopf.Settings(max_iter=T, workers=4), snap_iters=ts)
+    assert (gpu.iterations, gpu.status) == (ref.iterations, ref.status)
+    assert_snapshots_bitwise(gpu, ref, ts)
+
+
+def test_snapshots_rejected_on_the_streaming_path():
+    _, model = model_of_fixture("two_bus")
+    s = dopf.CudaSolver(0)
+    s.set_path("stream")
+    s.upload(model)
+    with pytest.raises(ValueError):
+        s.solve(dopf.Settings(max_iter=10), snapshots=10)
 
 
 def test_iteration_limit_is_a_status(solver):
