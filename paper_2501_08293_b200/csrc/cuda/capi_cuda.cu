@@ -124,6 +124,7 @@ struct dopf_cuda_ctx {
   const InstancePlan* dev_plan = nullptr;
   int staged_grid = 1;       // persistent CTAs of the staged streaming kernel
   int staged_ctas = 2;       // of them per SM
+  int local_threads = kStreamRows;  // direct-load CTA size (kWideRows for a hub subsystem wider than kStreamRows)
   bool stream_maps = false;  // the streaming layout's maps are on the device
   int64_t* d_psrc = nullptr;
   int64_t* d_asrc = nullptr;
@@ -731,7 +732,13 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   // (kBigCtasPerSm each) so they run beside the staged kernel
   c->staged_ctas = kDefaultStagedCtasPerSm;
   if (const char* e = std::getenv("DOPF_STAGED_CTAS")) c->staged_ctas = std::atoi(e) >= 3 ? 3 : 2;
-  const int big_sms = static_cast<int>((L.big_ids.size() + kBigCtasPerSm - 1) / kBigCtasPerSm);
+  c->local_threads = kStreamRows;
+  for (int32_t q : L.big_ids) {
+    const StreamChunk& ch = L.chunks[q];
+    if (std::max(ch.rows, std::max(ch.arows, ch.icols)) > kStreamRows) c->local_threads = kWideRows;
+  }
+  const int big_per_sm = c->local_threads > kStreamRows ? 1 : kBigCtasPerSm;
+  const int big_sms = static_cast<int>((L.big_ids.size() + big_per_sm - 1) / big_per_sm);
   // (0 when every chunk takes the direct path: the partial slots and the fold
   // count then cover the direct-load CTAs only)
   c->staged_grid = L.staged_ids.empty()
@@ -747,44 +754,7 @@ void upload_stream(dopf_cuda_ctx* c, const dopf_model_view& m, int nparts = 1, i
   d.export_rows = c->put(k++, L.export_rows);
   d.send = c->scratch<double>(k++, L.xstride());  // [exports | partials] record of this rank
   k++;  // (slot of the former separate partial gather)
-  // chunk -> CTA assignment of the persistent staged kernel (CTA b takes
-  // positions b, b + G, b + 2G, ...): cost-aware, deterministic. Chunks are
-  // dealt in rounds of G, heaviest first, each round's heaviest chunk to the
-  // CTA with the least accumulated cost (cost = stage bytes + a per-chunk
-  // constant for the fixed phases). DOPF_STREAM_RR=1 keeps the walk order.
-  {
-    const int G = std::max(1, c->staged_grid);
-    std::vector<int32_t> ids = L.staged_ids;
-    if (!std::getenv("DOPF_STREAM_RR") && G > 1 && ids.size() > static_cast<std::size_t>(G)) {
-      std::vector<double> cost(ids.size());
-      for (std::size_t i = 0; i < ids.size(); ++i) {
-        StagePlan sp;
-        stage_plan(L.chunks[ids[i]], sp);
-        cost[i] = static_cast<double>(sp.total) + 8192.0;
-      }
-      std::vector<std::size_t> by_cost(ids.size());
-      for (std::size_t i = 0; i < ids.size(); ++i) by_cost[i] = i;
-      std::stable_sort(by_cost.begin(), by_cost.end(), [&](std::size_t a, std::size_t b) { return cost[a] > cost[b]; });
-      std::vector<double> load(G, 0.0);
-      std::vector<int> cta(G);
-      std::vector<int32_t> out(ids.size());
-      for (std::size_t r0 = 0, round = 0; r0 < ids.size(); r0 += G, ++round) {
-        const std::size_t cnt = std::min<std::size_t>(G, ids.size() - r0);
-        for (int b = 0; b < G; ++b) cta[b] = b;
-        // the last, partial round may only use CTAs whose position exists
-        std::stable_sort(cta.begin(), cta.end(), [&](int a, int b) { return load[a] < load[b]; });
-        if (cnt < static_cast<std::size_t>(G)) std::sort(cta.begin(), cta.begin() + cnt);
-        for (std::size_t j = 0; j < cnt; ++j) {
-          const int b = cnt < static_cast<std::size_t>(G) ? static_cast<int>(j) : cta[j];
-          const std::size_t i = by_cost[r0 + j];
-          out[round * G + b] = ids[i];
-          load[b] += cost[i];
-        }
-      }
-      ids.swap(out);
-    }
-    d.staged_ids = c->put(k++, ids);
-  }
+  d.staged_ids = c->put(k++, L.staged_ids);
   d.big_ids = c->put(k++, L.big_ids);
   d.imp_ptr = c->put(k++, L.imp_ptr);
   d.imp_slot = c->put(k++, L.imp_slot);
@@ -855,6 +825,7 @@ StreamParams stream_params(dopf_cuda_ctx* c, const dopf_settings* s, double* tra
   p.cols = L.cols;
   p.bcols = L.bcols;
   p.col_blocks = std::max(1, (L.bcols + kStreamRows - 1) / kStreamRows);
+  p.local_threads = c->local_threads;
   return p;
 }
 

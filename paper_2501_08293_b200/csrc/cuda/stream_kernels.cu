@@ -347,10 +347,12 @@ __device__ void arrive_and_finish(const StreamParams& p, double* red, bool* last
 }
 
 // Direct-load kernel for chunks whose stage would not fit shared memory:
-// one CTA per chunk, image read straight from HBM.
-__global__ void __launch_bounds__(kStreamRows, 2) k_local(const StreamParams p) {
-  __shared__ double tgt[kStreamRows], ush[kStreamRows], xsh[kStreamRows], zsh[kStreamRows];
-  __shared__ double red[7 * (kStreamRows / 32)];
+// one CTA per chunk, image read straight from HBM; kRows = kWideRows when a
+// chunk holds a subsystem wider than kStreamRows (a hub bus).
+template <int kRows>
+__global__ void __launch_bounds__(kRows, 1024 / kRows) k_local(const StreamParams p) {
+  __shared__ double tgt[kRows], ush[kRows], xsh[kRows], zsh[kRows];
+  __shared__ double red[7 * (kRows / 32)];
   __shared__ ChunkHead hsh;
   __shared__ bool lastflag;
   if (p.ctl->done) return;
@@ -363,10 +365,10 @@ __global__ void __launch_bounds__(kStreamRows, 2) k_local(const StreamParams p) 
   double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   auto sync = [] { __syncthreads(); };
   auto ld = [](const double* a) { return __ldcs(a); };
-  chunk_iteration<kStreamRows>(p, img, hsh, p.z + ch.row0, p.lam + ch.row0, p.ximp + ch.bimp0, tgt, ush, xsh,
+  chunk_iteration<kRows>(p, img, hsh, p.z + ch.row0, p.lam + ch.row0, p.ximp + ch.bimp0, tgt, ush, xsh,
                                zsh, v, sync, ld);
   __syncthreads();
-  write_partials<kStreamRows>(p, v, red, p.staged_grid + blockIdx.x, sync);
+  write_partials<kRows>(p, v, red, p.staged_grid + blockIdx.x, sync);
   __syncthreads();  // red is reused by the fold
   arrive_and_finish(p, red, &lastflag);
 }
@@ -618,7 +620,7 @@ cudaError_t stream_launch_regather(const StreamRegather& g, int sm_count, cudaSt
 
 using LocalKernel = void (*)(const StreamParams);
 
-LocalKernel local_kernel() { return &k_local; }
+LocalKernel local_kernel(int threads) { return threads > kStreamRows ? &k_local<kWideRows> : &k_local<kStreamRows>; }
 
 // kernel attributes are per device: set on every upload (the caller has made
 // the context's device current)
@@ -638,7 +640,7 @@ StagedKernel staged_kernel(int ctas_per_sm, bool prof) {
 }
 
 void launch_local_all(const StreamParams& p, cudaStream_t s) {
-  if (p.n_big > 0) local_kernel()<<<p.n_big, kStreamRows, 0, s>>>(p);
+  if (p.n_big > 0) local_kernel(p.local_threads)<<<p.n_big, p.local_threads, 0, s>>>(p);
   if (p.n_staged > 0)
     staged_kernel(p.staged_ctas, p.prof != nullptr)<<<p.staged_grid, kStagedThreads, p.stages * p.stage_bytes, s>>>(p);
 }
@@ -656,7 +658,7 @@ void stream_launch_local(const StreamParams& p, cudaStream_t s) {
   if (p.max_export > 0) k_pack<<<(p.max_export + 255) / 256, 256, 0, s>>>(p);
 }
 void stream_launch_direct(const StreamParams& p, cudaStream_t s) {
-  if (p.n_big > 0) local_kernel()<<<p.n_big, kStreamRows, 0, s>>>(p);
+  if (p.n_big > 0) local_kernel(p.local_threads)<<<p.n_big, p.local_threads, 0, s>>>(p);
 }
 void stream_launch_staged(const StreamParams& p, cudaStream_t s) {
   if (p.n_staged > 0)
@@ -703,8 +705,9 @@ cudaError_t stream_build_graph(StreamParams p, cudaGraphExec_t* exec) {
   kg.blockDim = dim3(kStreamRows);
   kg.kernelParams = args;
   kb = kg;
-  kb.func = reinterpret_cast<void*>(local_kernel());
+  kb.func = reinterpret_cast<void*>(local_kernel(p.local_threads));
   kb.gridDim = dim3(p.n_big);
+  kb.blockDim = dim3(p.local_threads);
   ks = kg;
   ks.func = reinterpret_cast<void*>(staged_kernel(p.staged_ctas, p.prof != nullptr));
   ks.gridDim = dim3(p.staged_grid);

@@ -68,6 +68,7 @@ struct StreamParams {
   int32_t npart;         // partial slots: staged_grid + n_big
   int32_t stages, stage_bytes;  // staged-kernel pipeline (dynamic smem = stages * stage_bytes)
   int32_t staged_ctas;   // staged CTAs per SM (2 or 3)
+  int32_t local_threads; // direct-load kernel CTA size: kStreamRows, or kWideRows when a chunk is wider
   long long* prof;
        // optional [staged_grid][8] phase cycles of the staged kernel (thread 0)
   int32_t cols;

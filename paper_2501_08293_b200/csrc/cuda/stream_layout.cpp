@@ -97,8 +97,8 @@ StreamLayout build_stream_layout_part(const dopf_model_view& m, int nparts, int 
     if (part_of(s) == part) order.push_back(s);
   auto ns_of = [&](int s) { return m.z_offsets[s + 1] - m.z_offsets[s]; };
   for (int s = 0; s < m.S; ++s)
-    if (ns_of(s) > kStreamRows || m.m_s[s] > kStreamRows)
-      throw std::invalid_argument("subsystem wider than a streaming chunk");
+    if (ns_of(s) > kWideRows || m.m_s[s] > kWideRows)
+      throw std::invalid_argument("subsystem wider than a streaming chunk (1024 columns or rows)");
 
   // ---- chunks of whole subsystems along the locality walk
   std::vector<int32_t> dev_of_ref(m.N_z, -1);

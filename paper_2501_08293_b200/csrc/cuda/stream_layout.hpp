@@ -29,7 +29,8 @@
 
 namespace dopf::cuda {
 
-constexpr int kStreamRows = 512;   // rows of the widest chunk (direct-load kernel threads)
+constexpr int kStreamRows = 512;   // direct-load kernel threads (and k_global's CTA size)
+constexpr int kWideRows = 1024;    // rows of the widest chunk: a wide (hub) subsystem gets a 1024-thread direct-load CTA
 // staged kernel: chunks of <= kStagedRows rows whose shared-memory stage
 // (image + z + lambda + imports) fits `stage_bytes`; `stages` stages per CTA
 #ifndef DOPF_STAGED_ROWS

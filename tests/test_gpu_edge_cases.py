@@ -193,3 +193,33 @@ def test_auto_path_falls_back_to_streaming_beyond_resident_limits():
     forced.set_path("resident")
     with pytest.raises(ValueError):
         forced.upload(m)
+
+
+@pytest.mark.parametrize("n,m", [(700, 300), (1024, 1000)])
+def test_hub_subsystem_wider_than_a_chunk_streams_bitwise(n, m):
+    """A subsystem wider than 512 columns (a hub bus: the root of a feeder
+    tiled > 85 times) runs on a 1024-thread direct-load CTA."""
+    mdl = wide_subsystem_model(n, m, seed=n)
+    s = dopf.CudaSolver(0)
+    s.upload(mdl)
+    assert s.info()["sync"] == "stream-graph"
+    st = dopf.Settings(max_iter=200)
+    assert_same(s.solve(st), O.solve(mdl, st), bitwise=True)
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(1200)
+def test_tiled_feeder_beyond_85_tiles_bitwise():
+    """96 IEEE-8500 tiles on one root bus: the root subsystem is ~580 columns
+    wide (rejected by both paths before); first iterations bitwise."""
+    import os
+    f = dopf.tiled_feeder("ieee8500", 96, 850096)
+    _, _, model = dopf.load_model(f, workers=os.cpu_count() or 1)
+    model.precompute(os.cpu_count() or 1)
+    ns = np.diff(model.z_offsets)
+    assert ns.max() > 512
+    s = dopf.CudaSolver(0)
+    s.upload(model)
+    st = dopf.Settings(max_iter=12)
+    ref = O.solve(model, dopf.Settings(max_iter=12, workers=os.cpu_count() or 1))
+    assert_same(s.solve(st), ref, bitwise=True)

@@ -104,7 +104,7 @@ def test_per_iterate_parity_synthetic(shape, seed, T, every):
     s = dopf.CudaSolver(0)
     s.upload(model)
     gpu = s.solve(st, snapshots=T)
-    ts = list(range(1, gpu.iterations + 1, every)) + [gpu.iterations]
+    ts = sorted(set(range(1, gpu.iterations + 1, every)) | {gpu.iterations})
     ref = O.solve(model, dopf.Settings(max_iter=T, workers=4), snap_iters=ts)
     assert (gpu.iterations, gpu.status) == (ref.iterations, ref.status)
     assert_snapshots_bitwise(gpu, ref, ts)
