@@ -66,7 +66,9 @@ int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
  * written by the device loop itself (one pass, not a re-run per t) and
  * returned in reference order, n + 3 N_z doubles per iteration:
  * [x | z | z_prev | lambda] (IterateSnapshot, admm.hpp:108-114). Single
- * model on the resident path; code 1 otherwise. */
+ * model, either path (the streaming path runs its iterations stream-ordered
+ * with a snapshot copy after each, then the regular solve); code 1 for a
+ * partitioned upload or a batch. */
 int dopf_cuda_solve_snapshots(dopf_cuda_ctx* ctx, const dopf_settings* settings,
                               dopf_result_view* result, double* snapshots, int32_t T);
 /* One-time operators on the GPU (reference admm.cpp:31-88, batched over all

@@ -1208,8 +1208,53 @@ int dopf_cuda_solve_snapshots(dopf_cuda_ctx* c, const dopf_settings* s, dopf_res
                               double* snaps, int32_t T) {
   if (!c || !r || !snaps || T < 1) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
+    if (c->streaming && !c->partitioned) {
+      // streaming path: the iteration's kernels launched stream-ordered with a
+      // snapshot copy after each (test facility), then the regular solve
+      check_settings(s);
+      const StreamLayout& L = c->SL;
+      auto& d = c->sd;
+      const int64_t R = L.rows, X = L.cols, stride = 2 * R + X;
+      double* dev = c->scratch<double>(118, static_cast<std::size_t>(T) * stride);
+      stream_reset(c);
+      const StreamParams p = stream_params(c, s, nullptr);
+      StreamCtl h{};
+      int rec = 0;
+      do {
+        stream_launch_iteration(p, c->stream);
+        ck(cudaMemcpyAsync(&h, d.ctl, sizeof(StreamCtl), cudaMemcpyDeviceToHost, c->stream), "ctl");
+        ck(cudaStreamSynchronize(c->stream), "iteration");
+        if (h.t >= 1 && h.t <= T && h.t > rec) {
+          double* sn = dev + static_cast<int64_t>(h.t - 1) * stride;
+          ck(cudaMemcpyAsync(sn, d.z, R * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "snap");
+          ck(cudaMemcpyAsync(sn + R, d.lam, R * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "snap");
+          ck(cudaMemcpyAsync(sn + 2 * R, d.x, X * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "snap");
+          rec = h.t;
+        }
+      } while (!h.done);
+      run_stream(c, s, r, true);
+      if (r->iterations != h.t) throw std::runtime_error("parity-mode rerun diverged");
+      std::vector<double> hs(static_cast<std::size_t>(rec) * stride), z0(R);
+      ck(cudaMemcpy(hs.data(), dev, hs.size() * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+      ck(cudaMemcpy(z0.data(), d.z0, R * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+      const int64_t n = L.n, out = n + 3 * R;
+      std::vector<double> prev(R);
+      for (int64_t q = 0; q < R; ++q) prev[L.ref_of_dev[q]] = z0[q];
+      for (int t = 0; t < rec; ++t) {
+        const double* sn = hs.data() + static_cast<int64_t>(t) * stride;
+        double* o = snaps + static_cast<int64_t>(t) * out;
+        for (int64_t cl = 0; cl < X; ++cl) o[L.gcol[cl]] = sn[2 * R + cl];
+        for (int64_t q = 0; q < R; ++q) {
+          o[n + L.ref_of_dev[q]] = sn[q];
+          o[n + 2 * R + L.ref_of_dev[q]] = sn[R + q];
+        }
+        std::copy(prev.begin(), prev.end(), o + n + R);
+        std::copy(o + n, o + n + R, prev.begin());
+      }
+      return;
+    }
     if (c->streaming || c->partitioned || !c->dev_plan || c->L.inst.size() != 1)
-      throw std::invalid_argument("iterate snapshots need a single model on the resident path");
+      throw std::invalid_argument("iterate snapshots need a single model (resident or streaming path)");
     const InstancePlan& P = *c->dev_plan;
     const int64_t R = c->L.rows_total, X = c->L.x_total;
     const int64_t stride = 2 * R + X;

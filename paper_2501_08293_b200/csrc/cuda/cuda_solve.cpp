@@ -125,10 +125,10 @@ SolveResult Solver::solve(const Settings& settings) {
   impl_->run(settings, result, true);
   if (settings.record_iterates) {
     // IterateSnapshot{x, z, z_prev, lambda} after every iteration t
-    // (admm.cpp:228-229), written by the device loop itself in parity mode
-    // (dopf_cuda_solve_snapshots, resident path: one run). The streaming
-    // path has no parity mode: the loop is deterministic, so the state after
-    // t iterations is the result of a run capped at max_iter = t.
+    // (admm.cpp:228-229), recorded on the device in parity mode
+    // (dopf_cuda_solve_snapshots, both paths). Fallback for a context the
+    // parity mode rejects: the loop is deterministic, so the state after t
+    // iterations is the result of a run capped at max_iter = t.
     const int n = impl_->model->global_cols, Nz = impl_->model->total_local_vars();
     const int T = std::max(1, result.iterations);
     std::vector<double> snaps(static_cast<std::size_t>(T) * (n + 3 * static_cast<std::size_t>(Nz)));

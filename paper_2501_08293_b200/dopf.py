@@ -471,10 +471,15 @@ def prepare_gpu(models: List["DecomposedModel"], solver: "CudaSolver", tol: floa
     partitioned, unreduced models. Raises InfeasibleSubsystemError /
     SingularSubsystemError naming the component like the host does. Returns
     the summed {pack, kernels, unpack} seconds of the device calls."""
+    import concurrent.futures as cf
+    import os
     tot = {"pack_s": 0.0, "kernels_s": 0.0, "unpack_s": 0.0}
+    # per-model host bookkeeping (views, adopting the results) on all cores:
+    # ctypes releases the GIL inside the native calls
+    pool = cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 1)
     for c0 in range(0, len(models), chunk):
         part = models[c0:c0 + chunk]
-        views = (N.ModelView_t * len(part))(*[m.view() for m in part])
+        views = (N.ModelView_t * len(part))(*pool.map(lambda m: m.view(), part))
         na = nb = ns = npp = nz = 0
         sizes = []
         for v in views:
@@ -505,16 +510,23 @@ def prepare_gpu(models: List["DecomposedModel"], solver: "CudaSolver", tol: floa
         tot["pack_s"] += secs[0]
         tot["kernels_s"] += secs[1]
         tot["unpack_s"] += secs[2]
-        a0 = b0 = s0 = p0 = z0 = 0
-        for m, (a, b, S, p2, n_z) in zip(part, sizes):
-            _check(N.host().dopf_model_set_reduced(
-                m.handle, A[a0:].ctypes.data_as(C.POINTER(C.c_double)),
-                B[b0:].ctypes.data_as(C.POINTER(C.c_double)), Ms[s0:].ctypes.data_as(C.POINTER(N.i32))))
-            _check(N.host().dopf_model_set_operators(
-                m.handle, Pp[p0:].ctypes.data_as(C.POINTER(C.c_double)),
-                V[z0:].ctypes.data_as(C.POINTER(C.c_double))))
+        starts, a0 = [], (0, 0, 0, 0, 0)
+        for (a, b, S, p2, n_z) in sizes:
+            starts.append(a0)
+            a0 = (a0[0] + a, a0[1] + b, a0[2] + S, a0[3] + p2, a0[4] + n_z)
+        dp, ip = C.POINTER(C.c_double), C.POINTER(N.i32)
+        base = (A.ctypes.data, B.ctypes.data, Ms.ctypes.data, Pp.ctypes.data, V.ctypes.data)
+
+        def adopt(job):
+            m, (oa, ob, os_, op, oz) = job
+            _check(N.host().dopf_model_set_reduced(m.handle, C.cast(base[0] + 8 * oa, dp),
+                                                   C.cast(base[1] + 8 * ob, dp), C.cast(base[2] + 4 * os_, ip)))
+            _check(N.host().dopf_model_set_operators(m.handle, C.cast(base[3] + 8 * op, dp),
+                                                     C.cast(base[4] + 8 * oz, dp)))
             m._view = None
-            a0, b0, s0, p0, z0 = a0 + a, b0 + b, s0 + S, p0 + p2, z0 + n_z
+
+        list(pool.map(adopt, zip(part, starts)))
+    pool.shutdown()
     return tot
 
 
@@ -682,7 +694,7 @@ class CudaSolver:
         return float(self._lib.dopf_cuda_bytes_per_iteration(self._h))
 
     def solve(self, settings: Settings, outputs: bool = True, snapshots: int = 0) -> SolveResult:
-        """One device solve. `snapshots` = T > 0 (parity mode, resident path)
+        """One device solve. `snapshots` = T > 0 (parity mode, either path)
         also records the state after every iteration t <= min(T, stop) on the
         device: result.snapshots[t] = {x, z, z_prev, lambda} (reference order,
         IterateSnapshot of admm.cpp:228-229)."""

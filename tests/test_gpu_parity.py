@@ -110,13 +110,26 @@ def test_per_iterate_parity_synthetic(shape, seed, T, every):
     assert_snapshots_bitwise(gpu, ref, ts)
 
 
-def test_snapshots_rejected_on_the_streaming_path():
-    _, model = model_of_fixture("two_bus")
+@pytest.mark.parametrize("src", ["two_bus_delta", "four_bus_delta", "ieee123"])
+def test_per_iterate_parity_streaming_path(src):
+    """Parity mode on the HBM-streaming path (stream-ordered iterations with
+    a snapshot copy after each): every iterate bitwise equal to the oracle."""
+    if src == "ieee123":
+        _, _, model = dopf.load_model(dopf.synthetic_feeder("ieee123", 123), workers=4)
+        model.precompute(4)
+        st = dopf.Settings(max_iter=300)
+    else:
+        _, model = model_of_fixture(src)
+        st = dopf.Settings(eps_rel=1e-12, max_iter=300)
     s = dopf.CudaSolver(0)
     s.set_path("stream")
     s.upload(model)
-    with pytest.raises(ValueError):
-        s.solve(dopf.Settings(max_iter=10), snapshots=10)
+    gpu = s.solve(st, snapshots=st.max_iter)
+    ts = list(range(1, gpu.iterations + 1))
+    ref = O.solve(model, st, snap_iters=ts)
+    assert (gpu.iterations, gpu.status) == (ref.iterations, ref.status)
+    assert sorted(gpu.snapshots) == ts
+    assert_snapshots_bitwise(gpu, ref, ts)
 
 
 def test_iteration_limit_is_a_status(solver):
