@@ -146,6 +146,12 @@ double dopf_cuda_last_kernel_seconds(const dopf_cuda_ctx* ctx);
  * residual combine. out receives [min(max_blocks, CTAs)][8] counters. */
 int dopf_cuda_set_profiling(dopf_cuda_ctx* ctx, int32_t on);
 int dopf_cuda_phase_cycles(const dopf_cuda_ctx* ctx, int64_t* out, int32_t max_blocks);
+/* Resident layout statistics per CTA (diagnostics, load-balance studies):
+ * [min(max_blocks, CTAs)][12] = rows, columns, interior columns, equality
+ * rows, P doubles, A doubles, copy references, neighbour blocks, remote copy
+ * reads, exported rows, longest per-thread GEMV chain (sum of n_s over a
+ * thread's rows), sum of n_s over rows. */
+int dopf_cuda_block_stats(const dopf_cuda_ctx* ctx, int64_t* out, int32_t max_blocks);
 /* With profiling on: %globaltimer stamps (ns) per CTA for 64 iterations from
  * t = 100 -- [CTA][iteration][u published, boundary update start, end]. */
 int dopf_cuda_timeline(const dopf_cuda_ctx* ctx, uint64_t* out, int64_t cap);

@@ -183,10 +183,12 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// The whole solve of one block descriptor `blk` (one CTA's share of one
+// instance) -- the body of the persistent kernel below.
 template <int K, bool kSmemOps>
-__global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(const KernelParams p) {
+__device__ __forceinline__ void solve_block(const KernelParams& p, const int blk) {
   extern __shared__ __align__(16) double smem[];
-  const BlockDesc bd = p.blocks[blockIdx.x];
+  const BlockDesc bd = p.blocks[blk];
   const InstDesc id = p.inst[bd.instance];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -707,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
       named_sync(kBarCompute, kCW);  // every u(t) in shared memory
       unsigned long long* tl = nullptr;
       if (p.timeline && ctid == 0 && t >= kTimelineT0 && t < kTimelineT0 + kTimelineIters) {
-        tl = p.timeline + (static_cast<int64_t>(blockIdx.x) * kTimelineIters + (t - kTimelineT0)) * 3;
+        tl = p.timeline + (static_cast<int64_t>(blk) * kTimelineIters + (t - kTimelineT0)) * 3;
         tl[0] = globaltimer();  // u(t) published (every warp's stores issued)
       }
       if (tick) {
@@ -765,10 +767,14 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
     // release the check warp from its wait for z^{t+1}
     if (ctid == 0) *reinterpret_cast<volatile double*>(adone) = t + 1;
     named_arrive(kBarZReady + ((t + 1) & 1), kCW + 32);
+    // consume the check warp's last "z^s checked" arrivals (s = t - 1, t; the
+    // loop consumed s <= t - 2): hardware barriers keep pending arrivals, and
+    // a CTA of a persistent group solves its next instance with the same ones
+    for (int s = t > 1 ? t - 1 : 1; s <= t; ++s) named_sync(kBarZFree + (s & 1), kCW + 32);
   }
   __syncthreads();
   stop_at = static_cast<int>(red[0]);
-  if (clock_on && tid < 8) p.prof[blockIdx.x * 8 + tid] += ph[tid];
+  if (clock_on && tid < 8) p.prof[blk * 8 + tid] += ph[tid];
   if (p.phase_sample && bd.instance == 0 && bd.inst_block == 0 && tid < 8) p.phase_sample[tid] = ph[tid];
   if (warp == 1 && lane == 0) {
     // max_local_infeasibility over iterations 1..stop_at: the check warp saw
@@ -789,6 +795,29 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(cons
       const ColMeta cmc = p.cmeta[bd.col_off + c];
       if (cmc.owner) p.x_out[id.x_off + cmc.gcol] = xfinal[c];
     }
+  }
+}
+
+// One CTA per block descriptor (single instance, clusters: admm_persistent),
+// or -- scenario batches, admm_groups -- a persistent grid of CTA groups: group g
+// (CTAs gG .. gG+G-1, co-resident through the cooperative launch) solves
+// instances g, g + groups, g + 2 groups, ... one after another, restaging
+// each instance's operators. Unlike one thread-block cluster per instance,
+// which must fit one GPC (33 clusters of 4 = 132 of 148 SMs on this B200,
+// tools/micro/cluster_occupancy.cu), every SM holds a CTA. Instances share
+// no state, so which group solves one does not change its results.
+template <int K, bool kSmemOps>
+__global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_persistent(const KernelParams p) {
+  solve_block<K, kSmemOps>(p, blockIdx.x);
+}
+
+template <int K, bool kSmemOps>
+__global__ void __launch_bounds__(kThreads, 512 / kThreads) admm_groups(const KernelParams p) {
+  const int G = p.group_size, groups = gridDim.x / G;
+  const int g = blockIdx.x / G, b = blockIdx.x - g * G;
+  for (int inst = g; inst < p.instances; inst += groups) {
+    solve_block<K, kSmemOps>(p, inst * G + b);
+    __syncthreads();  // shared memory is restaged for the next instance
   }
 }
 
@@ -844,6 +873,34 @@ cudaError_t launch_admm(const KernelParams& p, int num_blocks, int K, std::size_
     case 2: return launch_ops<2>(p, num_blocks, smem, mode, cluster_size, smem_ops, stream);
     case 3: return launch_ops<3>(p, num_blocks, smem, mode, cluster_size, smem_ops, stream);
     case 4: return launch_ops<4>(p, num_blocks, smem, mode, cluster_size, smem_ops, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+namespace {
+template <int K, bool kSmemOps>
+cudaError_t launch_groups_k(const KernelParams& p, int groups, std::size_t smem, cudaStream_t stream) {
+  auto kern = admm_groups<K, kSmemOps>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  KernelParams local = p;
+  void* args[] = {&local};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(groups * p.group_size), dim3(kThreads),
+                                     args, smem, stream);
+}
+template <int K>
+cudaError_t launch_groups_ops(const KernelParams& p, int groups, std::size_t smem, bool smem_ops, cudaStream_t s) {
+  return smem_ops ? launch_groups_k<K, true>(p, groups, smem, s) : launch_groups_k<K, false>(p, groups, smem, s);
+}
+}  // namespace
+
+cudaError_t launch_admm_groups(const KernelParams& p, int groups, int K, std::size_t smem, bool smem_ops,
+                               cudaStream_t stream) {
+  switch (K) {
+    case 1: return launch_groups_ops<1>(p, groups, smem, smem_ops, stream);
+    case 2: return launch_groups_ops<2>(p, groups, smem, smem_ops, stream);
+    case 3: return launch_groups_ops<3>(p, groups, smem, smem_ops, stream);
+    case 4: return launch_groups_ops<4>(p, groups, smem, smem_ops, stream);
     default: return cudaErrorInvalidValue;
   }
 }

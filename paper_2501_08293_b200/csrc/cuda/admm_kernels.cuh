@@ -68,14 +68,19 @@ struct KernelParams {
   int64_t trace_stride; // rows per instance in `trace`
   int32_t max_iter;
   int32_t blocks_per_instance;
-  int32_t sync_mode;    // SyncMode
-  int32_t pad;
+  int32_t sync_mode;    // SyncMode (cluster: the exchange between an instance's CTAs)
+  int32_t group_size;   // > 0: persistent groups of this many CTAs loop over the instances
+  int32_t instances;
 };
 
 /// Launches the persistent kernel: one CTA per block descriptor, all
 /// iterations on device until every instance converged or hit max_iter.
 cudaError_t launch_admm(const KernelParams& p, int num_blocks, int K, std::size_t smem_bytes,
                         SyncMode mode, int cluster_size, bool smem_ops, cudaStream_t stream);
+/// Scenario batches: a cooperative grid of `groups` x p.group_size CTAs
+/// looping over the instances (p.group_size, p.instances set).
+cudaError_t launch_admm_groups(const KernelParams& p, int groups, int K, std::size_t smem_bytes, bool smem_ops,
+                               cudaStream_t stream);
 
 /// Largest dynamic shared memory the kernel may use on this device.
 int max_dynamic_smem(int device);

@@ -523,9 +523,20 @@ void run(dopf_cuda_ctx* c, const dopf_settings* s, dopf_result_view* results, in
   p.snap_stride = 2 * L.rows_total + L.x_total;
   p.snap_iters = c->snap_dev ? c->snap_iters : 0;
 
+  // scenario batches: persistent CTA groups over the instances (every SM
+  // busy) unless DOPF_BATCH_CLUSTERS=1 asks for one cluster per instance
+  const bool groups = I > 1 && c->mode != SyncMode::grid && !std::getenv("DOPF_BATCH_CLUSTERS");
+  p.group_size = groups ? L.blocks_per_instance : 0;
+  p.instances = static_cast<int32_t>(I);
   ck(cudaEventRecord(c->ev0, c->stream), "event");
-  ck(launch_admm(p, c->num_blocks, L.K, L.smem_bytes, c->mode, c->cluster, L.all_ops_in_smem, c->stream),
-     "launch");
+  if (groups) {
+    const int G = L.blocks_per_instance;
+    const int ng = std::max(1, std::min<int>(static_cast<int>(I), c->sm_count * ctas_per_sm() / G));
+    ck(launch_admm_groups(p, ng, L.K, L.smem_bytes, L.all_ops_in_smem, c->stream), "launch");
+  } else {
+    ck(launch_admm(p, c->num_blocks, L.K, L.smem_bytes, c->mode, c->cluster, L.all_ops_in_smem, c->stream),
+       "launch");
+  }
   ck(cudaEventRecord(c->ev1, c->stream), "event");
   ++c->launches;
   ++c->kernels;
@@ -2079,6 +2090,32 @@ int dopf_cuda_set_profiling(dopf_cuda_ctx* c, int32_t on) {
     if (c->d_prof) ck(cudaMemset(c->d_prof, 0, c->prof_cap * sizeof(long long)), "memset");
     c->profiling = on != 0;
   });
+}
+
+int dopf_cuda_block_stats(const dopf_cuda_ctx* c, int64_t* out, int32_t max_blocks) {
+  if (!c || !out || max_blocks < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  const HostLayout& L = c->L;
+  const int nb = std::min<int>(max_blocks, static_cast<int>(L.blocks.size()));
+  const int cw = kComputeThreads;
+  for (int g = 0; g < nb; ++g) {
+    const BlockDesc& b = L.blocks[g];
+    int64_t remote = 0, exported = 0, chain = 0, n2 = 0;
+    for (int q = 0; q < b.copy_len; ++q) remote += L.copies[b.copy_off + q] < 0;
+    for (int r = 0; r < b.rows; ++r) {
+      const RowMeta& rm = L.rmeta[b.row0 + r];
+      exported += rm.exported;
+      n2 += rm.n;
+    }
+    for (int t = 0; t < cw; ++t) {  // a thread's rows t, t + cw, ...: its sequential GEMV chain
+      int64_t sum = 0;
+      for (int r = t; r < b.rows; r += cw) sum += L.rmeta[b.row0 + r].n;
+      chain = std::max(chain, sum);
+    }
+    const int64_t v[12] = {b.rows, b.cols, b.cols_int, b.arows, b.p_len, b.a_len, b.copy_len,
+                           b.nbr_cnt, remote, exported, chain, n2};
+    for (int q = 0; q < 12; ++q) out[static_cast<int64_t>(g) * 12 + q] = v[q];
+  }
+  return DOPF_OK;
 }
 
 int dopf_cuda_phase_cycles(const dopf_cuda_ctx* c, int64_t* out, int32_t max_blocks) {

@@ -244,6 +244,24 @@ def test_batch_ieee123_scenarios_bitwise():
     assert len(its) > 1  # scenarios really converge independently
 
 
+@pytest.mark.timeout(600)
+def test_batch_persistent_groups_several_instances_per_group_bitwise():
+    """Batches run as persistent CTA groups (admm_groups): with 100 IEEE-123
+    scenarios over 37 groups of 4 CTAs every group solves 2-3 instances one
+    after another in the same CTAs -- each still bitwise equal to the oracle
+    (iterations, status, x / z / lambda, max_local_infeasibility, trace)."""
+    import concurrent.futures as cf
+    import os
+    from paper_2501_08293_b200 import scenarios
+    models = scenarios.build_scenarios("ieee123", 123, range(100))
+    settings = dopf.Settings()
+    results = solver_batch(models, settings)
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        refs = list(ex.map(lambda m: O.solve(m, dopf.Settings(workers=1)), models))
+    for gpu, ref in zip(results, refs):
+        assert_same(gpu, ref, bitwise=True)
+
+
 # ------------------------------------------------------------ HBM-streaming path
 
 

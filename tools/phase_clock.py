@@ -42,6 +42,10 @@ for q, name in enumerate(PHASES):
     print(f"  {name:14s} {col[0]:8.0f} {col.min():8.0f} {np.median(col):8.0f} {col.max():8.0f} "
           f"{int(col.argmax()):6d}")
 busy = a[:, [0, 1, 2, 3, 5]].sum(axis=1)
+if os.environ.get("PHASE_DUMP"):  # per-CTA busy cycles + layout statistics for a cost-model fit
+    st = (N.i64 * (12 * G))()
+    lib.dopf_cuda_block_stats(s._h, st, G)
+    np.savez(os.environ["PHASE_DUMP"], phases=a, stats=np.array(st[:], dtype=np.int64).reshape(G, 12))
 print(f"  compute (no exch-wait): min {busy.min():.0f} median {np.median(busy):.0f} "
       f"max {busy.max():.0f} (CTA {int(busy.argmax())})")
 
