@@ -79,7 +79,14 @@ _cuda = None
 
 
 def _sig(lib, name, res, *args):
-    fn = getattr(lib, name)
+    try:
+        fn = getattr(lib, name)
+    except AttributeError:
+        # an older build loaded for an A/B (DOPF_CUDA_SO) may lack newer
+        # diagnostics; the product build must export everything
+        if os.environ.get("DOPF_CUDA_SO"):
+            return None
+        raise
     fn.restype = res
     fn.argtypes = list(args)
     return fn
