@@ -61,6 +61,17 @@ int dopf_cuda_solve_batch(dopf_cuda_ctx* ctx, const dopf_settings* settings,
                           dopf_result_view* results, int32_t count);
 
 int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
+/* Partition tuning of the resident path (setup step, like an autotuner):
+ * uploads the model, then for `rounds` rounds measures each CTA's slack at
+ * the iteration's final barrier with the phase clock and moves cost shares
+ * of the depth-first split away from the CTAs without slack (the critical
+ * region of the exchange), keeping the fastest split; the context keeps the
+ * tuned shares for later uploads of the same structure. Iterates are
+ * unchanged (bitwise: the global update sums in ascending s whatever the
+ * split). A no-op for batches and the streaming path. *seconds_per_iteration
+ * receives the best measured period. */
+int dopf_cuda_tune_partition(dopf_cuda_ctx* ctx, const dopf_model_view* model, const dopf_settings* settings,
+                             int32_t rounds, double* seconds_per_iteration);
 /* Parity mode (reference Settings::record_iterates, admm.cpp:228-229): the
  * same solve, with the state after every iteration t = 1 .. min(T, stop)
  * written by the device loop itself (one pass, not a re-run per t) and

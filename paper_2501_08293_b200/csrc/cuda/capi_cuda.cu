@@ -89,6 +89,7 @@ struct dopf_cuda_ctx {
   // HBM-streaming path (instances too large for shared-memory residency)
   int path_request = 0;      // 0 auto, 1 resident persistent kernel, 2 streaming graph
   double* snap_dev = nullptr;  // parity mode: per-iteration snapshots of the next resident run (slot 118)
+  std::vector<double> block_weights;  // tuned cost shares of the resident split (dopf_cuda_tune_partition)
   int snap_iters = 0;
   bool streaming = false;    // path of the uploaded model
   StreamLayout SL;
@@ -344,6 +345,16 @@ LayoutOptions options_for(const dopf_cuda_ctx* c) {
   o.smem_limit = cps == 1 ? static_cast<std::size_t>(c->smem_optin)
                           : static_cast<std::size_t>(c->smem_per_sm) / cps - 1024;  // 1 KB reserved per CTA
   o.max_blocks = c->sm_count * cps;
+  o.block_weights = c->block_weights;
+  if (const char* e = std::getenv("DOPF_BLOCK_WEIGHTS"); e && o.block_weights.empty()) {  // experiments
+    for (const char* q = e; *q;) {
+      char* end = nullptr;
+      const double v = std::strtod(q, &end);
+      if (end == q) break;
+      o.block_weights.push_back(v);
+      q = *end == ',' ? end + 1 : end;
+    }
+  }
   return o;
 }
 
@@ -2082,6 +2093,84 @@ int dopf_layout_probe_batch(const dopf_model_view* ms, int32_t count, int64_t sm
   } catch (const std::exception&) {
     return DOPF_ERR_RUNTIME;
   }
+}
+
+int dopf_cuda_tune_partition(dopf_cuda_ctx* c, const dopf_model_view* m, const dopf_settings* s,
+                             int32_t rounds, double* seconds_per_iteration) {
+  if (!c || !m || !s || rounds < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  int rc = dopf_cuda_upload(c, m);
+  if (rc != DOPF_OK) return rc;
+  if (c->streaming || c->mode != SyncMode::grid || c->L.inst.size() != 1) {
+    if (seconds_per_iteration) *seconds_per_iteration = 0;
+    return DOPF_OK;  // only a grid-wide single instance has a split to tune
+  }
+  rc = guarded(c, [&] {
+    check_settings(s);
+    const int G = static_cast<int>(c->L.blocks.size());
+    const int K0 = c->L.K;
+    std::vector<double> w(G, 1.0), best_w, best_wait(G), best_busy(G);
+    double best = 1e300, beta = 0.5;
+    std::vector<long long> cyc(static_cast<std::size_t>(G) * 8);
+    auto median = [](std::vector<double> x) {
+      std::nth_element(x.begin(), x.begin() + x.size() / 2, x.end());
+      return x[x.size() / 2];
+    };
+    for (int r = 0; r < rounds; ++r) {
+      c->block_weights = w;
+      bool ok = true;
+      try {
+        c->plan.reset();  // re-plan with these shares
+        if (dopf_cuda_upload(c, m) != DOPF_OK) throw std::invalid_argument(c->err);
+        ok = !c->streaming && c->mode == SyncMode::grid && c->L.K == K0 && c->L.all_ops_in_smem &&
+             static_cast<int>(c->L.blocks.size()) == G;
+      } catch (const std::invalid_argument&) {
+        ok = false;
+      }
+      double per = 1e300;
+      if (ok) {
+        dopf_result_view v{};
+        for (int q = 0; q < 3; ++q) {  // best of three plain runs
+          run(c, s, &v, 1, false);
+          per = std::min(per, c->last_kernel_s / std::max(1, v.iterations));
+        }
+      }
+      if (ok && per < best) {
+        best = per;
+        best_w = w;
+        // slack of every CTA at the iteration's final barrier (phase clock)
+        if (c->d_prof) ck(cudaMemset(c->d_prof, 0, c->prof_cap * sizeof(long long)), "memset");
+        c->profiling = true;
+        dopf_result_view v{};
+        run(c, s, &v, 1, false);
+        c->profiling = false;
+        ck(cudaMemcpy(cyc.data(), c->d_prof, cyc.size() * sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
+        for (int g = 0; g < G; ++g) {
+          const long long* ph = cyc.data() + static_cast<std::size_t>(g) * 8;
+          best_wait[g] = static_cast<double>(ph[4]);
+          best_busy[g] = static_cast<double>(ph[0] + ph[1] + ph[2] + ph[3] + ph[5]);
+        }
+      } else {
+        beta *= 0.5;  // rejected: a smaller step from the best split
+      }
+      if (best_w.empty()) break;
+      // CTAs without slack (the critical region) give cost shares away
+      const double mw = median(best_wait), mb = std::max(1.0, median(best_busy));
+      double sum = 0;
+      for (int g = 0; g < G; ++g) {
+        w[g] = best_w[g] * (1.0 + beta * (best_wait[g] - mw) / mb);
+        w[g] = std::min(1.5, std::max(0.5, w[g]));
+        sum += w[g];
+      }
+      for (double& x : w) x *= G / sum;
+    }
+    if (best_w.empty()) best_w.assign(G, 1.0);
+    c->block_weights = best_w;
+    c->plan.reset();
+    const int u = dopf_cuda_upload(c, m);
+    if (u != DOPF_OK) throw std::runtime_error(c->err);
+    if (seconds_per_iteration) *seconds_per_iteration = best;
+  });
+  return rc;
 }
 
 int dopf_cuda_set_profiling(dopf_cuda_ctx* c, int32_t on) {

@@ -56,19 +56,26 @@ std::vector<int> locality_order_impl(const dopf_model_view& m) {
   return order;
 }
 
-// Cuts `order` into at most G contiguous pieces of nearly equal cost.
+// Cuts `order` into at most G contiguous pieces of nearly equal cost, or --
+// with per-block shares `w` (G entries; a partition tuned from measured
+// per-CTA slack, LayoutOptions::block_weights) -- of cost proportional to them.
 std::vector<std::vector<int>> split_blocks(const dopf_model_view& m, const std::vector<int>& order,
-                                           int G) {
+                                           int G, const std::vector<double>& w = {}) {
   double total = 0;
   for (int s : order) total += sub_cost(m, s);
+  const bool weighted = static_cast<int>(w.size()) == G;
+  double wsum = 0;
+  for (double x : w) wsum += x;
   std::vector<std::vector<int>> out(1);
-  double acc = 0;
+  double acc = 0, wacc = weighted ? w[0] : 0;
   int g = 1;
   for (int s : order) {
     out.back().push_back(s);
     acc += sub_cost(m, s);
-    if (g < G && acc >= total * g / G) {
+    const double target = weighted ? total * wacc / wsum : total * g / G;
+    if (g < G && acc >= target) {
       out.emplace_back();
+      if (weighted) wacc += w[g];
       ++g;
     }
   }
@@ -142,7 +149,7 @@ bool InstancePlan::same_structure(const dopf_model_view& m, const LayoutOptions&
   };
   return m.has_pre && S == m.S && n == m.n && Nz == m.N_z && o.smem_limit == opt.smem_limit &&
          o.max_blocks == opt.max_blocks && o.threads == opt.threads &&
-         o.blocks_per_instance == opt.blocks_per_instance && eq(z_offsets, m.z_offsets, m.S + 1) &&
+         o.blocks_per_instance == opt.blocks_per_instance && o.block_weights == opt.block_weights && eq(z_offsets, m.z_offsets, m.S + 1) &&
          eq(m_s, m.m_s, m.S) && eq(l2g, m.l2g, m.N_z) && eq(csr_ptr, m.csr_ptr, m.n + 1) &&
          eq(csr_copy, m.csr_copy, m.N_z);
 }
@@ -162,7 +169,7 @@ InstancePlan plan_instance(const dopf_model_view& m, int G, const LayoutOptions&
   P.csr_copy.assign(m.csr_copy, m.csr_copy + m.N_z);
 
   const std::vector<std::vector<int>> parts =
-      split_blocks(m, locality_order_impl(m), std::max(1, std::min(G, std::max(1, m.S))));
+      split_blocks(m, locality_order_impl(m), std::max(1, std::min(G, std::max(1, m.S))), opt.block_weights);
   const int nb = static_cast<int>(parts.size());
   const int cw = opt.threads - 64;  // compute threads (kComputeThreads)
 

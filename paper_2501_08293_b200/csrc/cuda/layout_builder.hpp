@@ -44,6 +44,9 @@ struct LayoutOptions {
   std::size_t smem_limit = 227 * 1024;
   int max_blocks = 148;               // co-resident CTA budget (1 per SM)
   int threads = kThreads;
+  // optional per-block cost shares of a single instance's split (G entries):
+  // a partition tuned from measured slack (DOPF_BLOCK_WEIGHTS)
+  std::vector<double> block_weights;
 };
 
 /// Index structure of one instance's device layout (instance-relative

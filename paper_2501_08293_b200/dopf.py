@@ -680,6 +680,20 @@ class CudaSolver:
                 "stages")
         return {k: int(v) for k, v in zip(keys, out)}
 
+    def tune_partition(self, model: "DecomposedModel", settings: "Settings" = None, rounds: int = 8) -> float:
+        """Setup-time tuning of the resident split (dopf_cuda_tune_partition):
+        measured per-CTA slack moves cost away from the exchange's critical
+        region; the context keeps the tuned split (iterates unchanged).
+        Uploads `model`; returns the best measured seconds per iteration."""
+        if not model.has_precompute:
+            model.precompute()
+        st = (settings or Settings()).to_c()
+        out = C.c_double(0.0)
+        self._err(self._lib.dopf_cuda_tune_partition(self._h, C.byref(model.view()), C.byref(st), rounds,
+                                                     C.byref(out)))
+        self.model = model
+        return out.value
+
     def set_path(self, path: str) -> None:
         """'auto' | 'resident' | 'stream' for the next upload."""
         self._err(self._lib.dopf_cuda_set_path(self._h, {"auto": 0, "resident": 1, "stream": 2}[path]))

@@ -198,6 +198,26 @@ def solver_batch(models, settings):
 
 
 @pytest.mark.timeout(600)
+def test_tuned_partition_keeps_iterates_bitwise():
+    """The slack-tuned resident split (dopf_cuda_tune_partition) changes only
+    which CTA holds which subsystems: IEEE-8500 to convergence stays bitwise
+    equal to the oracle, and the tuned split is not slower than the default."""
+    f = dopf.synthetic_feeder("ieee8500", 8500)
+    _, _, model = dopf.load_model(f, workers=8)
+    model.precompute(8)
+    s = dopf.CudaSolver(0)
+    s.upload(model)
+    base = min(s.solve(dopf.Settings(), outputs=False).timings["solve"] for _ in range(3))
+    per = s.tune_partition(model, dopf.Settings(), rounds=6)
+    gpu = s.solve(dopf.Settings())
+    ref = O.solve(model, dopf.Settings(workers=8))
+    assert_same(gpu, ref, bitwise=True)
+    assert per * gpu.iterations <= base * 1.02
+    s.upload(model)  # a same-structure re-upload keeps the tuned split
+    assert_same(s.solve(dopf.Settings()), ref, bitwise=True)
+
+
+@pytest.mark.timeout(600)
 def test_ieee8500_full_solve_bitwise(solver):
     """The paper's largest case to convergence: identical iteration count and
     bitwise-identical x, z, lambda (the multi-block exchange protocol at scale)."""

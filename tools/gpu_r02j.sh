@@ -1,0 +1,9 @@
+TAG=${1:-r02j}
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -k "tuned_partition or ieee8500 or fixture_solve" -x -q -p no:cacheprovider > gpurun_out/${TAG}_pytest.log 2>&1; tail -3 gpurun_out/${TAG}_pytest.log
+for r in 1 2; do
+  for t in 1 0; do
+    DOPF_NO_TUNE=$t DOPF_BENCH_NO_NCU=1 timeout 300 python bench.py --config ieee8500 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ab.log 2>gpurun_out/ab.err
+    python -c "import json;d=json.loads(open('gpurun_out/ab.log').read().strip().splitlines()[-1]);print('no_tune=$t', round(d['value'],1), round(d['roofline']['frac'],4), round(d['e2e']['value'],1), d['clocks']['sm_mhz'], d['setup'])" || tail -3 gpurun_out/ab.err
+  done
+done
