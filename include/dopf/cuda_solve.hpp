@@ -47,6 +47,10 @@ class Solver {
   /// Runs the loop on the device; record_iterates fills `snapshots` by
   /// re-running the deterministic device loop to every t (test use).
   SolveResult solve(const Settings& settings);
+  /// Setup-time tuning of the resident split for the uploaded model
+  /// (dopf_cuda_tune_partition): later solves and same-structure uploads use
+  /// it; iterates are unchanged. Returns the best measured seconds/iteration.
+  double tune_partition(const Settings& settings, int rounds = 8);
 
  private:
   struct Impl;

@@ -118,6 +118,16 @@ void Solver::upload(const DecomposedModel& model, int workers) {
   impl_->model = &model;
 }
 
+double Solver::tune_partition(const Settings& settings, int rounds) {
+  check_settings(settings);
+  if (!impl_->model) throw std::invalid_argument("no model uploaded");
+  const dopf_model_view view = impl_->flat.view(*impl_->model, &impl_->pre);
+  const dopf_settings cs = to_c(settings);
+  double per = 0;
+  impl_->check(dopf_cuda_tune_partition(impl_->ctx, &view, &cs, rounds, &per));
+  return per;
+}
+
 SolveResult Solver::solve(const Settings& settings) {
   check_settings(settings);
   if (!impl_->model) throw std::invalid_argument("no model uploaded");
