@@ -72,6 +72,13 @@ int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
  * receives the best measured period. */
 int dopf_cuda_tune_partition(dopf_cuda_ctx* ctx, const dopf_model_view* model, const dopf_settings* settings,
                              int32_t rounds, double* seconds_per_iteration);
+/* The same for scenario batches: tunes the split of one instance's G CTAs
+ * (shared by every scenario of this structure) on models[0, count) -- a
+ * sample; upload the whole batch afterwards: it keeps the tuned split. For
+ * these tight G-CTA instances a position's load (compute without the
+ * exchange) drives the shares. *seconds_per_iteration: per scenario-iteration. */
+int dopf_cuda_tune_partition_batch(dopf_cuda_ctx* ctx, const dopf_model_view* models, int32_t count,
+                                   const dopf_settings* settings, int32_t rounds, double* seconds_per_iteration);
 /* Parity mode (reference Settings::record_iterates, admm.cpp:228-229): the
  * same solve, with the state after every iteration t = 1 .. min(T, stop)
  * written by the device loop itself (one pass, not a re-run per t) and

@@ -29,6 +29,21 @@ class BatchSolver:
         self.models = list(models)
         self._views = views
 
+    def tune_partition(self, models: List[dopf.DecomposedModel], settings: dopf.Settings = None,
+                       rounds: int = 6) -> float:
+        """Setup-time tuning of one instance's CTA split on a sample of the
+        scenarios (dopf_cuda_tune_partition_batch); the next upload of this
+        structure keeps it. Returns seconds per scenario-iteration."""
+        for m in models:
+            if not m.has_precompute:
+                m.precompute()
+        views = (N.ModelView_t * len(models))(*[m.view() for m in models])
+        st = (settings or dopf.Settings()).to_c()
+        out = C.c_double(0.0)
+        self._s._err(self._s._lib.dopf_cuda_tune_partition_batch(self._s._h, views, len(models), C.byref(st),
+                                                                 rounds, C.byref(out)))
+        return out.value
+
     def info(self) -> dict:
         return self._s.info()
 

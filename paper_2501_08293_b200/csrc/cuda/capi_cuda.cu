@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <new>
 #include <stdexcept>
@@ -2095,82 +2096,126 @@ int dopf_layout_probe_batch(const dopf_model_view* ms, int32_t count, int64_t sm
   }
 }
 
+}  // extern "C"
+
+namespace {
+
+// Feedback tuning of the resident split (shared by the single-instance and
+// the batch entry points). `upload` re-plans with c->block_weights. Single
+// grid-wide instance: a CTA's slack is its wait at the iteration's final
+// barrier, and CTAs without slack give cost shares away. Cluster / group
+// instances (G <= 8 CTAs, all tight): a CTA position's load is its compute
+// time without the exchange, and loaded positions give shares away.
+double tune_split(dopf_cuda_ctx* c, const std::function<int()>& upload, const dopf_settings* s, int rounds) {
+  check_settings(s);
+  const bool grid = c->mode == SyncMode::grid;
+  const int I = static_cast<int>(c->L.inst.size());
+  const int G = c->L.blocks_per_instance;
+  const int nb = static_cast<int>(c->L.blocks.size());
+  const int K0 = c->L.K;
+  std::vector<double> w(G, 1.0), best_w, best_sig(G), best_ref(G);
+  double best = 1e300, beta = 0.5;
+  std::vector<long long> cyc(static_cast<std::size_t>(nb) * 8);
+  std::vector<dopf_result_view> res(I);
+  auto median = [](std::vector<double> x) {
+    std::nth_element(x.begin(), x.begin() + x.size() / 2, x.end());
+    return x[x.size() / 2];
+  };
+  for (int r = 0; r < rounds; ++r) {
+    c->block_weights = w;
+    bool ok = true;
+    try {
+      c->plan.reset();  // re-plan with these shares
+      c->batch_plan.reset();
+      if (upload() != DOPF_OK) throw std::invalid_argument(c->err);
+      ok = !c->streaming && c->L.K == K0 && c->L.all_ops_in_smem && c->L.blocks_per_instance == G &&
+           static_cast<int>(c->L.blocks.size()) == nb;
+    } catch (const std::invalid_argument&) {
+      ok = false;
+    }
+    double per = 1e300;
+    if (ok) {
+      for (int q = 0; q < 3; ++q) {  // best of three plain runs: kernel time per (instance-)iteration
+        for (auto& v : res) v = dopf_result_view{};
+        run(c, s, res.data(), I, false);
+        long long its = 0;
+        for (const auto& v : res) its += std::max(1, v.iterations);
+        per = std::min(per, c->last_kernel_s / static_cast<double>(its));
+      }
+    }
+    if (ok && per < best) {
+      best = per;
+      best_w = w;
+      if (c->d_prof) ck(cudaMemset(c->d_prof, 0, c->prof_cap * sizeof(long long)), "memset");
+      c->profiling = true;
+      for (auto& v : res) v = dopf_result_view{};
+      run(c, s, res.data(), I, false);
+      c->profiling = false;
+      ck(cudaMemcpy(cyc.data(), c->d_prof, cyc.size() * sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
+      std::vector<double> sig(G, 0.0), ref(G, 0.0);
+      for (int blk = 0; blk < nb; ++blk) {
+        const long long* ph = cyc.data() + static_cast<std::size_t>(blk) * 8;
+        const double it = std::max(1, res[blk / G].iterations);
+        if (grid) {
+          sig[blk % G] += static_cast<double>(ph[4]) / it;                                // slack
+          ref[blk % G] += static_cast<double>(ph[0] + ph[1] + ph[2] + ph[3] + ph[5]) / it;  // busy
+        } else {
+          sig[blk % G] += static_cast<double>(ph[0] + ph[1] + ph[2] + ph[3]) / it;  // load
+          ref[blk % G] = sig[blk % G];
+        }
+      }
+      best_sig = sig;
+      best_ref = ref;
+    } else {
+      beta *= 0.5;  // rejected: a smaller step from the best split
+    }
+    if (best_w.empty()) break;
+    const double ms = median(best_sig), mr = std::max(1e-9, median(best_ref));
+    double sum = 0;
+    for (int g = 0; g < G; ++g) {
+      const double d = (best_sig[g] - ms) / mr;
+      w[g] = best_w[g] * (1.0 + (grid ? beta : -beta) * d);
+      w[g] = std::min(1.5, std::max(0.5, w[g]));
+      sum += w[g];
+    }
+    for (double& x : w) x *= G / sum;
+  }
+  if (best_w.empty()) best_w.assign(G, 1.0);
+  c->block_weights = best_w;
+  c->plan.reset();
+  c->batch_plan.reset();
+  if (upload() != DOPF_OK) throw std::runtime_error(c->err);
+  return best;
+}
+
+}  // namespace
+
+extern "C" {
+
 int dopf_cuda_tune_partition(dopf_cuda_ctx* c, const dopf_model_view* m, const dopf_settings* s,
                              int32_t rounds, double* seconds_per_iteration) {
   if (!c || !m || !s || rounds < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  if (seconds_per_iteration) *seconds_per_iteration = 0;
   int rc = dopf_cuda_upload(c, m);
   if (rc != DOPF_OK) return rc;
-  if (c->streaming || c->mode != SyncMode::grid || c->L.inst.size() != 1) {
-    if (seconds_per_iteration) *seconds_per_iteration = 0;
-    return DOPF_OK;  // only a grid-wide single instance has a split to tune
-  }
-  rc = guarded(c, [&] {
-    check_settings(s);
-    const int G = static_cast<int>(c->L.blocks.size());
-    const int K0 = c->L.K;
-    std::vector<double> w(G, 1.0), best_w, best_wait(G), best_busy(G);
-    double best = 1e300, beta = 0.5;
-    std::vector<long long> cyc(static_cast<std::size_t>(G) * 8);
-    auto median = [](std::vector<double> x) {
-      std::nth_element(x.begin(), x.begin() + x.size() / 2, x.end());
-      return x[x.size() / 2];
-    };
-    for (int r = 0; r < rounds; ++r) {
-      c->block_weights = w;
-      bool ok = true;
-      try {
-        c->plan.reset();  // re-plan with these shares
-        if (dopf_cuda_upload(c, m) != DOPF_OK) throw std::invalid_argument(c->err);
-        ok = !c->streaming && c->mode == SyncMode::grid && c->L.K == K0 && c->L.all_ops_in_smem &&
-             static_cast<int>(c->L.blocks.size()) == G;
-      } catch (const std::invalid_argument&) {
-        ok = false;
-      }
-      double per = 1e300;
-      if (ok) {
-        dopf_result_view v{};
-        for (int q = 0; q < 3; ++q) {  // best of three plain runs
-          run(c, s, &v, 1, false);
-          per = std::min(per, c->last_kernel_s / std::max(1, v.iterations));
-        }
-      }
-      if (ok && per < best) {
-        best = per;
-        best_w = w;
-        // slack of every CTA at the iteration's final barrier (phase clock)
-        if (c->d_prof) ck(cudaMemset(c->d_prof, 0, c->prof_cap * sizeof(long long)), "memset");
-        c->profiling = true;
-        dopf_result_view v{};
-        run(c, s, &v, 1, false);
-        c->profiling = false;
-        ck(cudaMemcpy(cyc.data(), c->d_prof, cyc.size() * sizeof(long long), cudaMemcpyDeviceToHost), "d2h");
-        for (int g = 0; g < G; ++g) {
-          const long long* ph = cyc.data() + static_cast<std::size_t>(g) * 8;
-          best_wait[g] = static_cast<double>(ph[4]);
-          best_busy[g] = static_cast<double>(ph[0] + ph[1] + ph[2] + ph[3] + ph[5]);
-        }
-      } else {
-        beta *= 0.5;  // rejected: a smaller step from the best split
-      }
-      if (best_w.empty()) break;
-      // CTAs without slack (the critical region) give cost shares away
-      const double mw = median(best_wait), mb = std::max(1.0, median(best_busy));
-      double sum = 0;
-      for (int g = 0; g < G; ++g) {
-        w[g] = best_w[g] * (1.0 + beta * (best_wait[g] - mw) / mb);
-        w[g] = std::min(1.5, std::max(0.5, w[g]));
-        sum += w[g];
-      }
-      for (double& x : w) x *= G / sum;
-    }
-    if (best_w.empty()) best_w.assign(G, 1.0);
-    c->block_weights = best_w;
-    c->plan.reset();
-    const int u = dopf_cuda_upload(c, m);
-    if (u != DOPF_OK) throw std::runtime_error(c->err);
-    if (seconds_per_iteration) *seconds_per_iteration = best;
+  if (c->streaming || c->L.inst.size() != 1 || c->L.blocks_per_instance < 2) return DOPF_OK;  // nothing to split
+  return guarded(c, [&] {
+    const double per = tune_split(c, [&] { return dopf_cuda_upload(c, m); }, s, rounds);
+    if (seconds_per_iteration) *seconds_per_iteration = per;
   });
-  return rc;
+}
+
+int dopf_cuda_tune_partition_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, int32_t count,
+                                   const dopf_settings* s, int32_t rounds, double* seconds_per_iteration) {
+  if (!c || !ms || count < 1 || !s || rounds < 1) return DOPF_ERR_INVALID_ARGUMENT;
+  if (seconds_per_iteration) *seconds_per_iteration = 0;
+  int rc = dopf_cuda_upload_batch(c, ms, count);
+  if (rc != DOPF_OK) return rc;
+  if (c->L.blocks_per_instance < 2) return DOPF_OK;
+  return guarded(c, [&] {
+    const double per = tune_split(c, [&] { return dopf_cuda_upload_batch(c, ms, count); }, s, rounds);
+    if (seconds_per_iteration) *seconds_per_iteration = per;
+  });
 }
 
 int dopf_cuda_set_profiling(dopf_cuda_ctx* c, int32_t on) {

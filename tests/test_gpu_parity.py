@@ -282,6 +282,30 @@ def test_batch_persistent_groups_several_instances_per_group_bitwise():
         assert_same(gpu, ref, bitwise=True)
 
 
+@pytest.mark.timeout(600)
+def test_tuned_batch_split_keeps_iterates_bitwise():
+    """A batch split tuned on a scenario sample (dopf_cuda_tune_partition_batch)
+    and a tuned 4-CTA single IEEE-123 instance: every scenario still bitwise
+    equal to the oracle."""
+    import concurrent.futures as cf
+    import os
+    from paper_2501_08293_b200 import scenarios
+    from paper_2501_08293_b200.batch import BatchSolver
+    models = scenarios.build_scenarios("ieee123", 123, range(60))
+    bs = BatchSolver(0)
+    bs.tune_partition(models[:20], dopf.Settings(), rounds=4)
+    bs.upload(models)
+    results = bs.solve(dopf.Settings())
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        refs = list(ex.map(lambda m: O.solve(m, dopf.Settings(workers=1)), models))
+    for gpu, ref in zip(results, refs):
+        assert_same(gpu, ref, bitwise=True)
+    s = dopf.CudaSolver(0)
+    s.tune_partition(models[0], dopf.Settings(), rounds=4)
+    assert s.info()["sync"] == "cluster"
+    assert_same(s.solve(dopf.Settings()), refs[0], bitwise=True)
+
+
 # ------------------------------------------------------------ HBM-streaming path
 
 
