@@ -495,7 +495,7 @@ def main():
             if upload() != 0:
                 raise RuntimeError(lib.dopf_cuda_last_error(solver._h).decode())
         else:
-            tuned_period = solver.tune_partition(models[0], settings, rounds=8) or None
+            tuned_period = solver.tune_partition(models[0], settings, rounds=12) or None
     info = solver.info()
     b_iter = solver.bytes_per_iteration() / len(models)   # one instance
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{device}")  # 256 MiB
@@ -638,7 +638,7 @@ def main():
                                   "operators are streamed from HBM every iteration")},
             "setup": {"partition": ("load-tuned CTA split of each scenario (dopf_cuda_tune_partition_batch on 74 "
                                     "scenarios, 6 rounds, untimed setup)" if batch else
-                                    "slack-tuned (dopf_cuda_tune_partition, 8 rounds, untimed setup)")
+                                    "slack-tuned (dopf_cuda_tune_partition, 12 rounds, untimed setup)")
                       if tuned_period else "default cost split"},
             "kernel": {"name": "admm_persistent" if info["sync"] != "stream-graph"
                        else "k_global+k_staged(+k_local), last chunk CTA folds + decides (graph while-node)",
