@@ -72,6 +72,11 @@ int dopf_cuda_info(const dopf_cuda_ctx* ctx, dopf_cuda_info_t* out);
  * receives the best measured period. */
 int dopf_cuda_tune_partition(dopf_cuda_ctx* ctx, const dopf_model_view* model, const dopf_settings* settings,
                              int32_t rounds, double* seconds_per_iteration);
+/* The context's tuned cost shares (copied into out[0, min(count, cap)));
+ * returns their count (0: default split). Feeding them back through
+ * DOPF_BLOCK_WEIGHTS (comma-separated) reproduces the split in another
+ * process (profilers). */
+int dopf_cuda_block_weights(const dopf_cuda_ctx* ctx, double* out, int32_t cap);
 /* The same for scenario batches: tunes the split of one instance's G CTAs
  * (shared by every scenario of this structure) on models[0, count) -- a
  * sample; upload the whole batch afterwards: it keeps the tuned split. For

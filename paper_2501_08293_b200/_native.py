@@ -178,6 +178,7 @@ def cuda() -> C.CDLL:
     _sig(lib, "dopf_cuda_phase_cycles", C.c_int, vp, P(i64), i32)
     _sig(lib, "dopf_cuda_block_stats", C.c_int, vp, P(i64), i32)
     _sig(lib, "dopf_cuda_tune_partition", C.c_int, vp, P(ModelView_t), P(Settings_t), i32, P(f64))
+    _sig(lib, "dopf_cuda_block_weights", C.c_int, vp, P(f64), i32)
     _sig(lib, "dopf_cuda_tune_partition_batch", C.c_int, vp, P(ModelView_t), i32, P(Settings_t), i32, P(f64))
     _sig(lib, "dopf_layout_probe", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))
     _sig(lib, "dopf_layout_probe_batch", C.c_int, P(ModelView_t), i32, i64, P(LayoutStats_t))

@@ -2193,6 +2193,13 @@ double tune_split(dopf_cuda_ctx* c, const std::function<int()>& upload, const do
 
 extern "C" {
 
+int dopf_cuda_block_weights(const dopf_cuda_ctx* c, double* out, int32_t cap) {
+  if (!c || (cap > 0 && !out)) return -1;
+  const int n = static_cast<int>(c->block_weights.size());
+  for (int i = 0; i < std::min(n, cap); ++i) out[i] = c->block_weights[i];
+  return n;
+}
+
 int dopf_cuda_tune_partition(dopf_cuda_ctx* c, const dopf_model_view* m, const dopf_settings* s,
                              int32_t rounds, double* seconds_per_iteration) {
   if (!c || !m || !s || rounds < 1) return DOPF_ERR_INVALID_ARGUMENT;

@@ -20,6 +20,15 @@ f = dopf.synthetic_feeder(shape, seed)
 _, _, model = dopf.load_model(f, workers=os.cpu_count() or 1)
 model.precompute(os.cpu_count() or 1)
 s = dopf.CudaSolver(0)
+if os.environ.get("DOPF_TUNE") == "1":
+    # the bench's slack-tuned split, exported for a profiler run of this tool
+    # with DOPF_BLOCK_WEIGHTS=<the printed shares> (no tuning launches there)
+    import ctypes as C
+    s.tune_partition(model, dopf.Settings(), rounds=12)
+    w = (C.c_double * 4096)()
+    n = s._lib.dopf_cuda_block_weights(s._h, w, 4096)
+    print("DOPF_BLOCK_WEIGHTS=" + ",".join(f"{w[i]:.9f}" for i in range(n)))
+    sys.exit(0)
 s.upload(model)
 for _ in range(solves):
     r = s.solve(dopf.Settings(), outputs=False)
