@@ -91,6 +91,7 @@ struct dopf_cuda_ctx {
   int path_request = 0;      // 0 auto, 1 resident persistent kernel, 2 streaming graph
   double* snap_dev = nullptr;  // parity mode: per-iteration snapshots of the next resident run (slot 118)
   std::vector<double> block_weights;  // tuned cost shares of the resident split (dopf_cuda_tune_partition)
+  uint64_t weights_sig = 0;           // structure they were tuned for (0: any)
   int snap_iters = 0;
   bool streaming = false;    // path of the uploaded model
   StreamLayout SL;
@@ -357,6 +358,22 @@ LayoutOptions options_for(const dopf_cuda_ctx* c) {
     }
   }
   return o;
+}
+
+// FNV-1a over a model's structure (sizes, z_offsets, l2g): tuned split shares
+// only apply to the structure they were measured on.
+uint64_t structure_sig(const dopf_model_view& m) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* p, std::size_t bytes) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (std::size_t i = 0; i < bytes; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  mix(&m.S, sizeof m.S);
+  mix(&m.n, sizeof m.n);
+  mix(&m.N_z, sizeof m.N_z);
+  if (m.S > 0 && m.z_offsets) mix(m.z_offsets, (m.S + 1) * sizeof(int32_t));
+  if (m.N_z > 0 && m.l2g) mix(m.l2g, m.N_z * sizeof(int32_t));
+  return h | 1ull;  // never 0
 }
 
 // Limits of the resident kernel a single-instance plan must meet (the same
@@ -1129,6 +1146,10 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
   if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     c->uploaded = false;
+    if (!c->block_weights.empty() && c->weights_sig && c->weights_sig != structure_sig(*m)) {
+      c->block_weights.clear();  // tuned for another structure
+      c->weights_sig = 0;
+    }
     const LayoutOptions opt = options_for(c);
     if (!m->has_pre) throw std::invalid_argument("model view lacks precomputed operators");
     c->streaming = c->path_request == 2 || (c->path_request == 0 && needs_streaming(*m, opt));
@@ -2208,7 +2229,9 @@ int dopf_cuda_tune_partition(dopf_cuda_ctx* c, const dopf_model_view* m, const d
   if (rc != DOPF_OK) return rc;
   if (c->streaming || c->L.inst.size() != 1 || c->L.blocks_per_instance < 2) return DOPF_OK;  // nothing to split
   return guarded(c, [&] {
+    c->weights_sig = 0;  // tuning re-plans this very structure
     const double per = tune_split(c, [&] { return dopf_cuda_upload(c, m); }, s, rounds);
+    c->weights_sig = structure_sig(*m);
     if (seconds_per_iteration) *seconds_per_iteration = per;
   });
 }
@@ -2222,6 +2245,7 @@ int dopf_cuda_tune_partition_batch(dopf_cuda_ctx* c, const dopf_model_view* ms, 
   if (c->L.blocks_per_instance < 2) return DOPF_OK;
   return guarded(c, [&] {
     const double per = tune_split(c, [&] { return dopf_cuda_upload_batch(c, ms, count); }, s, rounds);
+    c->weights_sig = 0;  // per-instance shares (size G): applied to batches of any structure with G CTAs
     if (seconds_per_iteration) *seconds_per_iteration = per;
   });
 }

@@ -215,6 +215,16 @@ def test_tuned_partition_keeps_iterates_bitwise():
     assert per * gpu.iterations <= base * 1.02
     s.upload(model)  # a same-structure re-upload keeps the tuned split
     assert_same(s.solve(dopf.Settings()), ref, bitwise=True)
+    import ctypes as C
+    w = (C.c_double * 256)()
+    assert s._lib.dopf_cuda_block_weights(s._h, w, 256) == s.info()["blocks"]
+    # another structure on the same context: the shares tuned for IEEE-8500 are dropped
+    _, _, other = dopf.load_model(dopf.synthetic_feeder("ieee8500", 8501), workers=8)
+    other.precompute(8)
+    s.upload(other)
+    assert s._lib.dopf_cuda_block_weights(s._h, w, 256) == 0
+    assert_same(s.solve(dopf.Settings(max_iter=200)), O.solve(other, dopf.Settings(max_iter=200, workers=8)),
+                bitwise=True)
 
 
 @pytest.mark.timeout(600)
