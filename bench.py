@@ -302,8 +302,17 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def upload_bytes(models) -> int:
-    """Bytes dopf_cuda_upload copies host -> device (the device layout)."""
+def upload_bytes(models, batch: bool = False) -> int:
+    """Bytes the per-step upload copies host -> device. A single model after
+    its first upload takes the same-structure path: the raw value arrays only
+    (P, A, b, v, z0, c, 1/copies, lo, hi), scattered on the device. A batch
+    upload copies its device layout (estimated from the model sizes)."""
+    if not batch:
+        tot = 0
+        for model in models:
+            st = model.stats()
+            tot += 8 * (st["sum_n2"] + st["sum_mn"] + st["sum_m"] + 2 * st["N_z"] + 4 * st["n"])
+        return int(tot)
     tot = 0
     for model in models:
         st = model.stats()
@@ -581,7 +590,7 @@ def main():
         if step > 0:  # first pass warms the host allocator
             e2e_t += dt
             e2e_it += sum(rs[i].iterations for i in range(K))
-    h2d = upload_bytes(models)
+    h2d = upload_bytes(models, batch)
     d2h = sum(8 * (m.view().n + 2 * m.view().N_z) + 32 for m in models) + 48 * int(np.mean(iters))
     e2e_value = e2e_it / e2e_t
     if world > 1:
