@@ -360,13 +360,13 @@ LayoutOptions options_for(const dopf_cuda_ctx* c) {
   return o;
 }
 
-// FNV-1a over a model's structure (sizes, z_offsets, l2g): tuned split shares
+// FNV-1a (32-bit words) over a model's structure (sizes, z_offsets, l2g): tuned split shares
 // only apply to the structure they were measured on.
 uint64_t structure_sig(const dopf_model_view& m) {
   uint64_t h = 1469598103934665603ull;
-  auto mix = [&](const void* p, std::size_t bytes) {
-    const unsigned char* b = static_cast<const unsigned char*>(p);
-    for (std::size_t i = 0; i < bytes; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  auto mix = [&](const void* p, std::size_t bytes) {  // 32-bit words (all inputs are int32 arrays)
+    const uint32_t* w = static_cast<const uint32_t*>(p);
+    for (std::size_t i = 0; i < bytes / 4; ++i) h = (h ^ w[i]) * 1099511628211ull;
   };
   mix(&m.S, sizeof m.S);
   mix(&m.n, sizeof m.n);
@@ -1146,8 +1146,11 @@ int dopf_cuda_upload(dopf_cuda_ctx* c, const dopf_model_view* m) {
   if (!c || !m) return DOPF_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     c->uploaded = false;
-    if (!c->block_weights.empty() && c->weights_sig && c->weights_sig != structure_sig(*m)) {
-      c->block_weights.clear();  // tuned for another structure
+    // shares tuned for another structure do not apply (the cheap plan
+    // comparison first: the common re-upload of the same model skips the hash)
+    if (!c->block_weights.empty() && c->weights_sig &&
+        !(c->plan && c->plan->same_structure(*m, options_for(c))) && c->weights_sig != structure_sig(*m)) {
+      c->block_weights.clear();
       c->weights_sig = 0;
     }
     const LayoutOptions opt = options_for(c);
