@@ -65,7 +65,7 @@ def _raise(code: int, msg: str):
     raise RuntimeError(msg)
 
 
-def _release(obj, free_name: str) -> None:
+def _release(obj, free_name: str, _native=N) -> None:
     """Frees a native handle once. Safe during interpreter shutdown, when
     module globals (the native library bindings) may already be gone."""
     h = getattr(obj, "_h", None)
@@ -73,7 +73,7 @@ def _release(obj, free_name: str) -> None:
     if h is None or not h.value:
         return
     try:
-        getattr(N.host(), free_name)(h)
+        getattr(_native.host(), free_name)(h)
     except Exception:  # shutdown: the process is exiting, the OS reclaims it
         pass
 
@@ -99,8 +99,8 @@ class Feeder:
     def __init__(self, handle: int):
         self._h = C.c_void_p(handle)
 
-    def __del__(self):
-        _release(self, "dopf_feeder_free")
+    def __del__(self, _rel=_release):  # bound at definition: module globals are gone at shutdown
+        _rel(self, "dopf_feeder_free")
 
     @property
     def handle(self):
@@ -185,8 +185,8 @@ class LinearSystem:
         self._v = v
         self.rows, self.cols, self.nnz = v.rows, v.cols, v.nnz
 
-    def __del__(self):
-        _release(self, "dopf_lp_free")
+    def __del__(self, _rel=_release):  # bound at definition: module globals are gone at shutdown
+        _rel(self, "dopf_lp_free")
 
     @property
     def handle(self):
@@ -315,8 +315,8 @@ class DecomposedModel:
         self._h = C.c_void_p(handle)
         self._view: Optional[N.ModelView_t] = None
 
-    def __del__(self):
-        _release(self, "dopf_model_free")
+    def __del__(self, _rel=_release):  # bound at definition: module globals are gone at shutdown
+        _rel(self, "dopf_model_free")
 
     @property
     def handle(self):
