@@ -51,6 +51,8 @@ class Solver {
   /// (dopf_cuda_tune_partition): later solves and same-structure uploads use
   /// it; iterates are unchanged. Returns the best measured seconds/iteration.
   double tune_partition(const Settings& settings, int rounds = 8);
+  /// The underlying C-ABI context (diagnostics, dopf_cuda_* calls).
+  dopf_cuda_ctx* context() const;
 
  private:
   struct Impl;

@@ -245,15 +245,18 @@ def test_ieee8500_full_solve_bitwise(solver):
     assert np.array_equal(again.trace, gpu.trace)
 
 
-def test_cpp_dropin_program():
-    """Reference-style C++ caller of dopf::solve linked against libdopf_cuda.so."""
+@pytest.mark.parametrize("tune", ["0", "1"])
+def test_cpp_dropin_program(tune):
+    """Reference-style C++ caller of dopf::solve linked against libdopf_cuda.so
+    (DOPF_TUNE=1: the drop-in also tunes the split on its first call per
+    structure; the program's bitwise checks must hold either way)."""
     import os
     import subprocess
 
     from conftest import ROOT
     from paper_2501_08293_b200 import build
     proc = subprocess.run([build.DROPIN_TEST, os.path.join(ROOT, "tests", "golden", "fixtures")],
-                          capture_output=True, text=True, timeout=600)
+                          capture_output=True, text=True, timeout=600, env={**os.environ, "DOPF_TUNE": tune})
     assert proc.returncode == 0, proc.stdout + proc.stderr
     assert "PASS" in proc.stdout
 
