@@ -647,7 +647,8 @@ def main():
                                   "operators are streamed from HBM every iteration")},
             "setup": {"partition": ("load-tuned CTA split of each scenario (dopf_cuda_tune_partition_batch on 74 "
                                     "scenarios, 6 rounds, untimed setup)" if batch else
-                                    "slack-tuned (dopf_cuda_tune_partition, 12 rounds, untimed setup)")
+                                    "tuned CTA split (dopf_cuda_tune_partition, 12 rounds, untimed setup; slack signal for grid-wide "
+                                    "instances, load signal for cluster instances)")
                       if tuned_period else "default cost split"},
             "kernel": {"name": "admm_persistent" if info["sync"] != "stream-graph"
                        else "k_global+k_staged(+k_local), last chunk CTA folds + decides (graph while-node)",
