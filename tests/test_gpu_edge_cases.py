@@ -223,3 +223,33 @@ def test_tiled_feeder_beyond_85_tiles_bitwise():
     st = dopf.Settings(max_iter=12)
     ref = O.solve(model, dopf.Settings(max_iter=12, workers=os.cpu_count() or 1))
     assert_same(s.solve(st), ref, bitwise=True)
+
+
+def test_block_stats_describe_the_resident_layout():
+    """dopf_cuda_block_stats (load-balance diagnostics) agrees with the model:
+    every row in exactly one block, sums of n_s over rows = sum n_s^2."""
+    f = dopf.synthetic_feeder("ieee123", 123)
+    _, _, m = dopf.load_model(f, workers=4)
+    m.precompute(4)
+    s = dopf.CudaSolver(0)
+    s.upload(m)
+    G = s.info()["blocks"]
+    out = (N.i64 * (12 * G))()
+    assert s._lib.dopf_cuda_block_stats(s._h, out, G) == 0
+    st = np.array(out[:], dtype=np.int64).reshape(G, 12)
+    ns = np.diff(m.z_offsets)
+    assert st[:, 0].sum() == m.total_local_vars            # rows
+    assert st[:, 11].sum() == int((ns.astype(np.int64) ** 2).sum())  # sum of n_s over rows
+    assert (st[:, 10] >= 1).all()                             # longest per-thread chain
+
+
+def test_tuning_is_a_noop_off_the_resident_path():
+    """Split tuning on a streaming upload leaves the model untouched (0 returned)."""
+    _, _, m = dopf.load_model(fixture_path("four_bus_delta"))
+    m.precompute()
+    s = dopf.CudaSolver(0)
+    s.set_path("stream")
+    assert s.tune_partition(m, dopf.Settings(), rounds=3) == 0.0
+    assert s.info()["sync"] == "stream-graph"
+    st = dopf.Settings(eps_rel=1e-4)
+    assert_same(s.solve(st), O.solve(m, st), bitwise=True)
