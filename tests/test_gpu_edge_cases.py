@@ -253,3 +253,26 @@ def test_tuning_is_a_noop_off_the_resident_path():
     assert s.info()["sync"] == "stream-graph"
     st = dopf.Settings(eps_rel=1e-4)
     assert_same(s.solve(st), O.solve(m, st), bitwise=True)
+
+
+@pytest.mark.parametrize("seed", range(100, 112))
+def test_random_radial_feeders_bitwise_both_paths(seed):
+    """Random radial feeders (tests/feeder_gen.py, the ranges of the reference's
+    test_util.hpp:77-172, 20-60 buses) through the whole pipeline and both
+    device paths: iterations, status, x / z / lambda, infeasibility and near-tie
+    counters identical to the oracle. Infeasible draws (a legitimate outcome,
+    test_decompose.cpp:319-323) are skipped."""
+    from feeder_gen import random_feeder
+    f = dopf.parse_feeder(random_feeder(seed, n_buses=20 + (seed % 5) * 10))
+    try:
+        _, _, m = dopf.load_model(f)
+        m.precompute()
+    except (dopf.InfeasibleSubsystemError, dopf.SingularSubsystemError):
+        pytest.skip("infeasible / singular draw")
+    st = dopf.Settings(eps_rel=1e-4, max_iter=3000)
+    ref = O.solve(m, st)
+    for path in ("resident", "stream"):
+        s = dopf.CudaSolver(0)
+        s.set_path(path)
+        s.upload(m)
+        assert_same(s.solve(st), ref, bitwise=True)
