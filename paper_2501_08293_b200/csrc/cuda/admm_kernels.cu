@@ -498,7 +498,9 @@ __device__ __forceinline__ void solve_block(const KernelParams& p, const int blk
       const int c = ctid + k * kCW;
       cpk[k] = c < bd.cols_int ? pack_col(c) : 0u;
     }
-    const int cb = bd.cols_int + ctid;
+    // boundary columns spread over the compute warps (lane-major): each warp
+    // polls a few neighbours' records instead of three warps polling all
+    const int cb = bd.cols_int + (ctid & 31) * (kCW / 32) + (ctid >> 5);
     const uint32_t cpkb = cb < bd.cols ? pack_col(cb) : 0u;
 
     auto row_n = [](uint32_t v) { return static_cast<int>(v & 0x7fu); };
